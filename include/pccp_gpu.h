@@ -16,8 +16,9 @@
  *   pccp_gpu_enumerate        (new: all-solutions counting; the reference has only
  *                              branch-and-bound, solver.cpp:122-146 gives the DFS order)
  *   pccp_gpu_solve            solve_parallel / solve_dfs        solver.hpp:105-128, solver.cpp:229-283
- *   pccp_gpu_decompose        eps_decompose                     solver.hpp:115-119, solver.cpp:180-227
- *   pccp_gpu_branch           branch                            solver.hpp:99-100,  solver.cpp:19-47
+ *                             (its EPS phase restates eps_decompose, solver.cpp:180-227,
+ *                              and every node runs branch, solver.cpp:19-47, on the device)
+ *   pccp_gpu_replay           materialize                       solver.cpp:91-102
  *
  * Return codes: PCCP_OK, PCCP_EMODEL (ModelError/SchemaError/CompileError,
  * lattice.hpp:24-32), PCCP_ECUDA, PCCP_ELIMIT, PCCP_EARG.  The message of the

@@ -1,0 +1,623 @@
+// engine.cu — host side of the B200 engine: contexts, launch planning, the
+// EPS driver and the C ABI of include/pccp_gpu.h.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <chrono>
+#include <cmath>
+#include <cstddef>
+#include <cstdlib>
+#include <cstring>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "../../../include/pccp_gpu.h"
+#include "search.cuh"
+
+using namespace pccp_b200;
+
+namespace {
+
+thread_local std::string g_err;
+
+struct CudaError : std::runtime_error {
+  using std::runtime_error::runtime_error;
+};
+struct LimitError : std::runtime_error {
+  using std::runtime_error::runtime_error;
+};
+struct ArgError : std::runtime_error {
+  using std::runtime_error::runtime_error;
+};
+
+#define CK(x)                                                                                     \
+  do {                                                                                            \
+    const cudaError_t e_ = (x);                                                                   \
+    if (e_ != cudaSuccess) throw CudaError(std::string(#x) + ": " + cudaGetErrorString(e_));      \
+  } while (0)
+
+template <class F>
+int api(F&& f) {
+  try {
+    return f();
+  } catch (const CudaError& e) {
+    g_err = e.what();
+    return PCCP_ECUDA;
+  } catch (const LimitError& e) {
+    g_err = e.what();
+    return PCCP_ELIMIT;
+  } catch (const ArgError& e) {
+    g_err = e.what();
+    return PCCP_EARG;
+  } catch (const std::exception& e) {
+    g_err = e.what();
+    return PCCP_EMODEL;
+  }
+}
+
+template <class T>
+struct DBuf {
+  T* p = nullptr;
+  size_t n = 0;
+  void ensure(size_t k) {
+    if (k <= n && p) return;
+    release();
+    k = std::max<size_t>(k, 1);
+    if (cudaMalloc(&p, k * sizeof(T)) != cudaSuccess) {
+      cudaGetLastError();
+      p = nullptr;
+      n = 0;
+      throw LimitError("device allocation of " + std::to_string(k * sizeof(T)) + " bytes failed");
+    }
+    n = k;
+  }
+  void release() {
+    if (p) cudaFree(p);
+    p = nullptr;
+    n = 0;
+  }
+};
+
+std::uint32_t align4(std::uint32_t x) { return (x + 3u) & ~3u; }
+
+double now_ms() {
+  return std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now().time_since_epoch()).count();
+}
+
+}  // namespace
+
+struct pccp_gpu_ctx {
+  pccp_gpu_cfg cfg{};
+  int device = 0;
+  int n_sm = 0;
+  size_t smem_optin = 0;
+  cudaStream_t stream = nullptr;
+  cudaEvent_t ev[4] = {};
+  bool loaded = false;
+
+  Lowered low;
+  std::vector<std::uint8_t> slot_kind;
+  std::vector<std::uint32_t> slot_word;
+  pccp_model view{};  // host copy of the slot tables (commands not kept)
+  DBuf<int> blob;
+
+  // launch plan
+  bool warp = true;
+  int block = 256;
+  int gpc = 8;  // groups per CTA
+  int ctas = 0;
+  size_t smem = 0;
+  int store_stride = 4;
+  int table_in_smem = 0;
+
+  DBuf<int> fa, fb, ia, ib, stack, best, io;
+  DBuf<unsigned char> flags, st;
+  DBuf<unsigned> rnd;
+  dev::Globals* G = nullptr;
+  int* d_count = nullptr;
+  std::vector<void*> opened;
+  DBuf<int*> d_peers;
+  int n_peers = 0;
+  std::uint64_t launches = 0;
+
+  int groups() const { return ctas * (warp ? gpc : 1); }
+
+  dev::Model model() const {
+    dev::Model M;
+    M.L = low.L;
+    M.blob = blob.p;
+    M.table_in_smem = table_in_smem;
+    M.store_stride = store_stride;
+    return M;
+  }
+};
+
+namespace {
+
+template <class Gp>
+void set_smem_attrs(size_t smem) {
+  CK(cudaFuncSetAttribute(dev::k_propagate<Gp>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  CK(cudaFuncSetAttribute(dev::k_root<Gp>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  CK(cudaFuncSetAttribute(dev::k_expand<Gp>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  CK(cudaFuncSetAttribute(dev::k_search<Gp>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+}
+
+template <class Gp>
+int occupancy(int block, size_t smem) {
+  int occ = 0;
+  CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, dev::k_search<Gp>, block, smem));
+  return occ;
+}
+
+void plan(pccp_gpu_ctx* c) {
+  const DeviceLayout& L = c->low.L;
+  c->store_stride = (int)align4(std::max<std::uint32_t>(L.n_words, 1));
+  const int gt = c->cfg.group_threads;
+  c->warp = gt == 32 || (gt == 0 && L.n_words <= 256);
+  if (c->warp) {
+    c->gpc = c->cfg.groups_per_cta > 0 ? std::min(c->cfg.groups_per_cta, 32) : 8;
+    c->block = 32 * c->gpc;
+  } else {
+    int t = gt;
+    if (t <= 0) {
+      t = 128;
+      while (t < 1024 && (std::uint32_t)(2 * t) <= L.n_ref_cmds / 16) t *= 2;
+    }
+    if (t < 64 || t > 1024 || (t & 31)) throw ArgError("group_threads must be 32 or a multiple of 32 in [64, 1024]");
+    c->gpc = 1;
+    c->block = t;
+  }
+  const size_t base = 72 * 4 + (size_t)(c->warp ? c->gpc : 1) * c->store_stride * 4;
+  const size_t table = (size_t)align4(L.blob_words) * 4;
+  if (base > c->smem_optin) throw LimitError("store of " + std::to_string(L.n_words) + " words exceeds shared memory");
+  const char* env = std::getenv("PCCP_TABLE_SMEM");
+  bool in_smem = base + table <= 100 * 1024;
+  if (env) in_smem = std::atoi(env) != 0 && base + table <= c->smem_optin;
+  c->table_in_smem = in_smem ? 1 : 0;
+  c->smem = base + (in_smem ? table : 0);
+  int occ;
+  if (c->warp) {
+    set_smem_attrs<dev::WarpGroup>(c->smem);
+    occ = occupancy<dev::WarpGroup>(c->block, c->smem);
+  } else {
+    set_smem_attrs<dev::CtaGroup>(c->smem);
+    occ = occupancy<dev::CtaGroup>(c->block, c->smem);
+  }
+  if (occ < 1) throw LimitError("kernel does not fit on an SM (smem " + std::to_string(c->smem) + " B)");
+  if (c->cfg.ctas_per_sm > 0) occ = std::min(occ, c->cfg.ctas_per_sm);
+  c->ctas = c->n_sm * occ;
+}
+
+void reset_globals(pccp_gpu_ctx* c, const pccp_limits* lim) {
+  dev::Globals h;
+  std::memset(&h, 0, sizeof(h));
+  h.incumbent = INT32_MAX;
+  h.best_value = INT32_MAX;
+  h.node_limit = lim ? lim->node_limit : ~0ull;
+  h.timeout_ns = (lim && lim->timeout_s > 0) ? (unsigned long long)(lim->timeout_s * 1e9) : 0ull;
+  CK(cudaMemcpyAsync(c->G, &h, sizeof(h), cudaMemcpyHostToDevice, c->stream));
+  dev::k_init_clock<<<1, 1, 0, c->stream>>>(c->G);
+  CK(cudaGetLastError());
+  ++c->launches;
+}
+
+// Depth bound for the DFS stacks: a variable of width w can be bisected at
+// most ceil(log2 w) times along one path (solver.cpp:44-46).
+int depth_bound(const pccp_gpu_ctx* c, const std::vector<std::int32_t>& root) {
+  const DeviceLayout& L = c->low.L;
+  long long d = 2;
+  for (std::uint32_t i = 0; i < L.n_cand; ++i) {
+    const int w = c->low.blob[L.cand_lbw + i];
+    const long long lo = root[w], hi = root[w + 1];
+    if (lo == INT32_MIN || hi == INT32_MAX) {
+      d += 33;
+    } else if (hi > lo) {
+      d += (long long)std::ceil(std::log2((double)(hi - lo + 1))) + 1;
+    }
+  }
+  return (int)std::min<long long>(d, 1 << 20);
+}
+
+struct RunOut {
+  dev::Globals g;
+  double decompose_ms = 0, kernel_ms = 0, elapsed_ms = 0;
+  std::uint64_t subproblems = 0;
+  bool root_failed = false;
+};
+
+template <class Gp>
+void run_search(pccp_gpu_ctx* c, int mode, const int32_t* root_words, int depth_cap, const pccp_limits* lim,
+                RunOut& out) {
+  const double t_start = now_ms();
+  const DeviceLayout& L = c->low.L;
+  const int nw = (int)L.n_words;
+  const int stride = c->store_stride;
+  const int shard_count = std::max(1, c->cfg.shard_count);
+  const int shard_index = c->cfg.shard_index;
+  if (shard_index < 0 || shard_index >= shard_count) throw ArgError("shard_index out of range");
+  const dev::Model M = c->model();
+  dev::SearchCtl C{};
+  C.G = c->G;
+  C.n_peers = mode == 1 ? c->n_peers : 0;
+  C.peers = c->d_peers.p;
+  C.mode = mode;
+  C.hash = c->cfg.hash;
+  C.depth_cap = depth_cap;
+  C.count = shard_index == 0 ? 1 : 0;  // the decomposition runs on every GPU, counted once
+  c->best.ensure((size_t)std::max(nw, 1));
+  C.best_store = c->best.p;
+
+  reset_globals(c, lim);
+  c->fa.ensure((size_t)stride);
+  c->ia.ensure(1);
+  c->flags.ensure(2);
+  std::vector<std::int32_t> root(root_words, root_words + nw);
+  CK(cudaMemcpyAsync(c->fa.p, root.data(), (size_t)nw * 4, cudaMemcpyHostToDevice, c->stream));
+  const int zero = 0;
+  CK(cudaMemcpyAsync(c->ia.p, &zero, 4, cudaMemcpyHostToDevice, c->stream));
+  CK(cudaEventRecord(c->ev[0], c->stream));
+  dev::k_root<Gp><<<1, c->block, c->smem, c->stream>>>(M, C, c->fa.p, c->flags.p);
+  CK(cudaGetLastError());
+  ++c->launches;
+  unsigned char rflag = 0;
+  CK(cudaMemcpyAsync(&rflag, c->flags.p, 1, cudaMemcpyDeviceToHost, c->stream));
+  CK(cudaMemcpyAsync(root.data(), c->fa.p, (size_t)nw * 4, cudaMemcpyDeviceToHost, c->stream));
+  CK(cudaStreamSynchronize(c->stream));
+
+  // EPS decomposition: whole BFS levels until the frontier holds target nodes.
+  const int eps = c->cfg.eps_factor > 0 ? c->cfg.eps_factor : 8;
+  const long long target = (long long)eps * c->groups() * shard_count;
+  int count = rflag ? 1 : 0;
+  int level = 0;
+  c->d_count = nullptr;
+  DBuf<int> dcount;
+  dcount.ensure(1);
+  while (count > 0 && count < target) {
+    dev::Globals probe;
+    CK(cudaMemcpyAsync(&probe.stop, &c->G->stop, sizeof(int), cudaMemcpyDeviceToHost, c->stream));
+    CK(cudaStreamSynchronize(c->stream));
+    if (probe.stop == 2) break;
+    const size_t nchild = 2 * (size_t)count;
+    c->fb.ensure(nchild * stride);
+    c->ib.ensure(nchild);
+    c->flags.ensure(nchild);
+    const int grid = (int)std::min<long long>(c->ctas, (count + (c->warp ? c->gpc : 1) - 1) / (c->warp ? c->gpc : 1));
+    dev::k_expand<Gp><<<grid, c->block, c->smem, c->stream>>>(M, C, c->fa.p, c->ia.p, count, stride, level + 1,
+                                                                c->fb.p, c->flags.p);
+    CK(cudaGetLastError());
+    dev::k_compact<<<1, 1024, 0, c->stream>>>(c->flags.p, (int)nchild, c->ib.p, dcount.p);
+    CK(cudaGetLastError());
+    c->launches += 2;
+    CK(cudaMemcpyAsync(&count, dcount.p, 4, cudaMemcpyDeviceToHost, c->stream));
+    CK(cudaStreamSynchronize(c->stream));
+    std::swap(c->fa, c->fb);
+    std::swap(c->ia, c->ib);
+    ++level;
+  }
+  dcount.release();
+  CK(cudaEventRecord(c->ev[1], c->stream));
+  out.subproblems = (std::uint64_t)count;
+
+  bool searched = false;
+  if (count > 0) {
+    int dmax = depth_bound(c, root);
+    if (depth_cap >= 0) dmax = std::min(dmax, depth_cap + 2);
+    const int entry = (int)align4((std::uint32_t)nw + 3);
+    c->stack.ensure((size_t)c->groups() * (size_t)dmax * (size_t)entry);
+    dev::SearchParams P{};
+    P.frontier = c->fa.p;
+    P.frontier_idx = c->ia.p;
+    P.n_frontier = count;
+    P.stride = stride;
+    P.depth0 = level;
+    P.shard_index = shard_index;
+    P.shard_count = shard_count;
+    P.stack_pool = c->stack.p;
+    P.stack_depth = dmax;
+    P.entry_stride = entry;
+    C.count = 1;
+    dev::k_search<Gp><<<c->ctas, c->block, c->smem, c->stream>>>(M, C, P);
+    CK(cudaGetLastError());
+    ++c->launches;
+    searched = true;
+  }
+  CK(cudaEventRecord(c->ev[2], c->stream));
+  CK(cudaMemcpyAsync(&out.g, c->G, sizeof(dev::Globals), cudaMemcpyDeviceToHost, c->stream));
+  CK(cudaStreamSynchronize(c->stream));
+  float ms = 0;
+  CK(cudaEventElapsedTime(&ms, c->ev[0], c->ev[1]));
+  out.decompose_ms = ms;
+  if (searched) {
+    CK(cudaEventElapsedTime(&ms, c->ev[1], c->ev[2]));
+    out.kernel_ms = ms;
+  }
+  out.elapsed_ms = now_ms() - t_start;
+  if (out.g.stop == 2) {
+    if (out.g.error_code == 1) throw std::runtime_error("branch: a candidate variable is unbounded");
+    throw LimitError("DFS stack capacity exceeded");
+  }
+}
+
+void fill_stats(const pccp_gpu_ctx* c, const RunOut& r, pccp_stats& s) {
+  std::memset(&s, 0, sizeof(s));
+  s.nodes = r.g.nodes;
+  s.failures = r.g.failures;
+  s.solutions = r.g.solutions;
+  s.open_leaves = r.g.open_leaves;
+  s.hash_sum = r.g.hash_sum;
+  s.rounds = r.g.rounds;
+  s.evals = r.g.rounds * (std::uint64_t)c->low.L.n_ref_cmds;
+  s.subproblems = r.subproblems;
+  s.max_depth = r.g.max_depth;
+  s.elapsed_ms = r.elapsed_ms;
+  s.kernel_ms = r.kernel_ms;
+  s.decompose_ms = r.decompose_ms;
+  s.launches = c->launches;
+}
+
+void check_loaded(const pccp_gpu_ctx* c) {
+  if (!c) throw ArgError("null context");
+  if (!c->loaded) throw ArgError("no model loaded");
+  CK(cudaSetDevice(c->device));
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* pccp_gpu_last_error(void) { return g_err.c_str(); }
+const char* pccp_gpu_version(void) { return "pccp-b200 0.1 (sm_100a)"; }
+
+int pccp_gpu_device_count(int32_t* out) {
+  return api([&] {
+    int n = 0;
+    const cudaError_t e = cudaGetDeviceCount(&n);
+    if (e != cudaSuccess) {
+      cudaGetLastError();
+      n = 0;
+    }
+    *out = n;
+    return n > 0 ? PCCP_OK : (g_err = "no CUDA device", PCCP_ECUDA);
+  });
+}
+
+int pccp_gpu_open(const pccp_gpu_cfg* cfg, pccp_gpu_ctx** out) {
+  return api([&] {
+    if (!out) throw ArgError("null output");
+    *out = nullptr;
+    auto* c = new pccp_gpu_ctx;
+    try {
+      if (cfg) c->cfg = *cfg;
+      c->device = c->cfg.device;
+      CK(cudaSetDevice(c->device));
+      cudaDeviceProp prop;
+      CK(cudaGetDeviceProperties(&prop, c->device));
+      if (prop.major < 10) throw CudaError("device is not sm_100 class (compute capability " +
+                                           std::to_string(prop.major) + "." + std::to_string(prop.minor) + ")");
+      c->n_sm = prop.multiProcessorCount;
+      c->smem_optin = prop.sharedMemPerBlockOptin;
+      CK(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
+      for (auto& e : c->ev) CK(cudaEventCreate(&e));
+      CK(cudaMalloc(&c->G, sizeof(dev::Globals)));
+      CK(cudaMemset(c->G, 0, sizeof(dev::Globals)));
+    } catch (...) {
+      pccp_gpu_close(c);
+      throw;
+    }
+    *out = c;
+    return PCCP_OK;
+  });
+}
+
+void pccp_gpu_close(pccp_gpu_ctx* c) {
+  if (!c) return;
+  cudaSetDevice(c->device);
+  if (c->stream) cudaStreamSynchronize(c->stream);
+  for (void* p : c->opened) cudaIpcCloseMemHandle(p);
+  c->blob.release();
+  c->fa.release();
+  c->fb.release();
+  c->ia.release();
+  c->ib.release();
+  c->stack.release();
+  c->best.release();
+  c->io.release();
+  c->flags.release();
+  c->st.release();
+  c->rnd.release();
+  c->d_peers.release();
+  if (c->G) cudaFree(c->G);
+  for (auto& e : c->ev)
+    if (e) cudaEventDestroy(e);
+  if (c->stream) cudaStreamDestroy(c->stream);
+  delete c;
+}
+
+int pccp_gpu_load(pccp_gpu_ctx* c, const pccp_model* m) {
+  return api([&] {
+    if (!c || !m) throw ArgError("null argument");
+    CK(cudaSetDevice(c->device));
+    c->loaded = false;
+    c->low = lower_model(*m);
+    if (c->low.L.n_cand >= (1u << 24)) throw LimitError("more than 2^24 branching candidates");
+    c->slot_kind.assign(m->slot_kind, m->slot_kind + m->n_slots);
+    c->slot_word.assign(m->slot_word, m->slot_word + m->n_slots);
+    c->view = *m;
+    c->view.slot_kind = c->slot_kind.data();
+    c->view.slot_word = c->slot_word.data();
+    c->view.cmd_off = nullptr;
+    c->view.cmd_code = nullptr;
+    c->view.cands = nullptr;
+    c->blob.ensure(c->low.blob.size() + 4);
+    CK(cudaMemcpyAsync(c->blob.p, c->low.blob.data(), c->low.blob.size() * 4, cudaMemcpyHostToDevice, c->stream));
+    plan(c);
+    CK(cudaStreamSynchronize(c->stream));
+    c->loaded = true;
+    return PCCP_OK;
+  });
+}
+
+int pccp_gpu_lowering_info(pccp_gpu_ctx* c, pccp_lowering_info* o) {
+  return api([&] {
+    check_loaded(c);
+    const DeviceLayout& L = c->low.L;
+    std::memset(o, 0, sizeof(*o));
+    o->n_words = L.n_words;
+    o->n_cmds = L.n_ref_cmds;
+    o->n_folded = L.n_fold;
+    o->n_small = L.n_small;
+    o->n_rows = L.n_rows;
+    o->n_row_terms = L.n_row_terms;
+    o->n_generic = L.n_gen;
+    o->table_bytes = L.blob_words * 4;
+    o->store_bytes = L.n_words * 4;
+    o->group_threads = c->warp ? 32 : c->block;
+    o->groups_per_cta = c->warp ? c->gpc : 1;
+    o->ctas = c->ctas;
+    o->smem_bytes = (std::uint32_t)c->smem;
+    o->table_in_smem = c->table_in_smem;
+    o->stack_in_smem = 0;
+    o->alg_bytes_per_eval = c->low.alg_bytes_per_eval;
+    return PCCP_OK;
+  });
+}
+
+int pccp_gpu_propagate_batch(pccp_gpu_ctx* c, const int32_t* in, uint32_t n, int32_t* out, uint8_t* status,
+                             uint32_t* rounds) {
+  return api([&] {
+    check_loaded(c);
+    if (n == 0) return PCCP_OK;
+    if (!in || !out || !status) throw ArgError("null buffer");
+    const size_t nw = c->low.L.n_words;
+    c->io.ensure((size_t)n * std::max<size_t>(nw, 1));
+    c->st.ensure(n);
+    c->rnd.ensure(n);
+    if (nw) CK(cudaMemcpyAsync(c->io.p, in, (size_t)n * nw * 4, cudaMemcpyHostToDevice, c->stream));
+    const dev::Model M = c->model();
+    const int per = c->warp ? c->gpc : 1;
+    const int grid = (int)std::min<long long>(c->ctas, ((long long)n + per - 1) / per);
+    if (c->warp)
+      dev::k_propagate<dev::WarpGroup><<<grid, c->block, c->smem, c->stream>>>(M, c->io.p, (int)n, (int)nw, c->st.p,
+                                                                               c->rnd.p, 1);
+    else
+      dev::k_propagate<dev::CtaGroup><<<grid, c->block, c->smem, c->stream>>>(M, c->io.p, (int)n, (int)nw, c->st.p,
+                                                                              c->rnd.p, 1);
+    CK(cudaGetLastError());
+    ++c->launches;
+    if (nw) CK(cudaMemcpyAsync(out, c->io.p, (size_t)n * nw * 4, cudaMemcpyDeviceToHost, c->stream));
+    CK(cudaMemcpyAsync(status, c->st.p, n, cudaMemcpyDeviceToHost, c->stream));
+    if (rounds) CK(cudaMemcpyAsync(rounds, c->rnd.p, (size_t)n * 4, cudaMemcpyDeviceToHost, c->stream));
+    CK(cudaStreamSynchronize(c->stream));
+    return PCCP_OK;
+  });
+}
+
+int pccp_gpu_replay(pccp_gpu_ctx* c, const int32_t* root, uint32_t n_paths, const uint32_t* path_off,
+                    const pccp_decision* dec, const int32_t* best, int32_t* out, uint8_t* status) {
+  return api([&] {
+    check_loaded(c);
+    const size_t nw = c->low.L.n_words;
+    std::vector<std::int32_t> stores((size_t)n_paths * nw);
+    for (uint32_t p = 0; p < n_paths; ++p) {
+      std::int32_t* s = stores.data() + (size_t)p * nw;
+      std::memcpy(s, root, nw * 4);
+      for (uint32_t k = path_off[p]; k < path_off[p + 1]; ++k) host_join_decision(c->view, s, dec[k]);
+      const std::int32_t b = best ? best[p] : INT32_MAX;
+      if (b != INT32_MAX && c->low.L.obj_lbw >= 0) {
+        std::int32_t& ub = s[c->low.L.obj_lbw + 1];
+        if (b - 1 < ub) ub = b - 1;
+      }
+    }
+    const int r = pccp_gpu_propagate_batch(c, stores.data(), n_paths, out, status, nullptr);
+    if (r != PCCP_OK) throw CudaError(g_err);
+    return PCCP_OK;
+  });
+}
+
+int pccp_gpu_enumerate(pccp_gpu_ctx* c, const int32_t* root, int32_t depth_cap, const pccp_limits* lim,
+                       pccp_enum_result* out) {
+  return api([&] {
+    check_loaded(c);
+    if (!root || !out) throw ArgError("null argument");
+    std::memset(out, 0, sizeof(*out));
+    if (lim && lim->node_limit == 0) return PCCP_OK;
+    RunOut r;
+    if (c->warp) run_search<dev::WarpGroup>(c, 0, root, depth_cap, lim, r);
+    else run_search<dev::CtaGroup>(c, 0, root, depth_cap, lim, r);
+    fill_stats(c, r, out->stats);
+    out->exhausted = r.g.incomplete ? 0 : 1;
+    return PCCP_OK;
+  });
+}
+
+int pccp_gpu_solve(pccp_gpu_ctx* c, const int32_t* root, const pccp_limits* lim, pccp_solve_result* out,
+                   int32_t* best_words) {
+  return api([&] {
+    check_loaded(c);
+    if (!root || !out) throw ArgError("null argument");
+    if (c->low.L.obj_lbw < 0) throw std::runtime_error("solve: the model has no objective");
+    std::memset(out, 0, sizeof(*out));
+    if (lim && lim->node_limit == 0) {  // should_stop before the root (solver.cpp:240)
+      out->status = PCCP_UNKNOWN;
+      return PCCP_OK;
+    }
+    RunOut r;
+    if (c->warp) run_search<dev::WarpGroup>(c, 1, root, -1, lim, r);
+    else run_search<dev::CtaGroup>(c, 1, root, -1, lim, r);
+    fill_stats(c, r, out->stats);
+    const bool exhausted = r.g.incomplete == 0;
+    const bool has = r.g.incumbent != INT32_MAX;
+    out->has_objective = has ? 1 : 0;
+    out->objective = has ? r.g.incumbent : 0;
+    out->status = has ? (exhausted ? PCCP_OPTIMAL : PCCP_SAT) : (exhausted ? PCCP_UNSAT : PCCP_UNKNOWN);
+    out->n_improvements = std::min(r.g.n_impr, 64);
+    for (int k = 0; k < out->n_improvements; ++k) {
+      out->improvements[k] = r.g.impr_val[k];
+      out->improvement_ms[k] = (double)r.g.impr_ns[k] * 1e-6;
+    }
+    if (best_words && has && r.g.best_value == r.g.incumbent)
+      CK(cudaMemcpy(best_words, c->best.p, (size_t)c->low.L.n_words * 4, cudaMemcpyDeviceToHost));
+    else if (best_words && has)
+      out->has_objective = 2;  // incumbent found on a peer GPU: its store lives there
+    return PCCP_OK;
+  });
+}
+
+int pccp_gpu_incumbent_handle(pccp_gpu_ctx* c, uint8_t* out64) {
+  return api([&] {
+    if (!c || !out64) throw ArgError("null argument");
+    CK(cudaSetDevice(c->device));
+    cudaIpcMemHandle_t h;
+    CK(cudaIpcGetMemHandle(&h, c->G));
+    static_assert(sizeof(h) <= 64, "IPC handle larger than 64 bytes");
+    std::memset(out64, 0, 64);
+    std::memcpy(out64, &h, sizeof(h));
+    return PCCP_OK;
+  });
+}
+
+int pccp_gpu_attach_peers(pccp_gpu_ctx* c, const uint8_t* handles, int32_t n, int32_t self) {
+  return api([&] {
+    if (!c || (n > 0 && !handles)) throw ArgError("null argument");
+    CK(cudaSetDevice(c->device));
+    std::vector<int*> ptrs;
+    for (int i = 0; i < n; ++i) {
+      if (i == self) continue;
+      cudaIpcMemHandle_t h;
+      std::memcpy(&h, handles + 64 * i, sizeof(h));
+      void* p = nullptr;
+      CK(cudaIpcOpenMemHandle(&p, h, cudaIpcMemLazyEnablePeerAccess));
+      c->opened.push_back(p);
+      ptrs.push_back(reinterpret_cast<int*>(static_cast<char*>(p) + offsetof(dev::Globals, incumbent)));
+    }
+    c->n_peers = (int)ptrs.size();
+    if (!ptrs.empty()) {
+      c->d_peers.ensure(ptrs.size());
+      CK(cudaMemcpy(c->d_peers.p, ptrs.data(), ptrs.size() * sizeof(int*), cudaMemcpyHostToDevice));
+    }
+    return PCCP_OK;
+  });
+}
+
+}  // extern "C"

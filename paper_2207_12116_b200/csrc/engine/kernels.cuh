@@ -1,0 +1,376 @@
+// kernels.cuh — sm_100a propagate-and-search kernels.
+//
+// One *group* of threads owns one search subproblem: either a single warp
+// (small stores: many independent subproblems per SM, fixed point detected
+// with warp votes) or a whole CTA (large stores: the fixed point detected
+// with __syncthreads_or over a 3-slot change ring, engine.cpp:86-116).  The
+// group's interval store lives in shared memory; propagators tighten it with
+// atomicMax (lb / ZInc words) and atomicMin (ub / ZDec words), the
+// lock-free lattice joins of Store::join_word (store.hpp:90-98).  Reads of
+// the store go through `volatile` so no word is cached in a register across
+// a round (the erratum of PAPER.md:459-460).
+//
+// Arithmetic is the reference's, bit for bit (H1): term values widen the
+// sentinels to +-2^40 and clamp finite products to +-2^40, sums accumulate in
+// int64 and narrow back to the int32 sentinels (command.cpp:11-27).
+#pragma once
+
+#include <climits>
+#include <cstdint>
+
+#include "lower.hpp"
+
+namespace pccp_b200 {
+namespace dev {
+
+constexpr long long kWide = 1LL << 40;
+constexpr unsigned kFull = 0xffffffffu;
+
+struct Model {
+  DeviceLayout L;
+  const int* __restrict__ blob;  // global copy of the tables
+  int table_in_smem;             // copy the blob into shared memory at kernel start
+  int store_stride;              // words per group store in smem (>= n_words, multiple of 4)
+};
+
+// Counters and control shared by all groups of one search (global memory).
+struct Globals {
+  unsigned long long nodes, failures, solutions, open_leaves, hash_sum, rounds, max_depth;
+  unsigned long long node_limit;   // ~0: none
+  unsigned long long nodes_reserved;  // materialisations admitted against node_limit
+  unsigned long long t0;           // %globaltimer at search start
+  unsigned long long timeout_ns;   // 0: none
+  unsigned int cursor;             // EPS work queue
+  int stop;                        // 1: limit reached, 2: model error
+  int incomplete;                  // a subproblem was abandoned
+  int incumbent;                   // best objective, INT_MAX: none (local replica)
+  int best_lock;
+  int best_value;
+  int n_impr;
+  int impr_val[64];
+  unsigned long long impr_ns[64];
+  int error_code;
+};
+
+__device__ __forceinline__ unsigned long long globaltimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+
+// term_value, command.cpp:11-19
+__device__ __forceinline__ long long tv(int c, int v) {
+  if (v == INT_MAX) return c > 0 ? kWide : (c < 0 ? -kWide : 0);
+  if (v == INT_MIN) return c > 0 ? -kWide : (c < 0 ? kWide : 0);
+  long long p = (long long)c * (long long)v;
+  return p > kWide ? kWide : (p < -kWide ? -kWide : p);
+}
+__device__ __forceinline__ int narrow(long long a) {
+  return a >= INT_MAX ? INT_MAX : (a <= INT_MIN ? INT_MIN : (int)a);
+}
+__device__ __forceinline__ int tcoef(int x) { return x >> kTermWordBits; }
+__device__ __forceinline__ int tword(int x) { return x & (int)kTermWordMask; }
+
+// Store::join_word, store.hpp:90-98: read first, only issue the atomic when
+// the value would strictly improve; returns the strict-change flag (bx).
+__device__ __forceinline__ bool join_max(volatile int* S, int w, int v) {
+  if (v > S[w]) return atomicMax((int*)(S + w), v) < v;
+  return false;
+}
+__device__ __forceinline__ bool join_min(volatile int* S, int w, int v) {
+  if (v < S[w]) return atomicMin((int*)(S + w), v) > v;
+  return false;
+}
+
+// ---- groups --------------------------------------------------------------------
+
+struct WarpGroup {
+  int lane;
+  __device__ __forceinline__ int rank() const { return lane; }
+  __device__ __forceinline__ int size() const { return 32; }
+  __device__ __forceinline__ int warp() const { return 0; }
+  __device__ __forceinline__ int warps() const { return 1; }
+  __device__ __forceinline__ void sync() const { __syncwarp(); }
+  __device__ __forceinline__ void round_begin() const {}
+  // End of a fixed-point round: one vote per flag.
+  __device__ __forceinline__ void round_end(bool ch, bool fl, bool& any_ch, bool& any_fl, int) const {
+    __syncwarp();
+    any_ch = __any_sync(kFull, ch);
+    any_fl = __any_sync(kFull, fl);
+  }
+  __device__ __forceinline__ bool any(bool p) const { return __any_sync(kFull, p); }
+  __device__ __forceinline__ unsigned long long min_u64(unsigned long long v) const {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      const unsigned long long u = __shfl_xor_sync(kFull, v, o);
+      v = u < v ? u : v;
+    }
+    return v;
+  }
+  __device__ __forceinline__ int bcast0(int v) const { return __shfl_sync(kFull, v, 0); }
+};
+
+struct CtaGroup {
+  int tid, n;
+  int* ring;                 // 4 ints of smem: 3-slot change ring + spare
+  unsigned long long* red;   // 33 u64 of smem
+  __device__ __forceinline__ int rank() const { return tid; }
+  __device__ __forceinline__ int size() const { return n; }
+  __device__ __forceinline__ int warp() const { return tid >> 5; }
+  __device__ __forceinline__ int warps() const { return n >> 5; }
+  __device__ __forceinline__ void sync() const { __syncthreads(); }
+  __device__ __forceinline__ void round_begin() const {
+    if (tid < 3) ring[tid] = 0;
+    __syncthreads();
+  }
+  // One barrier per round: round i sets ring[i%3] on change and clears
+  // ring[(i+1)%3]; after the barrier everybody reads ring[i%3] (the
+  // past/present/future ring of run_parallel, engine.cpp:86-116).
+  __device__ __forceinline__ void round_end(bool ch, bool fl, bool& any_ch, bool& any_fl, int i) const {
+    if (ch) ring[i % 3] = 1;
+    if (tid == 0) ring[(i + 1) % 3] = 0;
+    any_fl = __syncthreads_or(fl) != 0;
+    any_ch = *(volatile int*)&ring[i % 3] != 0;
+  }
+  __device__ __forceinline__ bool any(bool p) const { return __syncthreads_or(p) != 0; }
+  __device__ __forceinline__ unsigned long long min_u64(unsigned long long v) const {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      const unsigned long long u = __shfl_xor_sync(kFull, v, o);
+      v = u < v ? u : v;
+    }
+    if ((tid & 31) == 0) red[tid >> 5] = v;
+    __syncthreads();
+    if (tid < 32) {
+      v = tid < (n >> 5) ? red[tid] : ~0ull;
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) {
+        const unsigned long long u = __shfl_xor_sync(kFull, v, o);
+        v = u < v ? u : v;
+      }
+      if (tid == 0) red[32] = v;
+    }
+    __syncthreads();
+    v = red[32];
+    __syncthreads();
+    return v;
+  }
+  __device__ __forceinline__ int bcast0(int v) const {
+    if (tid == 0) ring[3] = v;
+    __syncthreads();
+    v = ring[3];
+    __syncthreads();
+    return v;
+  }
+};
+
+// ---- propagators -----------------------------------------------------------------
+
+// LinExpr::eval over a flat [k, n, (coef, word)*n] expression (command.cpp:21-27).
+__device__ __forceinline__ int lin_eval(const int* __restrict__ e, volatile int* S) {
+  long long acc = e[0];
+  const int n = e[1];
+  for (int t = 0; t < n; ++t) acc += tv(e[2 + 2 * t], S[e[3 + 2 * t]]);
+  return narrow(acc);
+}
+
+// Interpreted fallback: GuardedCommand::apply (command.cpp:93-113) on the flat stream.
+__device__ bool eval_generic(volatile int* S, const int* __restrict__ c) {
+  const int ng = c[0], kind = c[2], tw = c[3], mask = c[4];
+  const int* p = c + 5;
+  for (int g = 0; g < ng; ++g) {
+    const int rel = p[0], rhs = p[1];
+    const int v = lin_eval(p + 2, S);
+    if (rel == PCCP_LEQ ? !(v <= rhs) : !(v > rhs)) return false;
+    p += 4 + 2 * p[3];
+  }
+  const int *sc = nullptr, *lb = nullptr, *ub = nullptr;
+  if (mask & PCCP_FN_SCALAR) { sc = p; p += 2 + 2 * p[1]; }
+  if (mask & PCCP_FN_LB) { lb = p; p += 2 + 2 * p[1]; }
+  if (mask & PCCP_FN_UB) { ub = p; }
+  bool ch = false;
+  if (kind == PCCP_INTERVAL) {
+    if (lb) ch |= join_max(S, tw, lin_eval(lb, S));
+    if (ub) ch |= join_min(S, tw + 1, lin_eval(ub, S));
+  } else {
+    const int v = lin_eval(sc, S);
+    ch |= (kind == PCCP_ZINC || kind == PCCP_BINC) ? join_max(S, tw, v) : join_min(S, tw, v);
+  }
+  return ch;
+}
+
+// Small command i: up to two normalised guards `tv + tv <= T`, then the lb
+// and/or ub tell, each `narrow(k + tv)`.
+__device__ __forceinline__ bool eval_small(volatile int* S, const int* __restrict__ T, const DeviceLayout& L,
+                                           int i) {
+  const int a0 = T[L.small_g[0] + i], a1 = T[L.small_g[1] + i];
+  long long s = 0;
+  if (a0) s += tv(tcoef(a0), S[tword(a0)]);
+  if (a1) s += tv(tcoef(a1), S[tword(a1)]);
+  if (s > (long long)T[L.small_T[0] + i]) return false;
+  const int T1 = T[L.small_T[1] + i];
+  const int a2 = T[L.small_g[2] + i], a3 = T[L.small_g[3] + i];
+  if (a2 | a3) {
+    s = 0;
+    if (a2) s += tv(tcoef(a2), S[tword(a2)]);
+    if (a3) s += tv(tcoef(a3), S[tword(a3)]);
+    if (s > (long long)T1) return false;
+  } else if (T1 < 0) {
+    return false;  // 0 <= T1 fails
+  }
+  const int tw = T[L.small_tw + i];
+  bool ch = false;
+  const int lbk = T[L.small_lbk + i], lbt = T[L.small_lbt + i];
+  if (lbt) ch |= join_max(S, tw, narrow((long long)lbk + tv(tcoef(lbt), S[tword(lbt)])));
+  else if (lbk != INT_MIN) ch |= join_max(S, tw, lbk);
+  const int ubk = T[L.small_ubk + i], ubt = T[L.small_ubt + i];
+  if (ubt) ch |= join_min(S, tw + 1, narrow((long long)ubk + tv(tcoef(ubt), S[tword(ubt)])));
+  else if (ubk != INT_MAX) ch |= join_min(S, tw + 1, ubk);
+  return ch;
+}
+
+// Fused sum rows (H2).  A sub-warp of L.row_lanes lanes owns a row: it reads
+// every lb once, reduces S = sum tv(coef, lb), joins lsum <- narrow(S) (and
+// +inf when S > c, the overload rule), then evaluates each zeroing guard
+// `coef + lsum - coef*lb(x) > c` with lsum taken from the same reduction.
+// The second read of lb(x) can only be newer than the one summed, which
+// makes the guard weaker, never unsound; at the quiet round both reads agree.
+template <class G>
+__device__ bool eval_rows(const G& g, volatile int* S, const int* __restrict__ T, const DeviceLayout& L) {
+  const int R = (int)L.row_lanes;
+  const int sub = g.rank() & (R - 1);
+  const int per_pass = g.size() / R;
+  const int my = g.rank() / R;
+  bool ch = false;
+  for (int base = 0; base < (int)L.n_rows; base += per_pass) {
+    const int row = base + my;
+    const bool act = row < (int)L.n_rows;
+    long long s = 0;
+    int beg = 0, end = 0;
+    if (act) {
+      beg = T[L.row_off + row];
+      end = T[L.row_off + row + 1];
+      for (int j = beg + sub; j < end; j += R) {
+        const int x = T[L.row_terms + j];
+        s += tv(tcoef(x), S[tword(x)]);
+      }
+    }
+    for (int o = R >> 1; o > 0; o >>= 1) s += __shfl_xor_sync(kFull, s, o, R);
+    if (act) {
+      const int c = T[L.row_c + row];
+      const int lsum = narrow(s);
+      const int cell = lsum > c ? INT_MAX : lsum;  // [lsum > c] => lsum <- +inf
+      if (sub == 0) ch |= join_max(S, T[L.row_lsum + row], cell);
+      if (c != INT_MAX) {
+        const long long wl = tv(1, cell);
+        for (int j = beg + sub; j < end; j += R) {
+          const int x = T[L.row_terms + j];
+          const int coef = tcoef(x), w = tword(x);
+          if ((long long)coef + wl + tv(-coef, S[w]) > (long long)c) {
+            ch |= join_max(S, w, 0);
+            ch |= join_min(S, w + 1, 0);
+          }
+        }
+      }
+    }
+  }
+  return ch;
+}
+
+// Unguarded constant tells, joined once at node entry.
+template <class G>
+__device__ __forceinline__ void apply_fold(const G& g, volatile int* S, const int* __restrict__ T,
+                                           const DeviceLayout& L) {
+  for (int i = g.rank(); i < (int)L.n_fold; i += g.size()) {
+    const int wf = T[L.fold_w + i];
+    const int v = T[L.fold_v + i];
+    const int w = wf & 0x7fffffff;
+    if (wf < 0) join_max(S, w, v);
+    else join_min(S, w, v);
+  }
+}
+
+// The eventless fixed-point loop (run_sequential / run_parallel,
+// engine.cpp:13-133): every round evaluates every command, joins with
+// atomics, and scans a strided slice of the store for failure (an empty
+// interval or a scalar at top, store.cpp:65-75).  Failure is monotone, so a
+// scan of any intermediate state is valid; it runs every round (H8).
+// Returns true iff the store failed.
+template <class G>
+__device__ bool propagate(const G& g, volatile int* S, const int* __restrict__ T, const DeviceLayout& L,
+                          int& rounds) {
+  g.round_begin();
+  int r = 0;
+  bool failed = false;
+  for (;;) {
+    bool ch = false, fl = false;
+    for (int i = g.rank(); i < (int)L.n_small; i += g.size()) ch |= eval_small(S, T, L, i);
+    if (L.n_rows) ch |= eval_rows(g, S, T, L);
+    for (int i = g.rank(); i < (int)L.n_gen; i += g.size())
+      ch |= eval_generic(S, T + L.gen_code + T[L.gen_off + i]);
+    for (int i = g.rank(); i < (int)L.n_iv; i += g.size()) {
+      const int w = T[L.iv_lb + i];
+      fl |= S[w] > S[w + 1];
+    }
+    for (int i = g.rank(); i < (int)L.n_sc; i += g.size()) fl |= S[T[L.sc_w + i]] == T[L.sc_top + i];
+    bool any_ch, any_fl;
+    g.round_end(ch, fl, any_ch, any_fl, r);
+    ++r;
+    if (any_fl) { failed = true; break; }
+    if (!any_ch) break;
+  }
+  rounds = r;
+  return failed;
+}
+
+// branch (solver.cpp:19-47): narrowest candidate with lo < hi, first in
+// candidate order on ties (key = width << 24 | position), mid = floor((lo+hi)/2).
+// Returns 0: none (a solution), 1: decision, -1: unbounded (ModelError).
+template <class G>
+__device__ int branch(const G& g, volatile int* S, const int* __restrict__ T, const DeviceLayout& L, int& lbw,
+                      int& mid) {
+  unsigned long long best = ~0ull;
+  for (int i = g.rank(); i < (int)L.n_cand; i += g.size()) {
+    const int w = T[L.cand_lbw + i];
+    const int lo = S[w], hi = S[w + 1];
+    if (lo < hi) {
+      const unsigned long long width = (unsigned long long)((long long)hi - (long long)lo + 1);
+      const unsigned long long key = (width << 24) | (unsigned long long)i;
+      best = key < best ? key : best;
+    }
+  }
+  best = g.min_u64(best);
+  if (best == ~0ull) return 0;
+  const int w = T[L.cand_lbw + (int)(best & 0xffffffull)];
+  const int lo = S[w], hi = S[w + 1];
+  if (lo == INT_MIN || hi == INT_MAX) return -1;
+  lbw = w;
+  mid = (int)(((long long)lo + (long long)hi) >> 1);
+  return 1;
+}
+
+// SURVEY 8(c) hash: FNV-style over the 4 little-endian bytes of each word.
+__device__ __forceinline__ unsigned long long store_hash(volatile int* S, int n) {
+  unsigned long long h = 1469598103934665603ull;
+  for (int w = 0; w < n; ++w) {
+    const unsigned v = (unsigned)S[w];
+#pragma unroll
+    for (int b = 0; b < 4; ++b) {
+      h ^= (v >> (8 * b)) & 0xffu;
+      h *= 1099511628211ull;
+    }
+  }
+  return h;
+}
+
+template <class G>
+__device__ __forceinline__ void copy_words(const G& g, volatile int* dst, const int* __restrict__ src, int n) {
+  for (int i = g.rank(); i < n; i += g.size()) dst[i] = src[i];
+}
+template <class G>
+__device__ __forceinline__ void copy_out(const G& g, int* __restrict__ dst, volatile int* src, int n) {
+  for (int i = g.rank(); i < n; i += g.size()) dst[i] = src[i];
+}
+
+}  // namespace dev
+}  // namespace pccp_b200

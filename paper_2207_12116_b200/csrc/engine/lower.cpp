@@ -1,0 +1,455 @@
+// lower.cpp — flat reference tables -> device tables (see lower.hpp).
+#include "lower.hpp"
+
+#include <algorithm>
+#include <optional>
+#include <stdexcept>
+#include <tuple>
+
+namespace pccp_b200 {
+
+namespace {
+
+struct Expr {
+  std::int32_t k = 0;
+  std::vector<std::pair<std::int32_t, std::uint32_t>> terms;  // (coef, word)
+};
+struct GuardP {
+  int rel;
+  std::int32_t rhs;
+  Expr lhs;
+};
+struct CmdP {
+  std::int32_t target;
+  int kind;
+  std::uint32_t tw;
+  std::vector<GuardP> guards;
+  std::optional<Expr> sc, lb, ub;
+};
+
+[[noreturn]] void bad(const std::string& why) { throw std::runtime_error(why); }
+
+std::vector<CmdP> parse(const pccp_model& m) {
+  std::vector<CmdP> out;
+  out.reserve(m.n_cmds);
+  const std::int32_t* code = m.cmd_code;
+  for (std::uint32_t i = 0; i < m.n_cmds; ++i) {
+    const std::uint32_t beg = m.cmd_off[i], end = m.cmd_off[i + 1];
+    if (end < beg + 5) bad("command " + std::to_string(i) + ": truncated header");
+    std::uint32_t p = beg;
+    auto take = [&]() -> std::int32_t {
+      if (p >= end) bad("command " + std::to_string(i) + ": truncated");
+      return code[p++];
+    };
+    auto expr = [&]() {
+      Expr e;
+      e.k = take();
+      const std::int32_t n = take();
+      if (n < 0) bad("negative term count");
+      for (std::int32_t t = 0; t < n; ++t) {
+        const std::int32_t coef = take();
+        const std::int32_t w = take();
+        if (w < 0 || static_cast<std::uint32_t>(w) >= m.n_words) bad("term word out of range");
+        e.terms.emplace_back(coef, static_cast<std::uint32_t>(w));
+      }
+      return e;
+    };
+    CmdP c;
+    const std::int32_t ng = take();
+    c.target = take();
+    c.kind = take();
+    const std::int32_t tw = take();
+    const std::int32_t mask = take();
+    if (ng < 0) bad("negative guard count");
+    if (c.target < 0 || static_cast<std::uint32_t>(c.target) >= m.n_slots) bad("tell target out of range");
+    if (c.kind != m.slot_kind[c.target]) bad("target kind does not match the schema");
+    if (static_cast<std::uint32_t>(tw) != m.slot_word[c.target]) bad("target word does not match the schema");
+    c.tw = static_cast<std::uint32_t>(tw);
+    for (std::int32_t g = 0; g < ng; ++g) {
+      GuardP gp;
+      gp.rel = take();
+      gp.rhs = take();
+      if (gp.rel != PCCP_LEQ && gp.rel != PCCP_GT) bad("bad guard relation");
+      gp.lhs = expr();
+      c.guards.push_back(std::move(gp));
+    }
+    if (mask & PCCP_FN_SCALAR) c.sc = expr();
+    if (mask & PCCP_FN_LB) c.lb = expr();
+    if (mask & PCCP_FN_UB) c.ub = expr();
+    if (p != end) bad("command " + std::to_string(i) + ": trailing words");
+    if (c.kind != PCCP_INTERVAL && !c.sc)
+      bad("scalar tell without a scalar expression");  // MonotoneFn::eval, command.cpp:63
+    out.push_back(std::move(c));
+  }
+  return out;
+}
+
+bool fits_term(std::int32_t coef, std::uint32_t word) {
+  return coef >= -2048 && coef <= 2047 && word <= kTermWordMask;
+}
+std::int32_t pack(std::int32_t coef, std::uint32_t word) {
+  return static_cast<std::int32_t>((static_cast<std::uint32_t>(coef) << kTermWordBits) | word);
+}
+
+// Normalised guard: sum tv(c_i, v_i) <= T.  Returns false if not expressible.
+//   narrow(k + S) <= rhs  <=>  rhs == +inf || S <= rhs - k
+//   narrow(k + S) >  rhs  <=>  rhs != +inf && -S <= k - rhs - 1,  tv(-c, v) = -tv(c, v)
+struct NormGuard {
+  bool always = false, never = false;
+  std::int32_t T = 0;
+  std::vector<std::pair<std::int32_t, std::uint32_t>> terms;
+};
+std::optional<NormGuard> normalise(const GuardP& g) {
+  NormGuard n;
+  if (g.rhs == INT32_MAX) {
+    if (g.rel == PCCP_LEQ) n.always = true;
+    else n.never = true;
+    return n;
+  }
+  std::int64_t T;
+  if (g.rel == PCCP_LEQ) {
+    T = std::int64_t{g.rhs} - g.lhs.k;
+    n.terms = g.lhs.terms;
+  } else {
+    T = std::int64_t{g.lhs.k} - g.rhs - 1;
+    for (auto [c, w] : g.lhs.terms) {
+      if (c == INT32_MIN) return std::nullopt;
+      n.terms.emplace_back(-c, w);
+    }
+  }
+  if (T < INT32_MIN || T > INT32_MAX) return std::nullopt;
+  n.T = static_cast<std::int32_t>(T);
+  return n;
+}
+
+std::uint32_t align4(std::uint32_t x) { return (x + 3u) & ~3u; }
+
+}  // namespace
+
+Lowered lower_model(const pccp_model& m) {
+  if (m.n_slots && (!m.slot_kind || !m.slot_word)) bad("null slot tables");
+  if (m.n_cmds && (!m.cmd_off || !m.cmd_code)) bad("null command tables");
+  Lowered out;
+  DeviceLayout& L = out.L;
+  L.n_words = m.n_words;
+  L.n_ref_cmds = m.n_cmds;
+
+  // Schema: word directions and owners.
+  out.word_up.assign(m.n_words, 0);
+  out.slot_of_word.assign(m.n_words, -1);
+  std::vector<std::uint8_t> is_lb(m.n_words, 0);
+  for (std::uint32_t s = 0; s < m.n_slots; ++s) {
+    const std::uint32_t w = m.slot_word[s];
+    const int k = m.slot_kind[s];
+    if (k < 0 || k > 4) bad("bad slot kind");
+    const std::uint32_t span = k == PCCP_INTERVAL ? 2 : 1;
+    if (w + span > m.n_words) bad("slot word out of range");
+    if (k == PCCP_INTERVAL) {
+      out.word_up[w] = 1;
+      out.word_up[w + 1] = 0;
+      is_lb[w] = 1;
+      out.slot_of_word[w] = out.slot_of_word[w + 1] = static_cast<std::int32_t>(s);
+    } else {
+      out.word_up[w] = (k == PCCP_ZINC || k == PCCP_BINC);
+      out.slot_of_word[w] = static_cast<std::int32_t>(s);
+    }
+  }
+
+  const std::vector<CmdP> cmds = parse(m);
+
+  // B_alg of SURVEY 8(d): 4*(guard terms) + 4*(fn terms + target words).
+  {
+    double total = 0;
+    for (const CmdP& c : cmds) {
+      std::size_t b = 0;
+      for (const GuardP& g : c.guards) b += 4 * g.lhs.terms.size();
+      if (c.kind == PCCP_INTERVAL) {
+        if (c.lb) b += 4 * (c.lb->terms.size() + 1);
+        if (c.ub) b += 4 * (c.ub->terms.size() + 1);
+      } else {
+        b += 4 * (c.sc->terms.size() + 1);
+      }
+      total += static_cast<double>(b);
+    }
+    out.alg_bytes_per_eval = cmds.empty() ? 0.0 : total / static_cast<double>(cmds.size());
+  }
+
+  // Word reference counts, to prove an lsum cell is private to its row.
+  std::vector<std::uint32_t> refs(m.n_words, 0);
+  for (const CmdP& c : cmds) {
+    ++refs[c.tw];
+    for (const GuardP& g : c.guards)
+      for (auto& t : g.lhs.terms) ++refs[t.second];
+    for (const auto* e : {&c.sc, &c.lb, &c.ub})
+      if (*e)
+        for (auto& t : (*e)->terms) ++refs[t.second];
+  }
+
+  std::vector<std::int32_t> fold_w, fold_v;
+  struct Small {
+    std::int32_t g[4] = {0, 0, 0, 0};
+    std::int32_t T[2] = {INT32_MAX, INT32_MAX};
+    std::int32_t lbk = INT32_MIN, lbt = 0, ubk = INT32_MAX, ubt = 0;
+    std::int32_t tw = 0;
+    std::uint32_t shape = 0;
+  };
+  std::vector<Small> smalls;
+  struct Row {
+    std::uint32_t lsum;
+    std::int32_t c;
+    std::vector<std::int32_t> terms;
+  };
+  std::vector<Row> rows;
+  std::vector<std::uint32_t> generic;
+
+  // compile_sum pattern (propagation.cpp:314-335) starting at command i.
+  auto match_row = [&](std::size_t i) -> std::size_t {
+    const CmdP& s = cmds[i];
+    if (!s.guards.empty() || s.kind != PCCP_ZINC || !s.sc || s.lb || s.ub || s.sc->k != 0) return 0;
+    const auto& terms = s.sc->terms;
+    const std::size_t n = terms.size();
+    if (n == 0 || i + 2 + n > cmds.size()) return 0;
+    const std::uint32_t lw = s.tw;
+    for (auto [coef, w] : terms)
+      if (coef < 0 || !is_lb[w] || !fits_term(coef, w)) return 0;
+    const CmdP& o = cmds[i + 1];  // [lsum > c] => lsum <- +inf
+    if (o.target != s.target || o.guards.size() != 1 || !o.sc || o.lb || o.ub) return 0;
+    if (o.sc->k != INT32_MAX || !o.sc->terms.empty()) return 0;
+    const GuardP& og = o.guards[0];
+    if (og.rel != PCCP_GT || og.lhs.k != 0 || og.lhs.terms.size() != 1 || og.lhs.terms[0].first != 1 ||
+        og.lhs.terms[0].second != lw)
+      return 0;
+    const std::int32_t c = og.rhs;
+    for (std::size_t t = 0; t < n; ++t) {  // [coef + lsum - coef*lb(x) > c] => x <- (0,0)
+      const CmdP& z = cmds[i + 2 + t];
+      const auto [coef, w] = terms[t];
+      if (z.guards.size() != 1 || z.kind != PCCP_INTERVAL || z.tw != w || z.sc) return 0;
+      if (!z.lb || !z.ub || z.lb->k != 0 || z.ub->k != 0 || !z.lb->terms.empty() || !z.ub->terms.empty())
+        return 0;
+      const GuardP& g = z.guards[0];
+      if (g.rel != PCCP_GT || g.rhs != c || g.lhs.k != coef || g.lhs.terms.size() != 2) return 0;
+      if (g.lhs.terms[0] != std::make_pair(std::int32_t{1}, lw)) return 0;
+      if (coef == INT32_MIN || g.lhs.terms[1] != std::make_pair(-coef, w)) return 0;
+    }
+    // lsum must be private: 1 + n reads in zero guards, 1 in overload guard,
+    // 2 as a target (tell + overload).
+    if (refs[lw] != n + 3) return 0;
+    Row r;
+    r.lsum = lw;
+    r.c = c;
+    for (auto [coef, w] : terms) r.terms.push_back(pack(coef, w));
+    rows.push_back(std::move(r));
+    return 2 + n;
+  };
+
+  for (std::size_t i = 0; i < cmds.size();) {
+    if (const std::size_t used = match_row(i)) {
+      i += used;
+      continue;
+    }
+    const CmdP& c = cmds[i];
+    // fold: unguarded constant tells
+    bool constant = c.guards.empty();
+    for (const auto* e : {&c.sc, &c.lb, &c.ub})
+      if (*e && !(*e)->terms.empty()) constant = false;
+    if (constant) {
+      if (c.kind == PCCP_INTERVAL) {
+        if (c.lb) { fold_w.push_back(static_cast<std::int32_t>(c.tw | 0x80000000u)); fold_v.push_back(c.lb->k); }
+        if (c.ub) { fold_w.push_back(static_cast<std::int32_t>(c.tw + 1)); fold_v.push_back(c.ub->k); }
+      } else {
+        fold_w.push_back(static_cast<std::int32_t>(c.tw | (out.word_up[c.tw] ? 0x80000000u : 0u)));
+        fold_v.push_back(c.sc->k);
+      }
+      ++i;
+      continue;
+    }
+    // small: interval target, <= 2 guards of <= 2 terms, <= 1 term per bound
+    bool ok = c.kind == PCCP_INTERVAL && c.guards.size() <= 2 && c.tw + 1 <= kTermWordMask;
+    Small s;
+    bool never = false;
+    int ng = 0;
+    std::uint32_t shape = 0;
+    if (ok) {
+      for (const GuardP& g : c.guards) {
+        auto n = normalise(g);
+        if (!n || n->terms.size() > 2) { ok = false; break; }
+        if (n->never) { never = true; break; }
+        if (n->always) continue;
+        for (std::size_t t = 0; t < n->terms.size(); ++t) {
+          if (!fits_term(n->terms[t].first, n->terms[t].second)) { ok = false; break; }
+          s.g[2 * ng + t] = pack(n->terms[t].first, n->terms[t].second);
+        }
+        s.T[ng] = n->T;
+        shape |= static_cast<std::uint32_t>(n->terms.size()) << (4 * ng);
+        ++ng;
+      }
+    }
+    if (never) {  // can never fire: dropped (still counted as a reference command)
+      ++out.n_dropped;
+      ++i;
+      continue;
+    }
+    if (ok) {
+      for (const auto* e : {&c.lb, &c.ub}) {
+        if (*e && ((*e)->terms.size() > 1 ||
+                   ((*e)->terms.size() == 1 && !fits_term((*e)->terms[0].first, (*e)->terms[0].second))))
+          ok = false;
+      }
+    }
+    if (!ok) {
+      generic.push_back(static_cast<std::uint32_t>(i));
+      ++i;
+      continue;
+    }
+    if (c.lb) {
+      s.lbk = c.lb->k;
+      if (!c.lb->terms.empty()) s.lbt = pack(c.lb->terms[0].first, c.lb->terms[0].second);
+      shape |= 1u << 8 | (c.lb->terms.empty() ? 0u : 1u << 9);
+    }
+    if (c.ub) {
+      s.ubk = c.ub->k;
+      if (!c.ub->terms.empty()) s.ubt = pack(c.ub->terms[0].first, c.ub->terms[0].second);
+      shape |= 1u << 10 | (c.ub->terms.empty() ? 0u : 1u << 11);
+    }
+    s.tw = static_cast<std::int32_t>(c.tw);
+    s.shape = shape | static_cast<std::uint32_t>(ng) << 12;
+    smalls.push_back(s);
+    ++i;
+  }
+  // Group shapes so a warp walks a homogeneous segment (fewer divergent paths).
+  std::stable_sort(smalls.begin(), smalls.end(), [](const Small& a, const Small& b) { return a.shape < b.shape; });
+
+  // ---- blob ----------------------------------------------------------------------
+  std::vector<std::int32_t>& B = out.blob;
+  auto reserve_arr = [&B](std::uint32_t n) {
+    const std::uint32_t off = align4(static_cast<std::uint32_t>(B.size()));
+    B.resize(off + n, 0);
+    return off;
+  };
+  const std::uint32_t ns = static_cast<std::uint32_t>(smalls.size());
+  L.n_small = ns;
+  for (int k = 0; k < 4; ++k) L.small_g[k] = reserve_arr(ns);
+  for (int k = 0; k < 2; ++k) L.small_T[k] = reserve_arr(ns);
+  L.small_lbk = reserve_arr(ns);
+  L.small_lbt = reserve_arr(ns);
+  L.small_ubk = reserve_arr(ns);
+  L.small_ubt = reserve_arr(ns);
+  L.small_tw = reserve_arr(ns);
+  for (std::uint32_t i = 0; i < ns; ++i) {
+    const Small& s = smalls[i];
+    for (int k = 0; k < 4; ++k) B[L.small_g[k] + i] = s.g[k];
+    for (int k = 0; k < 2; ++k) B[L.small_T[k] + i] = s.T[k];
+    B[L.small_lbk + i] = s.lbk;
+    B[L.small_lbt + i] = s.lbt;
+    B[L.small_ubk + i] = s.ubk;
+    B[L.small_ubt + i] = s.ubt;
+    B[L.small_tw + i] = s.tw;
+  }
+  L.n_rows = static_cast<std::uint32_t>(rows.size());
+  std::uint32_t n_terms = 0, max_terms = 0;
+  for (const Row& r : rows) {
+    n_terms += static_cast<std::uint32_t>(r.terms.size());
+    max_terms = std::max<std::uint32_t>(max_terms, static_cast<std::uint32_t>(r.terms.size()));
+  }
+  L.n_row_terms = n_terms;
+  L.row_lanes = 1;
+  while (L.row_lanes < 32 && L.row_lanes < max_terms) L.row_lanes <<= 1;
+  L.row_off = reserve_arr(L.n_rows + 1);
+  L.row_lsum = reserve_arr(L.n_rows);
+  L.row_c = reserve_arr(L.n_rows);
+  L.row_terms = reserve_arr(n_terms);
+  {
+    std::uint32_t t = 0;
+    for (std::uint32_t r = 0; r < L.n_rows; ++r) {
+      B[L.row_off + r] = static_cast<std::int32_t>(t);
+      B[L.row_lsum + r] = static_cast<std::int32_t>(rows[r].lsum);
+      B[L.row_c + r] = rows[r].c;
+      for (std::int32_t x : rows[r].terms) B[L.row_terms + t++] = x;
+    }
+    B[L.row_off + L.n_rows] = static_cast<std::int32_t>(t);
+  }
+  L.hot_words = static_cast<std::uint32_t>(B.size());
+
+  L.n_fold = static_cast<std::uint32_t>(fold_w.size());
+  L.fold_w = reserve_arr(L.n_fold);
+  L.fold_v = reserve_arr(L.n_fold);
+  for (std::uint32_t i = 0; i < L.n_fold; ++i) {
+    B[L.fold_w + i] = fold_w[i];
+    B[L.fold_v + i] = fold_v[i];
+  }
+
+  L.n_gen = static_cast<std::uint32_t>(generic.size());
+  L.gen_off = reserve_arr(L.n_gen + 1);
+  std::uint32_t gen_len = 0;
+  for (std::uint32_t g : generic) gen_len += m.cmd_off[g + 1] - m.cmd_off[g];
+  L.gen_code = reserve_arr(gen_len);
+  {
+    std::uint32_t p = 0;
+    for (std::uint32_t k = 0; k < L.n_gen; ++k) {
+      const std::uint32_t i = generic[k];
+      B[L.gen_off + k] = static_cast<std::int32_t>(p);
+      for (std::uint32_t x = m.cmd_off[i]; x < m.cmd_off[i + 1]; ++x) B[L.gen_code + p++] = m.cmd_code[x];
+    }
+    B[L.gen_off + L.n_gen] = static_cast<std::int32_t>(p);
+  }
+
+  std::vector<std::int32_t> iv, scw, sct;
+  for (std::uint32_t s = 0; s < m.n_slots; ++s) {
+    const int k = m.slot_kind[s];
+    if (k == PCCP_INTERVAL) {
+      iv.push_back(static_cast<std::int32_t>(m.slot_word[s]));
+    } else {
+      scw.push_back(static_cast<std::int32_t>(m.slot_word[s]));
+      sct.push_back(k == PCCP_ZINC ? INT32_MAX : k == PCCP_ZDEC ? INT32_MIN : k == PCCP_BINC ? 1 : 0);
+    }
+  }
+  L.n_iv = static_cast<std::uint32_t>(iv.size());
+  L.iv_lb = reserve_arr(L.n_iv);
+  std::copy(iv.begin(), iv.end(), B.begin() + L.iv_lb);
+  L.n_sc = static_cast<std::uint32_t>(scw.size());
+  L.sc_w = reserve_arr(L.n_sc);
+  L.sc_top = reserve_arr(L.n_sc);
+  std::copy(scw.begin(), scw.end(), B.begin() + L.sc_w);
+  std::copy(sct.begin(), sct.end(), B.begin() + L.sc_top);
+
+  std::vector<std::int32_t> cand;
+  if (m.n_cands == 0) {
+    for (std::uint32_t s = 0; s < m.n_slots; ++s)
+      if (m.slot_kind[s] == PCCP_INTERVAL) cand.push_back(static_cast<std::int32_t>(m.slot_word[s]));
+  } else {
+    if (!m.cands) bad("null candidate table");
+    for (std::uint32_t i = 0; i < m.n_cands; ++i) {
+      const std::int32_t s = m.cands[i];
+      if (s < 0 || static_cast<std::uint32_t>(s) >= m.n_slots) bad("candidate slot out of range");
+      if (m.slot_kind[s] == PCCP_INTERVAL) cand.push_back(static_cast<std::int32_t>(m.slot_word[s]));
+    }
+  }
+  L.n_cand = static_cast<std::uint32_t>(cand.size());
+  L.cand_lbw = reserve_arr(L.n_cand);
+  std::copy(cand.begin(), cand.end(), B.begin() + L.cand_lbw);
+
+  if (m.obj_slot >= 0) {
+    if (static_cast<std::uint32_t>(m.obj_slot) >= m.n_slots || m.slot_kind[m.obj_slot] != PCCP_INTERVAL)
+      bad("objective must be an interval slot");
+    L.obj_lbw = static_cast<std::int32_t>(m.slot_word[m.obj_slot]);
+  } else {
+    L.obj_lbw = -1;
+  }
+  L.blob_words = static_cast<std::uint32_t>(B.size());
+  if (B.empty()) B.push_back(0);
+  return out;
+}
+
+void host_join_decision(const pccp_model& m, std::int32_t* words, const pccp_decision& d) {
+  if (d.var < 0 || static_cast<std::uint32_t>(d.var) >= m.n_slots || m.slot_kind[d.var] != PCCP_INTERVAL)
+    throw std::runtime_error("decision on a non-interval slot");
+  const std::uint32_t w = m.slot_word[d.var];
+  if (d.upper) {
+    const std::int32_t lo = d.mid + 1;
+    if (lo > words[w]) words[w] = lo;
+  } else if (d.mid < words[w + 1]) {
+    words[w + 1] = d.mid;
+  }
+}
+
+}  // namespace pccp_b200

@@ -1,0 +1,74 @@
+// lower.hpp — flat reference tables -> device tables.
+//
+// The reference executes every GuardedCommand through one generic
+// interpreter (GuardedCommand::apply, command.cpp:100-113).  The device path
+// instead splits the command list into shape families, each a structure of
+// arrays that a warp walks with coalesced loads:
+//
+//   fold    unguarded constant tells (init domains).  Idempotent after their
+//           first application, so they are joined once at node entry instead
+//           of every round (exact: the store only grows).
+//   small   interval tells with <= 2 guards of <= 2 terms and <= 1 term per
+//           bound: every reified / not(and) / offset / binary-sum command.
+//           Guards are normalised to `sum tv(c_i, v_i) <= T` (H1 arithmetic).
+//   row     a general sum compiled by compile_sum (propagation.cpp:314-335):
+//           lsum tell + overload rule + one zeroing guard per term, fused
+//           into one row evaluated by a sub-warp from one read of the lbs (H2).
+//   generic anything else, interpreted from the flat stream on the device.
+//
+// Word indices are the reference's (H7), so stores round-trip unchanged.
+#pragma once
+
+#include <cstdint>
+#include <string>
+#include <vector>
+
+#include "../../../include/pccp_gpu.h"
+
+namespace pccp_b200 {
+
+// Packed term: (coef << 20) | word, coef in [-2048, 2047], word < 2^20.
+constexpr int kTermWordBits = 20;
+constexpr std::uint32_t kTermWordMask = (1u << kTermWordBits) - 1;
+
+struct DeviceLayout {
+  // offsets (int32 units) into the blob
+  std::uint32_t small_g[4], small_T[2], small_lbk, small_lbt, small_ubk, small_ubt, small_tw;
+  std::uint32_t n_small;
+  std::uint32_t fold_w, fold_v;  // fold_w: word | (up << 31)
+  std::uint32_t n_fold;
+  std::uint32_t row_off, row_lsum, row_c, row_terms;
+  std::uint32_t n_rows, n_row_terms, row_lanes;  // lanes per row (power of two <= 32)
+  std::uint32_t gen_off;                          // offsets into gen_code
+  std::uint32_t gen_code;
+  std::uint32_t n_gen;
+  std::uint32_t iv_lb;  // lb words of interval slots (failure scan)
+  std::uint32_t n_iv;
+  std::uint32_t sc_w, sc_top;  // scalar slots: word, top value
+  std::uint32_t n_sc;
+  std::uint32_t cand_lbw;  // lb word of each branching candidate, priority order
+  std::uint32_t n_cand;
+  std::int32_t obj_lbw;  // -1: no objective
+  std::uint32_t n_words;
+  std::uint32_t n_ref_cmds;
+  std::uint32_t blob_words;
+  std::uint32_t hot_words;  // prefix of the blob read every round (small + rows)
+};
+
+struct Lowered {
+  DeviceLayout L{};
+  std::vector<std::int32_t> blob;
+  std::uint32_t n_dropped = 0;  // commands that can never fire (guard rhs = +inf with '>')
+  double alg_bytes_per_eval = 0;  // SURVEY 8(d) B_alg over the reference commands
+  std::vector<std::uint8_t> word_up;
+  std::vector<std::int32_t> slot_of_word;  // for diagnostics
+};
+
+// Throws std::runtime_error (mapped to PCCP_EMODEL) on malformed tables.
+Lowered lower_model(const pccp_model& m);
+
+// Host-side join of a decision into a store (Decision::as_join +
+// Store::join_in_place on an Interval, solver.hpp:20-23, store.cpp:51-63).
+void host_join_decision(const pccp_model& m, std::int32_t* words, const pccp_decision& d);
+
+}  // namespace pccp_b200

@@ -1,0 +1,459 @@
+// search.cuh — node processing, EPS decomposition and the persistent DFS.
+//
+// Node = materialisation + fixed point (materialize, solver.cpp:91-102).  The
+// device keeps the parent's fixed point instead of replaying the decision path
+// from the subproblem root: the fixed point above (parent fixpoint ⊔ decision
+// ⊔ objective bound) equals the fixed point above (root ⊔ path ⊔ bound) — the
+// reference's own "replay = incremental descent" property
+// (test_solver.cpp:196-227) — and tests/test_gpu_parity.py replays sampled
+// paths on the CPU oracle to prove it per node.
+#pragma once
+
+#include "kernels.cuh"
+
+namespace pccp_b200 {
+namespace dev {
+
+struct SearchCtl {
+  Globals* G;
+  int* best_store;       // n_words, the best solution store
+  int* const* peers;     // peer replicas of the incumbent cell (system-scope atomics)
+  int n_peers;
+  int mode;              // 0: enumerate, 1: minimise the objective
+  int hash;              // accumulate the fixed-point hash-sum
+  int depth_cap;         // < 0: none
+  int count;             // accumulate counters (EPS on shard 0 only)
+};
+
+struct Cnt {
+  unsigned long long nodes = 0, fails = 0, sols = 0, open = 0, hash = 0, rounds = 0, maxd = 0;
+};
+
+__device__ __forceinline__ void flush(Globals* G, Cnt& c) {
+  if (c.nodes) atomicAdd(&G->nodes, c.nodes);
+  if (c.fails) atomicAdd(&G->failures, c.fails);
+  if (c.sols) atomicAdd(&G->solutions, c.sols);
+  if (c.open) atomicAdd(&G->open_leaves, c.open);
+  if (c.hash) atomicAdd(&G->hash_sum, c.hash);
+  if (c.rounds) atomicAdd(&G->rounds, c.rounds);
+  if (c.maxd) atomicMax(&G->max_depth, c.maxd);
+  c = Cnt{};
+}
+
+// Objective tightening at materialisation (solver.cpp:96-99): obj <= best-1.
+template <class G>
+__device__ __forceinline__ void join_objective(const G& g, volatile int* S, const DeviceLayout& L,
+                                               const SearchCtl& C) {
+  if (C.mode == 1 && L.obj_lbw >= 0 && g.rank() == 0) {
+    const int best = *(volatile int*)&C.G->incumbent;
+    if (best != INT_MAX) join_min(S, L.obj_lbw + 1, best - 1);
+  }
+}
+
+// SharedControl::should_stop (solver.cpp:68-76): stop flag, timeout, node limit.
+template <class G>
+__device__ __forceinline__ bool should_stop(const G& g, const SearchCtl& C) {
+  int stop = 0;
+  if (g.rank() == 0) {
+    Globals* Gl = C.G;
+    stop = *(volatile int*)&Gl->stop;
+    if (!stop && Gl->timeout_ns && globaltimer() - Gl->t0 >= Gl->timeout_ns) {
+      atomicCAS(&Gl->stop, 0, 1);
+      stop = 1;
+    }
+    if (!stop && Gl->node_limit != ~0ull) {
+      // one reservation per materialisation; the limit admits exactly node_limit nodes
+      if (atomicAdd(&Gl->nodes_reserved, 1ull) >= Gl->node_limit) {
+        atomicCAS(&Gl->stop, 0, 1);
+        stop = 1;
+      }
+    }
+  }
+  return g.bcast0(stop) != 0;
+}
+
+// record_solution + Objective::improve (solver.cpp:104-118, solver.hpp:43-49):
+// CAS-min on the incumbent, pushed to every peer GPU's replica; the best
+// store is written under a lock so it always matches best_value.
+template <class G>
+__device__ void record_solution(const G& g, volatile int* S, const DeviceLayout& L, const SearchCtl& C, Cnt& cnt) {
+  Globals* Gl = C.G;
+  const int value = S[L.obj_lbw];
+  int improved = 0;
+  if (g.rank() == 0) {
+    const int old = atomicMin(&Gl->incumbent, value);
+    improved = value < old;
+    if (improved) {
+      for (int p = 0; p < C.n_peers; ++p) atomicMin_system(C.peers[p], value);
+      const int k = atomicAdd(&Gl->n_impr, 1);
+      if (k < 64) {
+        Gl->impr_val[k] = value;
+        Gl->impr_ns[k] = globaltimer() - Gl->t0;
+      }
+      while (atomicCAS(&Gl->best_lock, 0, 1) != 0) {
+      }
+      if (C.count) ++cnt.sols;
+    }
+  }
+  improved = g.bcast0(improved);
+  if (!improved) return;
+  int do_copy = 0;
+  if (g.rank() == 0) do_copy = value < *(volatile int*)&Gl->best_value;
+  do_copy = g.bcast0(do_copy);
+  if (do_copy) copy_out(g, C.best_store, S, (int)L.n_words);
+  __threadfence();
+  g.sync();
+  if (g.rank() == 0) {
+    if (do_copy) *(volatile int*)&Gl->best_value = value;
+    __threadfence();
+    atomicExch(&Gl->best_lock, 0);
+  }
+}
+
+// After a node's fixed point: count, hash, classify.  Returns 1 when the node
+// must be expanded (lbw/mid set), 0 when it is a leaf, -1 on a model error.
+template <class G>
+__device__ int classify(const G& g, volatile int* S, const int* __restrict__ T, const DeviceLayout& L,
+                        const SearchCtl& C, Cnt& cnt, bool failed, int depth, int& lbw, int& mid) {
+  if (failed) {
+    if (C.count) ++cnt.fails;
+    return 0;
+  }
+  if (C.hash && C.count && g.rank() == 0) cnt.hash += store_hash(S, (int)L.n_words);
+  const int b = branch(g, S, T, L, lbw, mid);
+  if (b < 0) {
+    if (g.rank() == 0) {
+      C.G->error_code = 1;
+      atomicExch(&C.G->stop, 2);
+    }
+    return -1;
+  }
+  if (b == 0) {  // every candidate fixed: a solution
+    if (C.mode == 1) record_solution(g, S, L, C, cnt);
+    else if (C.count) ++cnt.sols;
+    return 0;
+  }
+  if (C.depth_cap >= 0 && depth >= C.depth_cap) {
+    if (C.count) ++cnt.open;
+    return 0;
+  }
+  return 1;
+}
+
+// Kernel prologue: optional smem copy of the tables, CTA scratch, group store.
+struct Frame {
+  const int* __restrict__ T;
+  int* ring;
+  unsigned long long* red;
+  int* stores;
+};
+
+__device__ __forceinline__ Frame frame(const Model& M) {
+  extern __shared__ __align__(16) int smem[];
+  Frame f;
+  int off = 0;
+  f.T = M.blob;
+  if (M.table_in_smem) {
+    const int4* src = reinterpret_cast<const int4*>(M.blob);
+    int4* dst = reinterpret_cast<int4*>(smem);
+    const int n4 = ((int)M.L.blob_words + 3) >> 2;
+    for (int i = threadIdx.x; i < n4; i += blockDim.x) dst[i] = src[i];
+    f.T = smem;
+    off = n4 * 4;
+  }
+  f.ring = smem + off;
+  f.red = reinterpret_cast<unsigned long long*>(smem + off + 4);
+  off += 72;
+  f.stores = smem + off;
+  __syncthreads();
+  return f;
+}
+
+template <class G>
+struct GroupOf;
+template <>
+struct GroupOf<WarpGroup> {
+  static __device__ __forceinline__ WarpGroup make(const Frame&) { return WarpGroup{(int)(threadIdx.x & 31)}; }
+  static __device__ __forceinline__ int in_cta() { return (int)(threadIdx.x >> 5); }
+  static __device__ __forceinline__ int per_cta() { return (int)(blockDim.x >> 5); }
+};
+template <>
+struct GroupOf<CtaGroup> {
+  static __device__ __forceinline__ CtaGroup make(const Frame& f) {
+    return CtaGroup{(int)threadIdx.x, (int)blockDim.x, f.ring, f.red};
+  }
+  static __device__ __forceinline__ int in_cta() { return 0; }
+  static __device__ __forceinline__ int per_cta() { return 1; }
+};
+
+// ---- K1: batched fixed points (run_sequential on N independent stores) ---------
+template <class G>
+__global__ void k_propagate(Model M, int* stores, int n, int stride, unsigned char* status, unsigned* rounds,
+                            int fold) {
+  const Frame f = frame(M);
+  const G g = GroupOf<G>::make(f);
+  volatile int* S = f.stores + GroupOf<G>::in_cta() * M.store_stride;
+  const int gid = blockIdx.x * GroupOf<G>::per_cta() + GroupOf<G>::in_cta();
+  const int ng = gridDim.x * GroupOf<G>::per_cta();
+  for (int i = gid; i < n; i += ng) {
+    int* io = stores + (size_t)i * stride;
+    copy_words(g, S, io, (int)M.L.n_words);
+    g.sync();
+    if (fold) {
+      apply_fold(g, S, f.T, M.L);
+      g.sync();
+    }
+    int r = 0;
+    const bool failed = propagate(g, S, f.T, M.L, r);
+    copy_out(g, io, S, (int)M.L.n_words);
+    if (g.rank() == 0) {
+      status[i] = failed ? 1 : 0;
+      if (rounds) rounds[i] = (unsigned)r;
+    }
+    g.sync();
+  }
+}
+
+// ---- the problem root: fold, objective, fixed point, classification ----------------
+template <class G>
+__global__ void k_root(Model M, SearchCtl C, int* store, unsigned char* flag) {
+  const Frame f = frame(M);
+  const G g = GroupOf<G>::make(f);
+  if (GroupOf<G>::in_cta() != 0 || blockIdx.x != 0) return;
+  volatile int* S = f.stores;
+  Cnt cnt;
+  copy_words(g, S, store, (int)M.L.n_words);
+  g.sync();
+  apply_fold(g, S, f.T, M.L);
+  g.sync();
+  join_objective(g, S, M.L, C);
+  g.sync();
+  int r = 0;
+  const bool failed = propagate(g, S, f.T, M.L, r);
+  if (C.count) {
+    ++cnt.nodes;
+    cnt.rounds += (unsigned long long)r;
+  }
+  int lbw = 0, mid = 0;
+  const int e = classify(g, S, f.T, M.L, C, cnt, failed, 0, lbw, mid);
+  copy_out(g, store, S, (int)M.L.n_words);
+  if (g.rank() == 0) {
+    *flag = e == 1 ? 1 : 0;
+    flush(C.G, cnt);
+  }
+}
+
+// ---- K5: one level of the EPS decomposition (decompose, solver.cpp:180-213) ------
+// Parent p's children go to slots 2p (left, x <= mid) and 2p+1 (right); the
+// compaction below keeps BFS order, so the frontier is identical on every GPU.
+template <class G>
+__global__ void k_expand(Model M, SearchCtl C, const int* parents, const int* parent_idx, int n_par, int stride,
+                         int child_depth, int* children, unsigned char* flags) {
+  const Frame f = frame(M);
+  const G g = GroupOf<G>::make(f);
+  volatile int* S = f.stores + GroupOf<G>::in_cta() * M.store_stride;
+  const int gid = blockIdx.x * GroupOf<G>::per_cta() + GroupOf<G>::in_cta();
+  const int ng = gridDim.x * GroupOf<G>::per_cta();
+  const DeviceLayout& L = M.L;
+  Cnt cnt;
+  for (int p = gid; p < n_par; p += ng) {
+    const int* par = parents + (size_t)parent_idx[p] * stride;
+    copy_words(g, S, par, (int)L.n_words);
+    g.sync();
+    int lbw = 0, mid = 0;
+    const int b = branch(g, S, f.T, L, lbw, mid);
+    for (int side = 0; side < 2; ++side) {
+      unsigned char keep = 0;
+      if (b == 1) {
+        if (side == 1) {
+          copy_words(g, S, par, (int)L.n_words);
+          g.sync();
+        }
+        if (g.rank() == 0) {
+          if (side == 0) join_min(S, lbw + 1, mid);
+          else join_max(S, lbw, mid + 1);
+        }
+        g.sync();
+        join_objective(g, S, L, C);
+        g.sync();
+        int r = 0;
+        const bool failed = propagate(g, S, f.T, L, r);
+        if (C.count) {
+          ++cnt.nodes;
+          cnt.rounds += (unsigned long long)r;
+          if ((unsigned long long)child_depth > cnt.maxd) cnt.maxd = (unsigned long long)child_depth;
+        }
+        int clbw, cmid;
+        const int e = classify(g, S, f.T, L, C, cnt, failed, child_depth, clbw, cmid);
+        if (e == 1) {
+          copy_out(g, children + (size_t)(2 * p + side) * stride, S, (int)L.n_words);
+          keep = 1;
+        }
+      } else if (b < 0 && g.rank() == 0) {
+        C.G->error_code = 1;
+        atomicExch(&C.G->stop, 2);
+      }
+      if (g.rank() == 0) flags[2 * p + side] = keep;
+      g.sync();
+    }
+  }
+  if (g.rank() == 0) flush(C.G, cnt);
+}
+
+// Stable compaction of the child flags into the next frontier's index list.
+__global__ void k_compact(const unsigned char* flags, int n, int* idx, int* count) {
+  __shared__ int wsum[32];
+  __shared__ int base;
+  const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+  if (tid == 0) base = 0;
+  __syncthreads();
+  for (int start = 0; start < n; start += blockDim.x) {
+    const int i = start + tid;
+    const bool f = i < n && flags[i];
+    const unsigned m = __ballot_sync(kFull, f);
+    const int pre = __popc(m & ((1u << lane) - 1u));
+    if (lane == 0) wsum[wid] = __popc(m);
+    __syncthreads();
+    if (wid == 0) {
+      int v = lane < (int)(blockDim.x >> 5) ? wsum[lane] : 0;
+      for (int o = 1; o < 32; o <<= 1) {
+        const int u = __shfl_up_sync(kFull, v, o);
+        if (lane >= o) v += u;
+      }
+      wsum[lane] = v;
+    }
+    __syncthreads();
+    const int woff = wid == 0 ? 0 : wsum[wid - 1];
+    if (f) idx[base + woff + pre] = i;
+    __syncthreads();
+    if (tid == 0) base += wsum[31];
+    __syncthreads();
+  }
+  if (tid == 0) *count = base;
+}
+
+__global__ void k_init_clock(Globals* G) { G->t0 = globaltimer(); }
+
+struct SearchParams {
+  const int* frontier;
+  const int* frontier_idx;
+  int n_frontier;
+  int stride;
+  int depth0;
+  int shard_index, shard_count;
+  int* stack_pool;
+  int stack_depth;   // entries per group
+  int entry_stride;  // words per entry: store + (lbw, mid, depth)
+};
+
+// ---- K4 + K6: persistent DFS over the EPS work queue ------------------------------
+// Each group pops subproblem k (this GPU owns frontier i = shard_index +
+// k*shard_count) and explores it depth-first, left branch first (dfs,
+// solver.cpp:122-146).  A branching node pushes (its fixed point, right
+// decision) and descends left in place; a leaf pops.
+template <class G>
+__global__ void k_search(Model M, SearchCtl C, SearchParams P) {
+  const Frame f = frame(M);
+  const G g = GroupOf<G>::make(f);
+  volatile int* S = f.stores + GroupOf<G>::in_cta() * M.store_stride;
+  const int gid = blockIdx.x * GroupOf<G>::per_cta() + GroupOf<G>::in_cta();
+  const DeviceLayout& L = M.L;
+  const int nw = (int)L.n_words;
+  int* stk = P.stack_pool + (size_t)gid * (size_t)P.stack_depth * (size_t)P.entry_stride;
+  Globals* Gl = C.G;
+  Cnt cnt;
+  for (;;) {
+    int k = 0;
+    if (g.rank() == 0) k = (int)atomicAdd(&Gl->cursor, 1u);
+    k = g.bcast0(k);
+    const long long idx = (long long)P.shard_index + (long long)k * (long long)P.shard_count;
+    if (idx >= P.n_frontier) break;
+    int stop = 0;
+    if (g.rank() == 0) stop = *(volatile int*)&Gl->stop;
+    if (g.bcast0(stop)) {
+      if (g.rank() == 0) Gl->incomplete = 1;
+      break;
+    }
+    copy_words(g, S, P.frontier + (size_t)P.frontier_idx[idx] * P.stride, nw);
+    g.sync();
+    int depth = P.depth0;
+    int sp = 0;
+    // Enumeration: the frontier node was counted and classified during the
+    // decomposition.  Minimisation: re-materialise it with the current bound,
+    // as dfs() does for its subproblem root.
+    bool need_prop = C.mode == 1;
+    bool abandoned = false;
+    if (need_prop) {
+      join_objective(g, S, L, C);
+      g.sync();
+    }
+    for (;;) {
+      int lbw = 0, mid = 0, e;
+      if (need_prop) {
+        if (should_stop(g, C)) {
+          abandoned = true;
+          break;
+        }
+        int r = 0;
+        const bool failed = propagate(g, S, f.T, L, r);
+        ++cnt.nodes;
+        cnt.rounds += (unsigned long long)r;
+        if ((unsigned long long)depth > cnt.maxd) cnt.maxd = (unsigned long long)depth;
+        e = classify(g, S, f.T, L, C, cnt, failed, depth, lbw, mid);
+      } else {
+        e = branch(g, S, f.T, L, lbw, mid);
+      }
+      if (e < 0) {
+        abandoned = true;
+        break;
+      }
+      if (e == 1) {
+        if (sp >= P.stack_depth) {  // capacity: cannot happen with the host's depth bound
+          if (g.rank() == 0) {
+            Gl->error_code = 2;
+            atomicExch(&Gl->stop, 2);
+          }
+          abandoned = true;
+          break;
+        }
+        int* ent = stk + (size_t)sp * P.entry_stride;
+        copy_out(g, ent, S, nw);
+        if (g.rank() == 0) {
+          ent[nw] = lbw;
+          ent[nw + 1] = mid;
+          ent[nw + 2] = depth;
+          join_min(S, lbw + 1, mid);  // left branch: x <= mid
+        }
+        ++sp;
+        ++depth;
+        g.sync();
+        join_objective(g, S, L, C);
+        g.sync();
+        need_prop = true;
+        continue;
+      }
+      if (sp == 0) break;
+      --sp;
+      const int* ent = stk + (size_t)sp * P.entry_stride;
+      copy_words(g, S, ent, nw);
+      g.sync();
+      if (g.rank() == 0) {
+        join_max(S, ent[nw], ent[nw + 1] + 1);  // right branch: x >= mid+1
+      }
+      depth = ent[nw + 2] + 1;
+      g.sync();
+      join_objective(g, S, L, C);
+      g.sync();
+      need_prop = true;
+    }
+    if (g.rank() == 0) {
+      if (abandoned) Gl->incomplete = 1;
+      flush(Gl, cnt);
+    }
+    if (abandoned) break;
+  }
+  if (g.rank() == 0) flush(Gl, cnt);
+}
+
+}  // namespace dev
+}  // namespace pccp_b200

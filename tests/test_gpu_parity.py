@@ -1,0 +1,195 @@
+"""Parity of the CUDA path against the reference (golden fixtures generated from
+the reference library by tests/golden/make_golden.py) and the C oracle.
+
+Integer work: every comparison is bit-exact.  Node counts of the optimisation
+runs differ from the reference only through search order (incumbent timing);
+those tests compare optima and check every solution independently."""
+import numpy as np
+import pytest
+
+from conftest import load_micro_csps, load_micro_rcpsps
+from oracle.port import Oracle, store_hash
+
+pytestmark = pytest.mark.gpu
+
+CONFIG_BUILDERS = {}
+
+
+def build(name):
+    from paper_2207_12116_b200 import Model
+    if name.startswith("nqueens"):
+        return Model.nqueens(int(name[len("nqueens"):]))
+    if name == "csp1":
+        return Model.random_csp(1)
+    if name.startswith("csp_small"):
+        return Model.random_csp(int(name[len("csp_small"):]), n_vars=60, n_cons=200)
+    if name.startswith("rcpsp30_s"):
+        return Model.rcpsp_random(int(name[len("rcpsp30_s"):]), 30, 4)
+    if name.startswith("rcpsp10_s"):
+        return Model.rcpsp_random(int(name[len("rcpsp10_s"):]), 10, 2)
+    if name.startswith("rcpsp120_s"):
+        return Model.rcpsp_random(int(name[len("rcpsp120_s"):]), 120, 4)
+    return None
+
+
+@pytest.fixture(scope="module")
+def engine():
+    from paper_2207_12116_b200 import Engine
+    with Engine(0) as e:
+        yield e
+
+
+@pytest.fixture(scope="module")
+def hengine():
+    from paper_2207_12116_b200 import Engine
+    with Engine(0, hash=True) as e:
+        yield e
+
+
+def config_names(golden, prefix=None):
+    return [n for n in golden if build(n) is not None and (prefix is None or n.startswith(prefix))]
+
+
+def test_root_fixpoints_all_configs(golden, engine):
+    """run_sequential on the bottom store of every configuration (K1)."""
+    for name in config_names(golden):
+        g = golden[name]
+        m = build(name)
+        assert m.tables().n_cmds == g["n_cmds"], name
+        engine.load(m)
+        failed, words, rounds = engine.run_sequential()
+        assert failed == g["root"]["failed"], name
+        if not failed:
+            assert store_hash(words) == g["root"]["hash"], name
+
+
+@pytest.mark.parametrize("tag", ["micro_csp_s2", "micro_csp_s4242"])
+def test_micro_csp_fixpoints(tag, engine):
+    """The reference acceptance confluence instances (acceptance_main.cpp:170-174)
+    and test_engine.cpp:94-114's: GPU fixed point == run_sequential's."""
+    for i, (t, failed, fix, _) in enumerate(load_micro_csps(tag)):
+        engine.load(t)
+        f, w, _ = engine.run_sequential()
+        assert f == failed, (tag, i)
+        if not failed:
+            assert np.array_equal(w, fix), (tag, i)
+
+
+def test_micro_csp_batch_random_stores(engine):
+    """Batched K1 on random sub-boxes of every micro CSP vs the C oracle."""
+    rng = np.random.default_rng(7)
+    for t, _, _, _ in load_micro_csps("micro_csp_s2")[:200]:
+        o = Oracle(t)
+        engine.load(t)
+        base = o.bottom()
+        stores = []
+        for _ in range(8):
+            s = base.copy()
+            for k, w in zip(t.slot_kind, t.slot_word):
+                if k == 4:
+                    a, b = sorted(rng.integers(-1, 10, 2))
+                    s[w], s[w + 1] = a, b + int(rng.integers(0, 3))
+            stores.append(s)
+        out, failed, _ = engine.propagate_batch(np.stack(stores))
+        for s, w, f in zip(stores, out, failed):
+            fo, wo, _, _ = o.run_sequential(s)
+            assert f == fo
+            if not f:
+                assert np.array_equal(w, wo)
+
+
+def test_replayed_paths(golden, engine):
+    """materialize() of sampled decision paths (with objective bounds) == reference."""
+    for name in config_names(golden):
+        g = golden[name]
+        reps = g.get("replays")
+        if not reps:
+            continue
+        engine.load(build(name))
+        paths = [r["decisions"] for r in reps]
+        best = [r["best"] for r in reps]
+        out, failed = engine.replay(paths, best)
+        for r, w, f in zip(reps, out, failed):
+            assert f == r["failed"], name
+            if not f:
+                assert store_hash(w) == r["hash"], name
+
+
+@pytest.mark.parametrize("n", [4, 5, 6, 8, 10])
+def test_enumerate_nqueens(n, golden, hengine):
+    g = golden[f"nqueens{n}"]["enumerate"]
+    res = hengine.load(build(f"nqueens{n}")).enumerate()
+    for k in ("nodes", "failures", "solutions", "open_leaves", "hash_sum"):
+        assert res[k] == g[k], (n, k)
+    assert res["exhausted"]
+
+
+def test_enumerate_csp_depth12(golden, hengine):
+    g = golden["csp1"]["enumerate_d12"]
+    res = hengine.load(build("csp1")).enumerate(depth_cap=12)
+    for k in ("nodes", "failures", "solutions", "open_leaves", "hash_sum"):
+        assert res[k] == g[k], k
+
+
+@pytest.mark.parametrize("seed", [2, 3])
+def test_enumerate_small_csp(seed, golden, hengine):
+    g = golden[f"csp_small{seed}"]["enumerate_d10"]
+    res = hengine.load(build(f"csp_small{seed}")).enumerate(depth_cap=10)
+    for k in ("nodes", "failures", "solutions", "open_leaves", "hash_sum"):
+        assert res[k] == g[k], k
+
+
+@pytest.mark.parametrize("seed", [1, 5, 11])
+def test_rcpsp30_optimum(seed, golden, engine):
+    m = build(f"rcpsp30_s{seed}")
+    res = engine.load(m).solve(timeout_s=120)
+    assert res.status == "OPTIMAL"
+    assert res.objective == golden[f"rcpsp30_s{seed}"]["optimum"]["value"]
+    assert m.check_solution(res.best_words)
+    incs = [v for v, _ in res.improvements]
+    assert all(a > b for a, b in zip(incs, incs[1:]))  # strictly decreasing (test_solver.cpp:247-261)
+
+
+@pytest.mark.parametrize("seed", range(1, 9))
+def test_rcpsp10_optimum(seed, golden, engine):
+    g = golden[f"rcpsp10_s{seed}"]["solve_dfs"]
+    m = build(f"rcpsp10_s{seed}")
+    res = engine.load(m).solve()
+    assert res.status == {0: "OPTIMAL", 2: "UNSAT"}[g["status"]]
+    assert res.objective == g["objective"]
+    if res.objective is not None:
+        assert m.check_solution(res.best_words)
+
+
+def test_micro_rcpsp_optimality(engine):
+    """200 micro RCPSPs of the optimality criterion (acceptance_main.cpp:243-287):
+    GPU optimum == brute-force enumeration, UNSAT where the reference proves it."""
+    for t, rec in load_micro_rcpsps():
+        engine.load(t)
+        res = engine.solve()
+        if rec["brute_force"] is None:
+            assert res.status == "UNSAT"
+        else:
+            assert res.status == "OPTIMAL" and res.objective == rec["brute_force"]
+
+
+def test_node_limit_zero_is_unknown(engine):
+    from paper_2207_12116_b200 import Model
+    m = Model.rcpsp([0, 2, 3, 0], [[0], [1], [1], [0]], [1], [(0, 1), (0, 2), (1, 2), (1, 3), (2, 3)], 5)
+    engine.load(m)
+    assert engine.solve(node_limit=0).status == "UNKNOWN"
+    r = engine.solve()
+    assert r.status == "OPTIMAL" and r.objective == 5  # test_solver.cpp:70-79
+
+
+def test_unsat_below_healthy_root(engine):
+    """test_solver.cpp:105-126: three unit tasks on capacity one cannot fit horizon 5."""
+    from paper_2207_12116_b200 import Model
+    prec = []
+    for i in (1, 2, 3):
+        prec += [(0, i), (i, 4)]
+    m = Model.rcpsp([0, 2, 2, 2, 0], [[0], [1], [1], [1], [0]], [1], prec, 5)
+    engine.load(m)
+    failed, _, _ = engine.run_sequential()
+    assert not failed
+    assert engine.solve().status == "UNSAT"
