@@ -135,24 +135,36 @@ struct pccp_gpu_ctx {
 
 namespace {
 
-template <class Gp>
+template <class Gp, bool TS>
 void set_smem_attrs(size_t smem) {
-  CK(cudaFuncSetAttribute(dev::k_propagate<Gp>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-  CK(cudaFuncSetAttribute(dev::k_root<Gp>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-  CK(cudaFuncSetAttribute(dev::k_expand<Gp>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-  CK(cudaFuncSetAttribute(dev::k_search<Gp>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  CK(cudaFuncSetAttribute(dev::k_propagate<Gp, TS>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  CK(cudaFuncSetAttribute(dev::k_root<Gp, TS>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  CK(cudaFuncSetAttribute(dev::k_expand<Gp, TS>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  CK(cudaFuncSetAttribute(dev::k_search<Gp, TS>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
 }
 
-template <class Gp>
+template <class Gp, bool TS>
 int occupancy(int block, size_t smem) {
   int occ = 0;
-  CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, dev::k_search<Gp>, block, smem));
+  CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, dev::k_search<Gp, TS>, block, smem));
   return occ;
+}
+
+// Calls f.template operator()<Group, TableInSmem>() for the context's plan.
+template <class F>
+void dispatch(const pccp_gpu_ctx* c, F&& f) {
+  if (c->warp) {
+    if (c->table_in_smem) f.template operator()<dev::WarpGroup, true>();
+    else f.template operator()<dev::WarpGroup, false>();
+  } else {
+    if (c->table_in_smem) f.template operator()<dev::CtaGroup, true>();
+    else f.template operator()<dev::CtaGroup, false>();
+  }
 }
 
 void plan(pccp_gpu_ctx* c) {
   const DeviceLayout& L = c->low.L;
-  c->store_stride = (int)align4(std::max<std::uint32_t>(L.n_words, 1));
+  c->store_stride = (int)align4(L.n_words + 1);  // + the constant-zero word
   const int gt = c->cfg.group_threads;
   c->warp = gt == 32 || (gt == 0 && L.n_words <= 256);
   if (c->warp) {
@@ -176,14 +188,11 @@ void plan(pccp_gpu_ctx* c) {
   if (env) in_smem = std::atoi(env) != 0 && base + table <= c->smem_optin;
   c->table_in_smem = in_smem ? 1 : 0;
   c->smem = base + (in_smem ? table : 0);
-  int occ;
-  if (c->warp) {
-    set_smem_attrs<dev::WarpGroup>(c->smem);
-    occ = occupancy<dev::WarpGroup>(c->block, c->smem);
-  } else {
-    set_smem_attrs<dev::CtaGroup>(c->smem);
-    occ = occupancy<dev::CtaGroup>(c->block, c->smem);
-  }
+  int occ = 0;
+  dispatch(c, [&]<class Gp, bool TS>() {
+    set_smem_attrs<Gp, TS>(c->smem);
+    occ = occupancy<Gp, TS>(c->block, c->smem);
+  });
   if (occ < 1) throw LimitError("kernel does not fit on an SM (smem " + std::to_string(c->smem) + " B)");
   if (c->cfg.ctas_per_sm > 0) occ = std::min(occ, c->cfg.ctas_per_sm);
   c->ctas = c->n_sm * occ;
@@ -226,7 +235,7 @@ struct RunOut {
   bool root_failed = false;
 };
 
-template <class Gp>
+template <class Gp, bool TS>
 void run_search(pccp_gpu_ctx* c, int mode, const int32_t* root_words, int depth_cap, const pccp_limits* lim,
                 RunOut& out) {
   const double t_start = now_ms();
@@ -257,7 +266,7 @@ void run_search(pccp_gpu_ctx* c, int mode, const int32_t* root_words, int depth_
   const int zero = 0;
   CK(cudaMemcpyAsync(c->ia.p, &zero, 4, cudaMemcpyHostToDevice, c->stream));
   CK(cudaEventRecord(c->ev[0], c->stream));
-  dev::k_root<Gp><<<1, c->block, c->smem, c->stream>>>(M, C, c->fa.p, c->flags.p);
+  dev::k_root<Gp, TS><<<1, c->block, c->smem, c->stream>>>(M, C, c->fa.p, c->flags.p);
   CK(cudaGetLastError());
   ++c->launches;
   unsigned char rflag = 0;
@@ -283,7 +292,7 @@ void run_search(pccp_gpu_ctx* c, int mode, const int32_t* root_words, int depth_
     c->ib.ensure(nchild);
     c->flags.ensure(nchild);
     const int grid = (int)std::min<long long>(c->ctas, (count + (c->warp ? c->gpc : 1) - 1) / (c->warp ? c->gpc : 1));
-    dev::k_expand<Gp><<<grid, c->block, c->smem, c->stream>>>(M, C, c->fa.p, c->ia.p, count, stride, level + 1,
+    dev::k_expand<Gp, TS><<<grid, c->block, c->smem, c->stream>>>(M, C, c->fa.p, c->ia.p, count, stride, level + 1,
                                                                 c->fb.p, c->flags.p);
     CK(cudaGetLastError());
     dev::k_compact<<<1, 1024, 0, c->stream>>>(c->flags.p, (int)nchild, c->ib.p, dcount.p);
@@ -317,7 +326,7 @@ void run_search(pccp_gpu_ctx* c, int mode, const int32_t* root_words, int depth_
     P.stack_depth = dmax;
     P.entry_stride = entry;
     C.count = 1;
-    dev::k_search<Gp><<<c->ctas, c->block, c->smem, c->stream>>>(M, C, P);
+    dev::k_search<Gp, TS><<<c->ctas, c->block, c->smem, c->stream>>>(M, C, P);
     CK(cudaGetLastError());
     ++c->launches;
     searched = true;
@@ -483,6 +492,31 @@ int pccp_gpu_lowering_info(pccp_gpu_ctx* c, pccp_lowering_info* o) {
   });
 }
 
+int pccp_lower_only(const pccp_model* m, pccp_lowering_info* o, uint32_t* shape_counts) {
+  return api([&] {
+    if (!m || !o) throw ArgError("null argument");
+    const Lowered low = lower_model(*m);
+    const DeviceLayout& L = low.L;
+    std::memset(o, 0, sizeof(*o));
+    o->n_words = L.n_words;
+    o->n_cmds = L.n_ref_cmds;
+    o->n_folded = L.n_fold;
+    o->n_small = L.n_small;
+    o->n_rows = L.n_rows;
+    o->n_row_terms = L.n_row_terms;
+    o->n_generic = L.n_gen;
+    o->table_bytes = L.blob_words * 4;
+    o->store_bytes = L.n_words * 4;
+    o->alg_bytes_per_eval = low.alg_bytes_per_eval;
+    if (shape_counts) {
+      shape_counts[0] = L.n_unit1;
+      shape_counts[1] = L.n_unit2;
+      shape_counts[2] = low.n_dropped;
+    }
+    return PCCP_OK;
+  });
+}
+
 int pccp_gpu_propagate_batch(pccp_gpu_ctx* c, const int32_t* in, uint32_t n, int32_t* out, uint8_t* status,
                              uint32_t* rounds) {
   return api([&] {
@@ -497,12 +531,10 @@ int pccp_gpu_propagate_batch(pccp_gpu_ctx* c, const int32_t* in, uint32_t n, int
     const dev::Model M = c->model();
     const int per = c->warp ? c->gpc : 1;
     const int grid = (int)std::min<long long>(c->ctas, ((long long)n + per - 1) / per);
-    if (c->warp)
-      dev::k_propagate<dev::WarpGroup><<<grid, c->block, c->smem, c->stream>>>(M, c->io.p, (int)n, (int)nw, c->st.p,
-                                                                               c->rnd.p, 1);
-    else
-      dev::k_propagate<dev::CtaGroup><<<grid, c->block, c->smem, c->stream>>>(M, c->io.p, (int)n, (int)nw, c->st.p,
-                                                                              c->rnd.p, 1);
+    dispatch(c, [&]<class Gp, bool TS>() {
+      dev::k_propagate<Gp, TS><<<grid, c->block, c->smem, c->stream>>>(M, c->io.p, (int)n, (int)nw, c->st.p,
+                                                                       c->rnd.p, 1);
+    });
     CK(cudaGetLastError());
     ++c->launches;
     if (nw) CK(cudaMemcpyAsync(out, c->io.p, (size_t)n * nw * 4, cudaMemcpyDeviceToHost, c->stream));
@@ -543,8 +575,7 @@ int pccp_gpu_enumerate(pccp_gpu_ctx* c, const int32_t* root, int32_t depth_cap, 
     std::memset(out, 0, sizeof(*out));
     if (lim && lim->node_limit == 0) return PCCP_OK;
     RunOut r;
-    if (c->warp) run_search<dev::WarpGroup>(c, 0, root, depth_cap, lim, r);
-    else run_search<dev::CtaGroup>(c, 0, root, depth_cap, lim, r);
+    dispatch(c, [&]<class Gp, bool TS>() { run_search<Gp, TS>(c, 0, root, depth_cap, lim, r); });
     fill_stats(c, r, out->stats);
     out->exhausted = r.g.incomplete ? 0 : 1;
     return PCCP_OK;
@@ -563,8 +594,7 @@ int pccp_gpu_solve(pccp_gpu_ctx* c, const int32_t* root, const pccp_limits* lim,
       return PCCP_OK;
     }
     RunOut r;
-    if (c->warp) run_search<dev::WarpGroup>(c, 1, root, -1, lim, r);
-    else run_search<dev::CtaGroup>(c, 1, root, -1, lim, r);
+    dispatch(c, [&]<class Gp, bool TS>() { run_search<Gp, TS>(c, 1, root, -1, lim, r); });
     fill_stats(c, r, out->stats);
     const bool exhausted = r.g.incomplete == 0;
     const bool has = r.g.incumbent != INT32_MAX;

@@ -164,6 +164,85 @@ struct CtaGroup {
   }
 };
 
+// ---- table access ------------------------------------------------------------------
+// TS = true: the tables were copied into shared memory at kernel start.
+template <bool TS>
+struct Tab;
+template <>
+struct Tab<true> {
+  const int* p;   // generic view (legacy paths)
+  unsigned base;  // shared address of table word 0
+  __device__ __forceinline__ int4 ld4(unsigned off, int i) const {
+    int4 r;
+    asm("ld.shared.v4.b32 {%0, %1, %2, %3}, [%4];"
+        : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w)
+        : "r"(base + 4u * off + 16u * (unsigned)i));
+    return r;
+  }
+  __device__ __forceinline__ int2 ld2(unsigned off, int i) const {
+    int2 r;
+    asm("ld.shared.v2.b32 {%0, %1}, [%2];" : "=r"(r.x), "=r"(r.y) : "r"(base + 4u * off + 8u * (unsigned)i));
+    return r;
+  }
+};
+template <>
+struct Tab<false> {
+  const int* p;
+  unsigned base;
+  __device__ __forceinline__ int4 ld4(unsigned off, int i) const {
+    return __ldg(reinterpret_cast<const int4*>(p + off) + i);
+  }
+  __device__ __forceinline__ int2 ld2(unsigned off, int i) const {
+    return __ldg(reinterpret_cast<const int2*>(p + off) + i);
+  }
+};
+
+// ---- store access by 32-bit shared address -------------------------------------------
+__device__ __forceinline__ int sld(unsigned a) {
+  int v;
+  asm volatile("ld.volatile.shared.b32 %0, [%1];" : "=r"(v) : "r"(a) : "memory");
+  return v;
+}
+__device__ __forceinline__ int satom_max(unsigned a, int v) {
+  int old;
+  asm volatile("atom.shared.max.s32 %0, [%1], %2;" : "=r"(old) : "r"(a), "r"(v) : "memory");
+  return old;
+}
+__device__ __forceinline__ int satom_min(unsigned a, int v) {
+  int old;
+  asm volatile("atom.shared.min.s32 %0, [%1], %2;" : "=r"(old) : "r"(a), "r"(v) : "memory");
+  return old;
+}
+__device__ __forceinline__ bool small30(int v) { return (unsigned)(v + 0x40000000) < 0x80000000u; }
+__device__ __forceinline__ long long widen(int v) {
+  return v == INT_MAX ? kWide : (v == INT_MIN ? -kWide : (long long)v);
+}
+
+// Unit guard `S[a] - S[b] <= T` (a, b packed in x).  Both reads in
+// (-2^30, 2^30): exact in 32 bits; otherwise the reference's widened int64
+// arithmetic (tv(+1, a) + tv(-1, b), command.cpp:11-27).
+__device__ __forceinline__ bool unit_guard(unsigned sb, int x, int T) {
+  const int va = sld(sb + (((unsigned)x & 0xffffu) << 2));
+  const int vb = sld(sb + (((unsigned)x >> 16) << 2));
+  if (small30(va) & small30(vb)) return va - vb <= T;
+  return widen(va) - widen(vb) <= (long long)T;
+}
+
+// Unit tell: target word tw <- k +- S[f], joined up (lb) or down (ub).
+// |k| < 2^30 is guaranteed by the lowering, so a small read needs no narrow.
+__device__ __forceinline__ bool unit_tell(unsigned sb, int k, int w) {
+  const unsigned tw = (unsigned)w & 0x7fffu, f = ((unsigned)w >> 15) & 0x7fffu;
+  const int vf = sld(sb + (f << 2));
+  const bool neg = (w & 0x40000000) != 0;
+  int val;
+  if (small30(vf)) val = neg ? k - vf : k + vf;
+  else val = narrow((long long)k + (neg ? -widen(vf) : widen(vf)));
+  const unsigned a = sb + (tw << 2);
+  const int cur = sld(a);
+  if (w < 0) return val > cur && satom_max(a, val) < val;
+  return val < cur && satom_min(a, val) > val;
+}
+
 // ---- propagators -----------------------------------------------------------------
 
 // LinExpr::eval over a flat [k, n, (coef, word)*n] expression (command.cpp:21-27).
@@ -296,14 +375,26 @@ __device__ __forceinline__ void apply_fold(const G& g, volatile int* S, const in
 // interval or a scalar at top, store.cpp:65-75).  Failure is monotone, so a
 // scan of any intermediate state is valid; it runs every round (H8).
 // Returns true iff the store failed.
-template <class G>
-__device__ bool propagate(const G& g, volatile int* S, const int* __restrict__ T, const DeviceLayout& L,
+template <class G, bool TS>
+__device__ bool propagate(const G& g, volatile int* S, unsigned sb, const Tab<TS>& tab, const DeviceLayout& L,
                           int& rounds) {
+  const int* __restrict__ T = tab.p;
   g.round_begin();
   int r = 0;
   bool failed = false;
   for (;;) {
     bool ch = false, fl = false;
+    for (int i = g.rank(); i < (int)L.n_unit1; i += g.size()) {
+      const int4 q = tab.ld4(L.unit1, i);
+      if (unit_guard(sb, q.x, q.y)) ch |= unit_tell(sb, q.z, q.w);
+    }
+    for (int i = g.rank(); i < (int)L.n_unit2; i += g.size()) {
+      const int4 q = tab.ld4(L.unit2, i);
+      if (unit_guard(sb, q.x, q.y)) {
+        const int2 q2 = tab.ld2(L.unit2g, i);
+        if (unit_guard(sb, q2.x, q2.y)) ch |= unit_tell(sb, q.z, q.w);
+      }
+    }
     for (int i = g.rank(); i < (int)L.n_small; i += g.size()) ch |= eval_small(S, T, L, i);
     if (L.n_rows) ch |= eval_rows(g, S, T, L);
     for (int i = g.rank(); i < (int)L.n_gen; i += g.size())

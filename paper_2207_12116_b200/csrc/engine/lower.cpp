@@ -2,6 +2,7 @@
 #include "lower.hpp"
 
 #include <algorithm>
+#include <cstdlib>
 #include <optional>
 #include <stdexcept>
 #include <tuple>
@@ -202,9 +203,11 @@ Lowered lower_model(const pccp_model& m) {
   std::vector<Row> rows;
   std::vector<std::uint32_t> generic;
 
+  const bool no_rows = std::getenv("PCCP_NO_ROWS") != nullptr;  // diagnostics: interpret sums
   // compile_sum pattern (propagation.cpp:314-335) starting at command i.
   auto match_row = [&](std::size_t i) -> std::size_t {
     const CmdP& s = cmds[i];
+    if (no_rows) return 0;
     if (!s.guards.empty() || s.kind != PCCP_ZINC || !s.sc || s.lb || s.ub || s.sc->k != 0) return 0;
     const auto& terms = s.sc->terms;
     const std::size_t n = terms.size();
@@ -242,6 +245,58 @@ Lowered lower_model(const pccp_model& m) {
     return 2 + n;
   };
 
+  // Unit records (kernels.cuh eval_unit): every guard in the canonical form
+  // S[a] - S[b] <= T (an absent term reads the constant-zero word Z =
+  // n_words), one bound tell `k +- S[f]` per record; a command telling both
+  // bounds becomes two records (same guards, same fixed points).
+  const std::uint32_t Z = m.n_words;
+  const bool unit_ok = Z < 0x7fffu && !std::getenv("PCCP_NO_UNIT");
+  L.zero_word = Z;
+  struct U1 {
+    std::int32_t x, y, z, w;
+  };
+  std::vector<U1> unit1;
+  std::vector<std::pair<U1, std::pair<std::int32_t, std::int32_t>>> unit2;
+  auto unit_guard = [&](const NormGuard& n, std::int32_t& x) {
+    std::uint32_t a = Z, b = Z;
+    for (auto [coef, w] : n.terms) {
+      if (w >= 0xffffu) return false;
+      if (coef == 1 && a == Z) a = w;
+      else if (coef == -1 && b == Z) b = w;
+      else return false;
+    }
+    x = static_cast<std::int32_t>(a | (b << 16));
+    return true;
+  };
+  auto try_unit = [&](const CmdP& c, const std::vector<NormGuard>& gs) {
+    std::int32_t gx[2] = {static_cast<std::int32_t>(Z | (Z << 16)), 0}, gT[2] = {0, 0};
+    for (std::size_t k = 0; k < gs.size(); ++k) {
+      if (!unit_guard(gs[k], gx[k])) return false;
+      gT[k] = gs[k].T;
+    }
+    std::vector<U1> recs;
+    for (int part = 0; part < 2; ++part) {
+      const std::optional<Expr>& e = part == 0 ? c.lb : c.ub;
+      if (!e) continue;
+      const std::uint32_t tw = c.tw + static_cast<std::uint32_t>(part);
+      if (tw >= 0x7fffu || e->terms.size() > 1 || e->k <= -(1 << 30) || e->k >= (1 << 30)) return false;
+      std::uint32_t f = Z, neg = 0;
+      if (e->terms.size() == 1) {
+        const auto [coef, w] = e->terms[0];
+        if ((coef != 1 && coef != -1) || w >= 0x7fffu) return false;
+        f = w;
+        neg = coef < 0 ? 1u : 0u;
+      }
+      recs.push_back(U1{gx[0], gT[0], e->k,
+                        static_cast<std::int32_t>(tw | (f << 15) | (neg << 30) | (part == 0 ? 1u << 31 : 0u))});
+    }
+    for (const U1& r : recs) {
+      if (gs.size() <= 1) unit1.push_back(r);
+      else unit2.push_back({r, {gx[1], gT[1]}});
+    }
+    return true;
+  };
+
   for (std::size_t i = 0; i < cmds.size();) {
     if (const std::size_t used = match_row(i)) {
       i += used;
@@ -269,6 +324,7 @@ Lowered lower_model(const pccp_model& m) {
     bool never = false;
     int ng = 0;
     std::uint32_t shape = 0;
+    std::vector<NormGuard> kept;
     if (ok) {
       for (const GuardP& g : c.guards) {
         auto n = normalise(g);
@@ -281,11 +337,16 @@ Lowered lower_model(const pccp_model& m) {
         }
         s.T[ng] = n->T;
         shape |= static_cast<std::uint32_t>(n->terms.size()) << (4 * ng);
+        kept.push_back(*n);
         ++ng;
       }
     }
     if (never) {  // can never fire: dropped (still counted as a reference command)
       ++out.n_dropped;
+      ++i;
+      continue;
+    }
+    if (ok && unit_ok && try_unit(c, kept)) {
       ++i;
       continue;
     }
@@ -326,6 +387,27 @@ Lowered lower_model(const pccp_model& m) {
     B.resize(off + n, 0);
     return off;
   };
+  L.n_unit1 = static_cast<std::uint32_t>(unit1.size());
+  L.unit1 = reserve_arr(4 * L.n_unit1);
+  for (std::uint32_t i = 0; i < L.n_unit1; ++i) {
+    const U1& r = unit1[i];
+    B[L.unit1 + 4 * i + 0] = r.x;
+    B[L.unit1 + 4 * i + 1] = r.y;
+    B[L.unit1 + 4 * i + 2] = r.z;
+    B[L.unit1 + 4 * i + 3] = r.w;
+  }
+  L.n_unit2 = static_cast<std::uint32_t>(unit2.size());
+  L.unit2 = reserve_arr(4 * L.n_unit2);
+  L.unit2g = reserve_arr(2 * L.n_unit2);
+  for (std::uint32_t i = 0; i < L.n_unit2; ++i) {
+    const U1& r = unit2[i].first;
+    B[L.unit2 + 4 * i + 0] = r.x;
+    B[L.unit2 + 4 * i + 1] = r.y;
+    B[L.unit2 + 4 * i + 2] = r.z;
+    B[L.unit2 + 4 * i + 3] = r.w;
+    B[L.unit2g + 2 * i + 0] = unit2[i].second.first;
+    B[L.unit2g + 2 * i + 1] = unit2[i].second.second;
+  }
   const std::uint32_t ns = static_cast<std::uint32_t>(smalls.size());
   L.n_small = ns;
   for (int k = 0; k < 4; ++k) L.small_g[k] = reserve_arr(ns);

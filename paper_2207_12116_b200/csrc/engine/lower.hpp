@@ -33,6 +33,9 @@ constexpr std::uint32_t kTermWordMask = (1u << kTermWordBits) - 1;
 
 struct DeviceLayout {
   // offsets (int32 units) into the blob
+  std::uint32_t unit1, n_unit1;          // int4 records: guard (a | b<<16, T), tell (k, tw | f<<15 | neg<<30 | up<<31)
+  std::uint32_t unit2, unit2g, n_unit2;  // same + int2 second guard
+  std::uint32_t zero_word;               // constant-zero word Z = n_words (store_stride > n_words)
   std::uint32_t small_g[4], small_T[2], small_lbk, small_lbt, small_ubk, small_ubt, small_tw;
   std::uint32_t n_small;
   std::uint32_t fold_w, fold_v;  // fold_w: word | (up << 31)

@@ -169,6 +169,23 @@ __device__ __forceinline__ Frame frame(const Model& M) {
   return f;
 }
 
+template <bool TS>
+__device__ __forceinline__ Tab<TS> make_tab(const Frame& f) {
+  Tab<TS> t;
+  t.p = f.T;
+  t.base = 0;
+  if constexpr (TS) t.base = (unsigned)__cvta_generic_to_shared((const void*)f.T);
+  return t;
+}
+
+// The constant-zero word Z read by absent unit-record terms; never written.
+template <class G>
+__device__ __forceinline__ unsigned init_store(const G& g, volatile int* S, const DeviceLayout& L) {
+  if (g.rank() == 0) S[L.zero_word] = 0;
+  g.sync();
+  return (unsigned)__cvta_generic_to_shared((const void*)S);
+}
+
 template <class G>
 struct GroupOf;
 template <>
@@ -187,12 +204,14 @@ struct GroupOf<CtaGroup> {
 };
 
 // ---- K1: batched fixed points (run_sequential on N independent stores) ---------
-template <class G>
+template <class G, bool TS>
 __global__ void k_propagate(Model M, int* stores, int n, int stride, unsigned char* status, unsigned* rounds,
                             int fold) {
   const Frame f = frame(M);
   const G g = GroupOf<G>::make(f);
+  const Tab<TS> tab = make_tab<TS>(f);
   volatile int* S = f.stores + GroupOf<G>::in_cta() * M.store_stride;
+  const unsigned sb = init_store(g, S, M.L);
   const int gid = blockIdx.x * GroupOf<G>::per_cta() + GroupOf<G>::in_cta();
   const int ng = gridDim.x * GroupOf<G>::per_cta();
   for (int i = gid; i < n; i += ng) {
@@ -204,7 +223,7 @@ __global__ void k_propagate(Model M, int* stores, int n, int stride, unsigned ch
       g.sync();
     }
     int r = 0;
-    const bool failed = propagate(g, S, f.T, M.L, r);
+    const bool failed = propagate(g, S, sb, tab, M.L, r);
     copy_out(g, io, S, (int)M.L.n_words);
     if (g.rank() == 0) {
       status[i] = failed ? 1 : 0;
@@ -215,12 +234,14 @@ __global__ void k_propagate(Model M, int* stores, int n, int stride, unsigned ch
 }
 
 // ---- the problem root: fold, objective, fixed point, classification ----------------
-template <class G>
+template <class G, bool TS>
 __global__ void k_root(Model M, SearchCtl C, int* store, unsigned char* flag) {
   const Frame f = frame(M);
   const G g = GroupOf<G>::make(f);
+  const Tab<TS> tab = make_tab<TS>(f);
   if (GroupOf<G>::in_cta() != 0 || blockIdx.x != 0) return;
   volatile int* S = f.stores;
+  const unsigned sb = init_store(g, S, M.L);
   Cnt cnt;
   copy_words(g, S, store, (int)M.L.n_words);
   g.sync();
@@ -229,7 +250,7 @@ __global__ void k_root(Model M, SearchCtl C, int* store, unsigned char* flag) {
   join_objective(g, S, M.L, C);
   g.sync();
   int r = 0;
-  const bool failed = propagate(g, S, f.T, M.L, r);
+  const bool failed = propagate(g, S, sb, tab, M.L, r);
   if (C.count) {
     ++cnt.nodes;
     cnt.rounds += (unsigned long long)r;
@@ -246,12 +267,14 @@ __global__ void k_root(Model M, SearchCtl C, int* store, unsigned char* flag) {
 // ---- K5: one level of the EPS decomposition (decompose, solver.cpp:180-213) ------
 // Parent p's children go to slots 2p (left, x <= mid) and 2p+1 (right); the
 // compaction below keeps BFS order, so the frontier is identical on every GPU.
-template <class G>
+template <class G, bool TS>
 __global__ void k_expand(Model M, SearchCtl C, const int* parents, const int* parent_idx, int n_par, int stride,
                          int child_depth, int* children, unsigned char* flags) {
   const Frame f = frame(M);
   const G g = GroupOf<G>::make(f);
+  const Tab<TS> tab = make_tab<TS>(f);
   volatile int* S = f.stores + GroupOf<G>::in_cta() * M.store_stride;
+  const unsigned sb = init_store(g, S, M.L);
   const int gid = blockIdx.x * GroupOf<G>::per_cta() + GroupOf<G>::in_cta();
   const int ng = gridDim.x * GroupOf<G>::per_cta();
   const DeviceLayout& L = M.L;
@@ -262,6 +285,7 @@ __global__ void k_expand(Model M, SearchCtl C, const int* parents, const int* pa
     g.sync();
     int lbw = 0, mid = 0;
     const int b = branch(g, S, f.T, L, lbw, mid);
+    g.sync();  // every thread has read S before rank 0 joins the decision
     for (int side = 0; side < 2; ++side) {
       unsigned char keep = 0;
       if (b == 1) {
@@ -277,7 +301,7 @@ __global__ void k_expand(Model M, SearchCtl C, const int* parents, const int* pa
         join_objective(g, S, L, C);
         g.sync();
         int r = 0;
-        const bool failed = propagate(g, S, f.T, L, r);
+        const bool failed = propagate(g, S, sb, tab, L, r);
         if (C.count) {
           ++cnt.nodes;
           cnt.rounds += (unsigned long long)r;
@@ -351,11 +375,13 @@ struct SearchParams {
 // k*shard_count) and explores it depth-first, left branch first (dfs,
 // solver.cpp:122-146).  A branching node pushes (its fixed point, right
 // decision) and descends left in place; a leaf pops.
-template <class G>
+template <class G, bool TS>
 __global__ void k_search(Model M, SearchCtl C, SearchParams P) {
   const Frame f = frame(M);
   const G g = GroupOf<G>::make(f);
+  const Tab<TS> tab = make_tab<TS>(f);
   volatile int* S = f.stores + GroupOf<G>::in_cta() * M.store_stride;
+  const unsigned sb = init_store(g, S, M.L);
   const int gid = blockIdx.x * GroupOf<G>::per_cta() + GroupOf<G>::in_cta();
   const DeviceLayout& L = M.L;
   const int nw = (int)L.n_words;
@@ -395,7 +421,7 @@ __global__ void k_search(Model M, SearchCtl C, SearchParams P) {
           break;
         }
         int r = 0;
-        const bool failed = propagate(g, S, f.T, L, r);
+        const bool failed = propagate(g, S, sb, tab, L, r);
         ++cnt.nodes;
         cnt.rounds += (unsigned long long)r;
         if ((unsigned long long)depth > cnt.maxd) cnt.maxd = (unsigned long long)depth;
@@ -418,6 +444,7 @@ __global__ void k_search(Model M, SearchCtl C, SearchParams P) {
         }
         int* ent = stk + (size_t)sp * P.entry_stride;
         copy_out(g, ent, S, nw);
+        g.sync();  // the parent fixed point is saved before the left decision lands
         if (g.rank() == 0) {
           ent[nw] = lbw;
           ent[nw + 1] = mid;
@@ -435,6 +462,7 @@ __global__ void k_search(Model M, SearchCtl C, SearchParams P) {
       if (sp == 0) break;
       --sp;
       const int* ent = stk + (size_t)sp * P.entry_stride;
+      g.sync();  // no thread still reads the leaf (hash, branch) when it is overwritten
       copy_words(g, S, ent, nw);
       g.sync();
       if (g.rank() == 0) {

@@ -1,0 +1,68 @@
+"""Ad-hoc exploration on the GPU box: per-config timings and launch plans.
+
+    python scripts/explore.py q14 csp rcpsp30 rcpsp120 [--gt 32 --gpc 8 ...]
+"""
+import argparse
+import json
+import os
+import sys
+import time
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+
+from paper_2207_12116_b200 import Engine, Model  # noqa: E402
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("what", nargs="+")
+    ap.add_argument("--gt", type=int, default=0)
+    ap.add_argument("--gpc", type=int, default=0)
+    ap.add_argument("--cps", type=int, default=0)
+    ap.add_argument("--eps", type=int, default=0)
+    ap.add_argument("--hash", action="store_true")
+    ap.add_argument("--timeout", type=float, default=60)
+    ap.add_argument("--reps", type=int, default=2)
+    a = ap.parse_args()
+    eng = Engine(0, group_threads=a.gt, groups_per_cta=a.gpc, ctas_per_sm=a.cps, eps_factor=a.eps, hash=a.hash)
+    for w in a.what:
+        if w.startswith("q"):
+            m = Model.nqueens(int(w[1:]))
+            eng.load(m)
+            info = eng.lowering_info()
+            for _ in range(a.reps):
+                t = time.time()
+                r = eng.enumerate()
+                dt = time.time() - t
+            print(w, json.dumps(info))
+            print(w, json.dumps(r), f"wall {dt:.4f}s nodes/s {r['nodes'] / dt:.3e} evals/s {r['evals'] / dt:.3e}")
+        elif w.startswith("csp"):
+            d = int(w[3:]) if len(w) > 3 else 22
+            m = Model.random_csp(1)
+            eng.load(m)
+            info = eng.lowering_info()
+            for _ in range(a.reps):
+                t = time.time()
+                r = eng.enumerate(depth_cap=d)
+                dt = time.time() - t
+            print(w, json.dumps(info))
+            print(w, json.dumps(r), f"wall {dt:.4f}s nodes/s {r['nodes'] / dt:.3e}")
+        elif w.startswith("rcpsp30") or w.startswith("rcpsp120"):
+            n = 30 if w.startswith("rcpsp30") else 120
+            seeds = [int(s) for s in w.split("_")[1:]] or [1]
+            for s in seeds:
+                m = Model.rcpsp_random(s, n, 4)
+                eng.load(m)
+                info = eng.lowering_info()
+                t = time.time()
+                r = eng.solve(timeout_s=a.timeout)
+                dt = time.time() - t
+                ok = m.check_solution(r.best_words) if r.best_words is not None else None
+                print(w, s, json.dumps(info))
+                print(w, s, r.status, r.objective, ok, json.dumps(r.stats), r.improvements[:8], f"wall {dt:.3f}s",
+                      f"nodes/s {r.stats['nodes'] / dt:.3e}")
+        sys.stdout.flush()
+
+
+if __name__ == "__main__":
+    main()

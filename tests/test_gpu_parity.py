@@ -131,6 +131,32 @@ def test_enumerate_csp_depth12(golden, hengine):
         assert res[k] == g[k], k
 
 
+@pytest.mark.parametrize("group_threads", [0, 32, 128, 512])
+def test_enumerate_csp_depth22_repeatable(group_threads, golden):
+    """Config 3 at the benchmark depth, under warp- and CTA-sized groups, three
+    times each: chaotic parallel rounds must still give identical counts."""
+    from paper_2207_12116_b200 import Engine
+    g = golden["csp1"]["enumerate_d22"]
+    with Engine(0, hash=True, group_threads=group_threads) as e:
+        e.load(build("csp1"))
+        for _ in range(3):
+            res = e.enumerate(depth_cap=22)
+            for k in ("nodes", "failures", "solutions", "open_leaves", "hash_sum"):
+                assert res[k] == g[k], (group_threads, k, res[k], g[k])
+
+
+@pytest.mark.parametrize("group_threads", [64, 256])
+def test_enumerate_nqueens_cta_groups(group_threads, golden):
+    from paper_2207_12116_b200 import Engine
+    g = golden["nqueens10"]["enumerate"]
+    with Engine(0, hash=True, group_threads=group_threads) as e:
+        e.load(build("nqueens10"))
+        for _ in range(3):
+            res = e.enumerate()
+            for k in ("nodes", "failures", "solutions", "hash_sum"):
+                assert res[k] == g[k], (group_threads, k)
+
+
 @pytest.mark.parametrize("seed", [2, 3])
 def test_enumerate_small_csp(seed, golden, hengine):
     g = golden[f"csp_small{seed}"]["enumerate_d10"]
