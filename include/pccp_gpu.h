@@ -132,6 +132,10 @@ typedef struct pccp_stats {
   double kernel_ms;     /* device time of the search kernels (CUDA events) */
   double decompose_ms;  /* device+host time of the EPS phase */
   uint64_t launches;    /* kernels launched by this call */
+  uint64_t search_evals;/* evals inside the persistent search kernel only */
+  uint64_t h2d_bytes;   /* host->device bytes moved by this call */
+  uint64_t d2h_bytes;   /* device->host bytes moved by this call */
+  double device_ms;     /* device time of the whole call (CUDA events on the engine stream) */
 } pccp_stats;
 
 typedef struct pccp_enum_result {

@@ -70,6 +70,10 @@ class PccpStats(C.Structure):
         ("kernel_ms", C.c_double),
         ("decompose_ms", C.c_double),
         ("launches", C.c_uint64),
+        ("search_evals", C.c_uint64),
+        ("h2d_bytes", C.c_uint64),
+        ("d2h_bytes", C.c_uint64),
+        ("device_ms", C.c_double),
     ]
 
 

@@ -232,13 +232,15 @@ struct RunOut {
   dev::Globals g;
   double decompose_ms = 0, kernel_ms = 0, elapsed_ms = 0;
   std::uint64_t subproblems = 0;
-  bool root_failed = false;
+  std::uint64_t bfs_rounds = 0, launches = 0, h2d = 0, d2h = 0;
+  double device_ms = 0;
 };
 
 template <class Gp, bool TS>
 void run_search(pccp_gpu_ctx* c, int mode, const int32_t* root_words, int depth_cap, const pccp_limits* lim,
                 RunOut& out) {
   const double t_start = now_ms();
+  const std::uint64_t launches0 = c->launches;
   const DeviceLayout& L = c->low.L;
   const int nw = (int)L.n_words;
   const int stride = c->store_stride;
@@ -265,6 +267,7 @@ void run_search(pccp_gpu_ctx* c, int mode, const int32_t* root_words, int depth_
   CK(cudaMemcpyAsync(c->fa.p, root.data(), (size_t)nw * 4, cudaMemcpyHostToDevice, c->stream));
   const int zero = 0;
   CK(cudaMemcpyAsync(c->ia.p, &zero, 4, cudaMemcpyHostToDevice, c->stream));
+  out.h2d += sizeof(dev::Globals) + (std::uint64_t)nw * 4 + 4;
   CK(cudaEventRecord(c->ev[0], c->stream));
   dev::k_root<Gp, TS><<<1, c->block, c->smem, c->stream>>>(M, C, c->fa.p, c->flags.p);
   CK(cudaGetLastError());
@@ -273,6 +276,7 @@ void run_search(pccp_gpu_ctx* c, int mode, const int32_t* root_words, int depth_
   CK(cudaMemcpyAsync(&rflag, c->flags.p, 1, cudaMemcpyDeviceToHost, c->stream));
   CK(cudaMemcpyAsync(root.data(), c->fa.p, (size_t)nw * 4, cudaMemcpyDeviceToHost, c->stream));
   CK(cudaStreamSynchronize(c->stream));
+  out.d2h += 1 + (std::uint64_t)nw * 4;
 
   // EPS decomposition: whole BFS levels until the frontier holds target nodes.
   const int eps = c->cfg.eps_factor > 0 ? c->cfg.eps_factor : 8;
@@ -300,12 +304,16 @@ void run_search(pccp_gpu_ctx* c, int mode, const int32_t* root_words, int depth_
     c->launches += 2;
     CK(cudaMemcpyAsync(&count, dcount.p, 4, cudaMemcpyDeviceToHost, c->stream));
     CK(cudaStreamSynchronize(c->stream));
+    out.d2h += 8;
     std::swap(c->fa, c->fb);
     std::swap(c->ia, c->ib);
     ++level;
   }
   dcount.release();
   CK(cudaEventRecord(c->ev[1], c->stream));
+  CK(cudaMemcpyAsync(&out.bfs_rounds, &c->G->rounds, 8, cudaMemcpyDeviceToHost, c->stream));
+  CK(cudaStreamSynchronize(c->stream));
+  out.d2h += 8;
   out.subproblems = (std::uint64_t)count;
 
   bool searched = false;
@@ -334,7 +342,11 @@ void run_search(pccp_gpu_ctx* c, int mode, const int32_t* root_words, int depth_
   CK(cudaEventRecord(c->ev[2], c->stream));
   CK(cudaMemcpyAsync(&out.g, c->G, sizeof(dev::Globals), cudaMemcpyDeviceToHost, c->stream));
   CK(cudaStreamSynchronize(c->stream));
+  out.d2h += sizeof(dev::Globals);
+  out.launches = c->launches - launches0;
   float ms = 0;
+  CK(cudaEventElapsedTime(&ms, c->ev[0], c->ev[2]));
+  out.device_ms = ms;
   CK(cudaEventElapsedTime(&ms, c->ev[0], c->ev[1]));
   out.decompose_ms = ms;
   if (searched) {
@@ -362,7 +374,11 @@ void fill_stats(const pccp_gpu_ctx* c, const RunOut& r, pccp_stats& s) {
   s.elapsed_ms = r.elapsed_ms;
   s.kernel_ms = r.kernel_ms;
   s.decompose_ms = r.decompose_ms;
-  s.launches = c->launches;
+  s.launches = r.launches;
+  s.search_evals = (r.g.rounds - r.bfs_rounds) * (std::uint64_t)c->low.L.n_ref_cmds;
+  s.h2d_bytes = r.h2d;
+  s.d2h_bytes = r.d2h;
+  s.device_ms = r.device_ms;
 }
 
 void check_loaded(const pccp_gpu_ctx* c) {
