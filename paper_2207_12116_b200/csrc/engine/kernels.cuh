@@ -17,6 +17,7 @@
 
 #include <climits>
 #include <cstdint>
+#include <type_traits>
 
 #include "lower.hpp"
 
@@ -375,9 +376,79 @@ __device__ __forceinline__ void apply_fold(const G& g, volatile int* S, const in
 // interval or a scalar at top, store.cpp:65-75).  Failure is monotone, so a
 // scan of any intermediate state is valid; it runs every round (H8).
 // Returns true iff the store failed.
+constexpr unsigned long long kAllDirty = ~0ull;
+
+// Filtered rounds for stores of <= 64 words (one bit per word, one register):
+// round r evaluates only the records that read a word changed in round r-1
+// (or at node entry, `dirty`).  A record whose inputs are unchanged since its
+// last evaluation would join the same value again — a no-op — so skipping it
+// leaves the fixed point, the failure status and the node set unchanged; the
+// loop ends when a round changes nothing, exactly as the eventless loop.
+// Failure is checked on the intervals touched since the previous check.
+template <bool TS>
+__device__ bool propagate_filtered(const WarpGroup& g, volatile int* S, unsigned sb, const Tab<TS>& tab,
+                                   const DeviceLayout& L, unsigned long long dirty, int& rounds) {
+  const int* __restrict__ T = tab.p;
+  const int nw = (int)L.n_words;
+  if (nw < 64) dirty &= (1ull << nw) - 1ull;
+  int r = 0;
+  bool failed = false;
+  unsigned long long D = dirty;
+  for (;;) {
+    unsigned long long mine = 0;
+    unsigned long long todo = D;
+    while (todo) {
+      const int w = __ffsll((long long)todo) - 1;
+      todo &= todo - 1ull;
+      const int beg = T[L.wl_off + w], end = T[L.wl_off + w + 1];
+      for (int j = beg + g.lane; j < end; j += 32) {
+        const int e = T[L.wl + j];
+        int4 q;
+        bool ok;
+        if (e >= 0) {
+          q = tab.ld4(L.unit1, e);
+          ok = unit_guard(sb, q.x, q.y);
+        } else {
+          const int i = e & 0x7fffffff;
+          q = tab.ld4(L.unit2, i);
+          ok = unit_guard(sb, q.x, q.y);
+          if (ok) {
+            const int2 q2 = tab.ld2(L.unit2g, i);
+            ok = unit_guard(sb, q2.x, q2.y);
+          }
+        }
+        if (ok && unit_tell(sb, q.z, q.w)) mine |= 1ull << ((unsigned)q.w & 0x7fffu);
+      }
+    }
+    __syncwarp();
+    const unsigned lo = __reduce_or_sync(kFull, (unsigned)mine);
+    const unsigned hi = __reduce_or_sync(kFull, (unsigned)(mine >> 32));
+    const unsigned long long changed = ((unsigned long long)hi << 32) | lo;
+    const unsigned long long touched = changed | D;
+    bool fl = false;
+    for (int i = g.lane; i < (int)L.n_iv; i += 32) {
+      const int w = T[L.iv_lb + i];
+      if ((touched >> w) & 3ull) fl |= S[w] > S[w + 1];
+    }
+    for (int i = g.lane; i < (int)L.n_sc; i += 32) fl |= S[T[L.sc_w + i]] == T[L.sc_top + i];
+    ++r;
+    if (__any_sync(kFull, fl)) {
+      failed = true;
+      break;
+    }
+    if (!changed) break;
+    D = changed;
+  }
+  rounds = r;
+  return failed;
+}
+
 template <class G, bool TS>
 __device__ bool propagate(const G& g, volatile int* S, unsigned sb, const Tab<TS>& tab, const DeviceLayout& L,
-                          int& rounds) {
+                          int& rounds, unsigned long long dirty = kAllDirty) {
+  if constexpr (std::is_same<G, WarpGroup>::value) {
+    if (L.filtered) return propagate_filtered(g, S, sb, tab, L, dirty, rounds);
+  }
   const int* __restrict__ T = tab.p;
   g.round_begin();
   int r = 0;

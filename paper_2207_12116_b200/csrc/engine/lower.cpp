@@ -408,6 +408,46 @@ Lowered lower_model(const pccp_model& m) {
     B[L.unit2g + 2 * i + 0] = unit2[i].second.first;
     B[L.unit2g + 2 * i + 1] = unit2[i].second.second;
   }
+  // Per-word reader lists for the filtered rounds.
+  L.filtered = (m.n_words <= 64 && smalls.empty() && rows.empty() && generic.empty() &&
+                !std::getenv("PCCP_EVENTLESS"))
+                   ? 1u
+                   : 0u;
+  {
+    std::vector<std::vector<std::int32_t>> readers(m.n_words);
+    auto note = [&](std::int32_t entry, std::uint32_t x, std::uint32_t w) {
+      std::uint32_t ws[3] = {x & 0xffffu, x >> 16, (w >> 15) & 0x7fffu};
+      for (int k = 0; k < 3; ++k) {
+        if (ws[k] >= m.n_words) continue;  // the zero word never changes
+        bool dup = false;
+        for (int j = 0; j < k; ++j) dup |= ws[j] == ws[k];
+        if (!dup) readers[ws[k]].push_back(entry);
+      }
+    };
+    if (L.filtered) {
+      for (std::uint32_t i = 0; i < unit1.size(); ++i)
+        note(static_cast<std::int32_t>(i), static_cast<std::uint32_t>(unit1[i].x), static_cast<std::uint32_t>(unit1[i].w));
+      for (std::uint32_t i = 0; i < unit2.size(); ++i) {
+        const std::int32_t e = static_cast<std::int32_t>(i | 0x80000000u);
+        note(e, static_cast<std::uint32_t>(unit2[i].first.x), static_cast<std::uint32_t>(unit2[i].first.w));
+        const std::uint32_t g2 = static_cast<std::uint32_t>(unit2[i].second.first);
+        for (std::uint32_t w2 : {g2 & 0xffffu, g2 >> 16}) {
+          if (w2 >= m.n_words) continue;
+          if (readers[w2].empty() || readers[w2].back() != e) readers[w2].push_back(e);
+        }
+      }
+    }
+    std::uint32_t total = 0;
+    for (const auto& r : readers) total += static_cast<std::uint32_t>(r.size());
+    L.wl_off = reserve_arr(m.n_words + 1);
+    L.wl = reserve_arr(total);
+    std::uint32_t p = 0;
+    for (std::uint32_t w = 0; w < m.n_words; ++w) {
+      B[L.wl_off + w] = static_cast<std::int32_t>(p);
+      for (std::int32_t e : readers[w]) B[L.wl + p++] = e;
+    }
+    B[L.wl_off + m.n_words] = static_cast<std::int32_t>(p);
+  }
   const std::uint32_t ns = static_cast<std::uint32_t>(smalls.size());
   L.n_small = ns;
   for (int k = 0; k < 4; ++k) L.small_g[k] = reserve_arr(ns);

@@ -36,6 +36,11 @@ struct DeviceLayout {
   std::uint32_t unit1, n_unit1;          // int4 records: guard (a | b<<16, T), tell (k, tw | f<<15 | neg<<30 | up<<31)
   std::uint32_t unit2, unit2g, n_unit2;  // same + int2 second guard
   std::uint32_t zero_word;               // constant-zero word Z = n_words (store_stride > n_words)
+  // Filtered rounds (stores of <= 64 words made only of unit records): a
+  // round re-evaluates just the records that read a word changed in the
+  // previous round (CSR lists per word, entry = record | unit2 << 31).
+  std::uint32_t filtered;
+  std::uint32_t wl_off, wl;
   std::uint32_t small_g[4], small_T[2], small_lbk, small_lbt, small_ubk, small_ubt, small_tw;
   std::uint32_t n_small;
   std::uint32_t fold_w, fold_v;  // fold_w: word | (up << 31)

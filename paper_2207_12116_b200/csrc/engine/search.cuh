@@ -40,14 +40,20 @@ __device__ __forceinline__ void flush(Globals* G, Cnt& c) {
   c = Cnt{};
 }
 
+__device__ __forceinline__ unsigned long long word_bit(int w) { return w < 64 ? 1ull << w : 0ull; }
+
 // Objective tightening at materialisation (solver.cpp:96-99): obj <= best-1.
+// Returns the dirty bit of the objective's ub word when it moved (uniform).
 template <class G>
-__device__ __forceinline__ void join_objective(const G& g, volatile int* S, const DeviceLayout& L,
-                                               const SearchCtl& C) {
-  if (C.mode == 1 && L.obj_lbw >= 0 && g.rank() == 0) {
+__device__ __forceinline__ unsigned long long join_objective(const G& g, volatile int* S, const DeviceLayout& L,
+                                                             const SearchCtl& C) {
+  if (C.mode != 1 || L.obj_lbw < 0) return 0ull;
+  int moved = 0;
+  if (g.rank() == 0) {
     const int best = *(volatile int*)&C.G->incumbent;
-    if (best != INT_MAX) join_min(S, L.obj_lbw + 1, best - 1);
+    if (best != INT_MAX) moved = join_min(S, L.obj_lbw + 1, best - 1) ? 1 : 0;
   }
+  return g.bcast0(moved) ? word_bit(L.obj_lbw + 1) : 0ull;
 }
 
 // SharedControl::should_stop (solver.cpp:68-76): stop flag, timeout, node limit.
@@ -298,10 +304,11 @@ __global__ void k_expand(Model M, SearchCtl C, const int* parents, const int* pa
           else join_max(S, lbw, mid + 1);
         }
         g.sync();
-        join_objective(g, S, L, C);
+        unsigned long long dirty = word_bit(side == 0 ? lbw + 1 : lbw);
+        dirty |= join_objective(g, S, L, C);
         g.sync();
         int r = 0;
-        const bool failed = propagate(g, S, sb, tab, L, r);
+        const bool failed = propagate(g, S, sb, tab, L, r, dirty);
         if (C.count) {
           ++cnt.nodes;
           cnt.rounds += (unsigned long long)r;
@@ -409,8 +416,9 @@ __global__ void k_search(Model M, SearchCtl C, SearchParams P) {
     // as dfs() does for its subproblem root.
     bool need_prop = C.mode == 1;
     bool abandoned = false;
+    unsigned long long dirty = 0;  // words changed since the store was last a fixed point
     if (need_prop) {
-      join_objective(g, S, L, C);
+      dirty = join_objective(g, S, L, C);
       g.sync();
     }
     for (;;) {
@@ -421,7 +429,7 @@ __global__ void k_search(Model M, SearchCtl C, SearchParams P) {
           break;
         }
         int r = 0;
-        const bool failed = propagate(g, S, sb, tab, L, r);
+        const bool failed = propagate(g, S, sb, tab, L, r, dirty);
         ++cnt.nodes;
         cnt.rounds += (unsigned long long)r;
         if ((unsigned long long)depth > cnt.maxd) cnt.maxd = (unsigned long long)depth;
@@ -454,7 +462,7 @@ __global__ void k_search(Model M, SearchCtl C, SearchParams P) {
         ++sp;
         ++depth;
         g.sync();
-        join_objective(g, S, L, C);
+        dirty = word_bit(lbw + 1) | join_objective(g, S, L, C);
         g.sync();
         need_prop = true;
         continue;
@@ -469,8 +477,9 @@ __global__ void k_search(Model M, SearchCtl C, SearchParams P) {
         join_max(S, ent[nw], ent[nw + 1] + 1);  // right branch: x >= mid+1
       }
       depth = ent[nw + 2] + 1;
+      dirty = word_bit(ent[nw]);
       g.sync();
-      join_objective(g, S, L, C);
+      dirty |= join_objective(g, S, L, C);
       g.sync();
       need_prop = true;
     }
