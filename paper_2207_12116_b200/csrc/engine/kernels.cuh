@@ -214,7 +214,9 @@ __device__ __forceinline__ int satom_min(unsigned a, int v) {
   asm volatile("atom.shared.min.s32 %0, [%1], %2;" : "=r"(old) : "r"(a), "r"(v) : "memory");
   return old;
 }
-__device__ __forceinline__ bool small30(int v) { return (unsigned)(v + 0x40000000) < 0x80000000u; }
+// -2^30 <= v < 2^30.  Unsigned arithmetic: a signed `v + 2^30` overflows for
+// v near INT_MAX (UB), which lets the compiler drop the upper check.
+__device__ __forceinline__ bool small30(int v) { return (unsigned)v + 0x40000000u < 0x80000000u; }
 __device__ __forceinline__ long long widen(int v) {
   return v == INT_MAX ? kWide : (v == INT_MIN ? -kWide : (long long)v);
 }

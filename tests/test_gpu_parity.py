@@ -98,6 +98,47 @@ def test_micro_csp_batch_random_stores(engine):
                 assert np.array_equal(w, wo)
 
 
+def _strip_init(m, n_init):
+    from paper_2207_12116_b200.model import Tables
+    t = m.tables()
+    off = (t.cmd_off[n_init:] - t.cmd_off[n_init]).astype(np.uint32)
+    return Tables(t.slot_kind, t.slot_word, t.n_words, off, t.cmd_code[t.cmd_off[n_init]:], t.cands, t.obj_slot)
+
+
+@pytest.mark.parametrize("shift", [0, 2**30 - 4, -(2**30) + 2, 2**31 - 12, -(2**31) + 12])
+@pytest.mark.parametrize("n", [8, 14])
+def test_sentinel_and_wide_arithmetic(n, shift, engine):
+    """H1: +-inf sentinels and values beyond +-2^30 (the 32-bit fast path's
+    range) must follow the reference's widened int64 arithmetic exactly.
+    N-Queens commands without their init tells, random stores with infinite
+    and shifted bounds, GPU == C oracle."""
+    t = _strip_init(build(f"nqueens{n}"), n)
+    o = Oracle(t)
+    engine.load(t)
+    rng = np.random.default_rng(n * 1000 + (shift % 997))
+    MIN, MAX = -(2**31), 2**31 - 1
+    stores = []
+    for _ in range(512):
+        s = o.bottom()
+        for w in t.slot_word:
+            r = rng.random()
+            a, b = sorted(int(v) + shift for v in rng.integers(-3, n + 1, 2))
+            a, b = min(max(a, MIN + 1), MAX - 1), min(max(b, MIN + 1), MAX - 1)
+            if r < 0.5:
+                s[w], s[w + 1] = a, b
+            elif r < 0.7:
+                s[w], s[w + 1] = MIN, b
+            elif r < 0.9:
+                s[w], s[w + 1] = a, MAX
+        stores.append(s)
+    out, failed, _ = engine.propagate_batch(np.stack(stores))
+    for s, w, f in zip(stores, out, failed):
+        fo, wo, _, _ = o.run_sequential(s)
+        assert f == fo
+        if not f:
+            assert np.array_equal(w, wo)
+
+
 def test_replayed_paths(golden, engine):
     """materialize() of sampled decision paths (with objective bounds) == reference."""
     for name in config_names(golden):
