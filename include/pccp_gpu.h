@@ -226,8 +226,9 @@ typedef struct pccp_lowering_info {
 int pccp_gpu_lowering_info(pccp_gpu_ctx* ctx, pccp_lowering_info* out);
 
 /* Host-only: lowers the tables without a device (validation / diagnostics).
- * shape_counts (optional, 3 entries): unit records with <= 1 guard, unit
- * records with 2 guards, commands dropped as never-firing. */
+ * shape_counts (optional, 5 entries): unit records with <= 1 guard, unit
+ * records with 2 guards, commands dropped as never-firing, fused not(and)
+ * groups, filtered-rounds flag. */
 int pccp_lower_only(const pccp_model* model, pccp_lowering_info* out, uint32_t* shape_counts);
 
 #ifdef __cplusplus

@@ -528,6 +528,8 @@ int pccp_lower_only(const pccp_model* m, pccp_lowering_info* o, uint32_t* shape_
       shape_counts[0] = L.n_unit1;
       shape_counts[1] = L.n_unit2;
       shape_counts[2] = low.n_dropped;
+      shape_counts[3] = L.n_ne;
+      shape_counts[4] = L.filtered;
     }
     return PCCP_OK;
   });

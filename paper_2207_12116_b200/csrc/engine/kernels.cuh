@@ -185,6 +185,11 @@ struct Tab<true> {
     asm("ld.shared.v2.b32 {%0, %1}, [%2];" : "=r"(r.x), "=r"(r.y) : "r"(base + 4u * off + 8u * (unsigned)i));
     return r;
   }
+  __device__ __forceinline__ int ld1(unsigned off, int i) const {
+    int r;
+    asm("ld.shared.b32 %0, [%1];" : "=r"(r) : "r"(base + 4u * (off + (unsigned)i)));
+    return r;
+  }
 };
 template <>
 struct Tab<false> {
@@ -196,6 +201,7 @@ struct Tab<false> {
   __device__ __forceinline__ int2 ld2(unsigned off, int i) const {
     return __ldg(reinterpret_cast<const int2*>(p + off) + i);
   }
+  __device__ __forceinline__ int ld1(unsigned off, int i) const { return __ldg(p + off + i); }
 };
 
 // ---- store access by 32-bit shared address -------------------------------------------
@@ -244,6 +250,48 @@ __device__ __forceinline__ bool unit_tell(unsigned sb, int k, int w) {
   const int cur = sld(a);
   if (w < 0) return val > cur && satom_max(a, val) < val;
   return val < cur && satom_min(a, val) > val;
+}
+
+__device__ __forceinline__ bool sjoin_max(unsigned a, int v) {
+  const int cur = sld(a);
+  return v > cur && satom_max(a, v) < v;
+}
+__device__ __forceinline__ bool sjoin_min(unsigned a, int v) {
+  const int cur = sld(a);
+  return v < cur && satom_min(a, v) > v;
+}
+
+// Fused not(and(x + a <= y, y + b <= x)): the four commands of
+// propagation.cpp:350-360 over lb/ub of x and y, from one read of the four
+// words.  Returns the mask of changed words (bit w of the word index, words
+// >= 64 unmasked: callers that track masks only use stores of <= 64 words).
+__device__ __forceinline__ unsigned long long eval_ne(unsigned sb, int4 q) {
+  const unsigned wx = (unsigned)q.x & 0xffffu, wy = (unsigned)q.x >> 16;
+  const unsigned ax = sb + (wx << 2), ay = sb + (wy << 2);
+  const int lx = sld(ax), ux = sld(ax + 4), ly = sld(ay), uy = sld(ay + 4);
+  const int a = q.y, b = q.z;
+  unsigned long long m = 0;
+  auto bit = [](unsigned w) { return 1ull << (w & 63u); };  // any bit flags a change past 64 words
+  if (small30(lx) & small30(ux) & small30(ly) & small30(uy)) {
+    if (ux - ly <= -a) {  // x - a... entailed: propagate not(y + b <= x) = x + 1 - b <= y
+      if (sjoin_min(ax + 4, uy + b - 1)) m |= bit(wx + 1);
+      if (sjoin_max(ay, lx + 1 - b)) m |= bit(wy);
+    }
+    if (uy - lx <= -b) {  // propagate not(x + a <= y) = y + 1 - a <= x
+      if (sjoin_min(ay + 4, ux + a - 1)) m |= bit(wy + 1);
+      if (sjoin_max(ax, ly + 1 - a)) m |= bit(wx);
+    }
+  } else {  // widened int64 arithmetic of command.cpp:11-27
+    if (widen(ux) - widen(ly) <= -(long long)a) {
+      if (sjoin_min(ax + 4, narrow((long long)(b - 1) + widen(uy)))) m |= bit(wx + 1);
+      if (sjoin_max(ay, narrow((long long)(1 - b) + widen(lx)))) m |= bit(wy);
+    }
+    if (widen(uy) - widen(lx) <= -(long long)b) {
+      if (sjoin_min(ay + 4, narrow((long long)(a - 1) + widen(ux)))) m |= bit(wy + 1);
+      if (sjoin_max(ax, narrow((long long)(1 - a) + widen(ly)))) m |= bit(wx);
+    }
+  }
+  return m;
 }
 
 // ---- propagators -----------------------------------------------------------------
@@ -402,9 +450,13 @@ __device__ bool propagate_filtered(const WarpGroup& g, volatile int* S, unsigned
     while (todo) {
       const int w = __ffsll((long long)todo) - 1;
       todo &= todo - 1ull;
-      const int beg = T[L.wl_off + w], end = T[L.wl_off + w + 1];
+      const int beg = tab.ld1(L.wl_off, w), end = tab.ld1(L.wl_off, w + 1);
       for (int j = beg + g.lane; j < end; j += 32) {
-        const int e = T[L.wl + j];
+        const int e = tab.ld1(L.wl, j);
+        if (e & 0x40000000) {
+          mine |= eval_ne(sb, tab.ld4(L.ne, e & 0x3fffffff));
+          continue;
+        }
         int4 q;
         bool ok;
         if (e >= 0) {
@@ -457,6 +509,7 @@ __device__ bool propagate(const G& g, volatile int* S, unsigned sb, const Tab<TS
   bool failed = false;
   for (;;) {
     bool ch = false, fl = false;
+    for (int i = g.rank(); i < (int)L.n_ne; i += g.size()) ch |= eval_ne(sb, tab.ld4(L.ne, i)) != 0ull;
     for (int i = g.rank(); i < (int)L.n_unit1; i += g.size()) {
       const int4 q = tab.ld4(L.unit1, i);
       if (unit_guard(sb, q.x, q.y)) ch |= unit_tell(sb, q.z, q.w);

@@ -297,7 +297,56 @@ Lowered lower_model(const pccp_model& m) {
     return true;
   };
 
+  // not(and(x + a <= y, y + b <= x)) compiles (propagation.cpp:350-360) to
+  //   [ub x - lb y <= -a] => ub x <- ub y + b - 1      [same] => lb y <- lb x + 1 - b
+  //   [ub y - lb x <= -b] => ub y <- ub x + a - 1      [same] => lb x <- lb y + 1 - a
+  struct NE {
+    std::int32_t x, a, b;
+  };
+  std::vector<NE> nes;
+  const bool ne_ok = !std::getenv("PCCP_NO_NE");
+  auto match_ne = [&](std::size_t i) -> bool {
+    if (!ne_ok || i + 4 > cmds.size()) return false;
+    auto guard_of = [](const CmdP& c, std::uint32_t plus, std::uint32_t minus, std::int32_t& rhs) {
+      if (c.guards.size() != 1) return false;
+      const GuardP& g = c.guards[0];
+      if (g.rel != PCCP_LEQ || g.lhs.k != 0 || g.lhs.terms.size() != 2) return false;
+      if (g.lhs.terms[0] != std::make_pair(std::int32_t{1}, plus)) return false;
+      if (g.lhs.terms[1] != std::make_pair(std::int32_t{-1}, minus)) return false;
+      rhs = g.rhs;
+      return true;
+    };
+    auto tell_of = [](const CmdP& c, bool upper, std::uint32_t lbw, std::uint32_t src, std::int64_t& k) {
+      if (c.kind != PCCP_INTERVAL || c.tw != lbw || c.sc) return false;
+      const std::optional<Expr>& e = upper ? c.ub : c.lb;
+      const std::optional<Expr>& other = upper ? c.lb : c.ub;
+      if (!e || other || e->terms.size() != 1 || e->terms[0] != std::make_pair(std::int32_t{1}, src)) return false;
+      k = e->k;
+      return true;
+    };
+    const std::uint32_t lx = cmds[i].tw, ly = cmds[i + 1].tw;
+    if (cmds[i].kind != PCCP_INTERVAL || cmds[i + 1].kind != PCCP_INTERVAL) return false;
+    if (lx >= 0xffffu || ly >= 0xffffu) return false;
+    std::int32_t r0, r1, r2, r3;
+    std::int64_t k0, k1, k2, k3;
+    if (!guard_of(cmds[i], lx + 1, ly, r0) || !tell_of(cmds[i], true, lx, ly + 1, k0)) return false;
+    if (!guard_of(cmds[i + 1], lx + 1, ly, r1) || r1 != r0 || !tell_of(cmds[i + 1], false, ly, lx, k1)) return false;
+    if (!guard_of(cmds[i + 2], ly + 1, lx, r2) || !tell_of(cmds[i + 2], true, ly, lx + 1, k2)) return false;
+    if (!guard_of(cmds[i + 3], ly + 1, lx, r3) || r3 != r2 || !tell_of(cmds[i + 3], false, lx, ly, k3)) return false;
+    const std::int64_t a = -std::int64_t{r0}, b = -std::int64_t{r2};
+    if (k0 != b - 1 || k1 != 1 - b || k2 != a - 1 || k3 != 1 - a) return false;
+    const std::int64_t lim = (1 << 30) - 2;
+    if (a < -lim || a > lim || b < -lim || b > lim) return false;
+    nes.push_back(NE{static_cast<std::int32_t>(lx | (ly << 16)), static_cast<std::int32_t>(a),
+                     static_cast<std::int32_t>(b)});
+    return true;
+  };
+
   for (std::size_t i = 0; i < cmds.size();) {
+    if (match_ne(i)) {
+      i += 4;
+      continue;
+    }
     if (const std::size_t used = match_row(i)) {
       i += used;
       continue;
@@ -387,6 +436,14 @@ Lowered lower_model(const pccp_model& m) {
     B.resize(off + n, 0);
     return off;
   };
+  L.n_ne = static_cast<std::uint32_t>(nes.size());
+  L.ne = reserve_arr(4 * L.n_ne);
+  for (std::uint32_t i = 0; i < L.n_ne; ++i) {
+    B[L.ne + 4 * i + 0] = nes[i].x;
+    B[L.ne + 4 * i + 1] = nes[i].a;
+    B[L.ne + 4 * i + 2] = nes[i].b;
+    B[L.ne + 4 * i + 3] = 0;
+  }
   L.n_unit1 = static_cast<std::uint32_t>(unit1.size());
   L.unit1 = reserve_arr(4 * L.n_unit1);
   for (std::uint32_t i = 0; i < L.n_unit1; ++i) {
@@ -435,6 +492,13 @@ Lowered lower_model(const pccp_model& m) {
           if (w2 >= m.n_words) continue;
           if (readers[w2].empty() || readers[w2].back() != e) readers[w2].push_back(e);
         }
+      }
+      for (std::uint32_t i = 0; i < nes.size(); ++i) {  // entry tag 01: fused not(and)
+        const std::int32_t e = static_cast<std::int32_t>(i | 0x40000000u);
+        const std::uint32_t lx = static_cast<std::uint32_t>(nes[i].x) & 0xffffu;
+        const std::uint32_t ly = static_cast<std::uint32_t>(nes[i].x) >> 16;
+        for (std::uint32_t w : {lx, lx + 1, ly, ly + 1})
+          if (readers[w].empty() || readers[w].back() != e) readers[w].push_back(e);
       }
     }
     std::uint32_t total = 0;

@@ -36,6 +36,9 @@ struct DeviceLayout {
   std::uint32_t unit1, n_unit1;          // int4 records: guard (a | b<<16, T), tell (k, tw | f<<15 | neg<<30 | up<<31)
   std::uint32_t unit2, unit2g, n_unit2;  // same + int2 second guard
   std::uint32_t zero_word;               // constant-zero word Z = n_words (store_stride > n_words)
+  // Fused not(and(x + a <= y, y + b <= x)) groups: the 4 commands compile_rec
+  // emits for it (propagation.cpp:350-360) read and write only lb/ub of x and y.
+  std::uint32_t ne, n_ne;                // int4 {lbx | lby << 16, a, b, 0}
   // Filtered rounds (stores of <= 64 words made only of unit records): a
   // round re-evaluates just the records that read a word changed in the
   // previous round (CSR lists per word, entry = record | unit2 << 31).

@@ -46,14 +46,16 @@ def lower(m):
     L.pccp_lower_only.argtypes = [C.POINTER(N.PccpModel), C.POINTER(N.PccpLoweringInfo), C.c_void_p]
     s, keep = m.tables().as_struct()
     info = N.PccpLoweringInfo()
-    sc = np.zeros(3, np.uint32)
+    sc = np.zeros(5, np.uint32)
     N.check(L.pccp_lower_only(C.byref(s), C.byref(info), sc.ctypes.data_as(C.c_void_p)))
     return info, sc
 
 
 def test_lowering_shapes():
     info, sc = lower(Model.nqueens(14))
-    assert info.n_folded == 28 and sc[0] == 1092 and info.n_generic == 0 and info.n_rows == 0
+    # every not(and(leq_offset, leq_offset)) fuses: 91 pairs x 3 offsets, nothing left over
+    assert info.n_folded == 28 and sc[3] == 273 and sc[0] == 0 and info.n_generic == 0 and info.n_rows == 0
+    assert sc[4] == 1  # filtered rounds
     info, sc = lower(Model.random_csp(1))
     assert info.n_rows == 690 and info.n_generic == 0
     info, sc = lower(Model.rcpsp_random(1, 30, 4))
