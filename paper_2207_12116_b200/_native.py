@@ -10,7 +10,7 @@ import ctypes as C
 import os
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "libpccp_b200.so")
+LIB_PATH = os.environ.get("PCCP_LIB") or os.path.join(HERE, "libpccp_b200.so")  # PCCP_LIB: build variants
 
 OK, EMODEL, ECUDA, ELIMIT, EARG = 0, 1, 2, 3, 4
 ZINC, ZDEC, BINC, BDEC, INTERVAL = 0, 1, 2, 3, 4

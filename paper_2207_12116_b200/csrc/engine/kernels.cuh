@@ -205,9 +205,11 @@ struct Tab<false> {
 };
 
 // ---- store access by 32-bit shared address -------------------------------------------
+// asm volatile keeps these loads in program order with the atomics below
+// (no "memory" clobber, so loop-invariant table arithmetic can still hoist).
 __device__ __forceinline__ int sld(unsigned a) {
   int v;
-  asm volatile("ld.volatile.shared.b32 %0, [%1];" : "=r"(v) : "r"(a) : "memory");
+  asm volatile("ld.volatile.shared.b32 %0, [%1];" : "=r"(v) : "r"(a));
   return v;
 }
 __device__ __forceinline__ int satom_max(unsigned a, int v) {
@@ -273,13 +275,18 @@ __device__ __forceinline__ unsigned long long eval_ne(unsigned sb, int4 q) {
   unsigned long long m = 0;
   auto bit = [](unsigned w) { return 1ull << (w & 63u); };  // any bit flags a change past 64 words
   if (small30(lx) & small30(ux) & small30(ly) & small30(uy)) {
-    if (ux - ly <= -a) {  // x - a... entailed: propagate not(y + b <= x) = x + 1 - b <= y
-      if (sjoin_min(ax + 4, uy + b - 1)) m |= bit(wx + 1);
-      if (sjoin_max(ay, lx + 1 - b)) m |= bit(wy);
-    }
-    if (uy - lx <= -b) {  // propagate not(x + a <= y) = y + 1 - a <= x
-      if (sjoin_min(ay + 4, ux + a - 1)) m |= bit(wy + 1);
-      if (sjoin_max(ax, ly + 1 - a)) m |= bit(wx);
+    // Branch-free up to the joins.  The snapshot doubles as the pre-join
+    // check: a bound only moves toward top, so a value that does not beat
+    // the snapshot cannot beat the current word either.
+    const bool g1 = ux - ly <= -a;  // x + a <= y entailed: enforce not(y + b <= x), i.e. x + 1 - b <= y
+    const bool g2 = uy - lx <= -b;  // y + b <= x entailed: enforce y + 1 - a <= x
+    const int v1 = uy + b - 1, v2 = lx + 1 - b, v3 = ux + a - 1, v4 = ly + 1 - a;
+    const bool c1 = g1 & (v1 < ux), c2 = g1 & (v2 > ly), c3 = g2 & (v3 < uy), c4 = g2 & (v4 > lx);
+    if (c1 | c2 | c3 | c4) {
+      if (c1 && satom_min(ax + 4, v1) > v1) m |= bit(wx + 1);
+      if (c2 && satom_max(ay, v2) < v2) m |= bit(wy);
+      if (c3 && satom_min(ay + 4, v3) > v3) m |= bit(wy + 1);
+      if (c4 && satom_max(ax, v4) < v4) m |= bit(wx);
     }
   } else {  // widened int64 arithmetic of command.cpp:11-27
     if (widen(ux) - widen(ly) <= -(long long)a) {

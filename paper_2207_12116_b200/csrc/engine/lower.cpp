@@ -465,9 +465,10 @@ Lowered lower_model(const pccp_model& m) {
     B[L.unit2g + 2 * i + 0] = unit2[i].second.first;
     B[L.unit2g + 2 * i + 1] = unit2[i].second.second;
   }
-  // Per-word reader lists for the filtered rounds.
+  // Per-word reader lists for the filtered rounds (opt-in, PCCP_FILTERED=1:
+  // with fused NE records the eventless loop needs ~30% fewer rounds and wins).
   L.filtered = (m.n_words <= 64 && smalls.empty() && rows.empty() && generic.empty() &&
-                !std::getenv("PCCP_EVENTLESS"))
+                std::getenv("PCCP_FILTERED") != nullptr)
                    ? 1u
                    : 0u;
   {

@@ -55,7 +55,7 @@ def test_lowering_shapes():
     info, sc = lower(Model.nqueens(14))
     # every not(and(leq_offset, leq_offset)) fuses: 91 pairs x 3 offsets, nothing left over
     assert info.n_folded == 28 and sc[3] == 273 and sc[0] == 0 and info.n_generic == 0 and info.n_rows == 0
-    assert sc[4] == 1  # filtered rounds
+    assert sc[4] == (1 if os.environ.get("PCCP_FILTERED") else 0)  # filtered rounds are opt-in
     info, sc = lower(Model.random_csp(1))
     assert info.n_rows == 690 and info.n_generic == 0
     info, sc = lower(Model.rcpsp_random(1, 30, 4))
