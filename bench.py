@@ -250,6 +250,7 @@ def main():
 
     for _ in range(max(a.warmup, 0)):
         step()
+    eng.load(tables)
     info = eng.lowering_info()
 
     sampler = ClockSampler([local]) if rank == 0 else None
