@@ -301,6 +301,76 @@ __device__ __forceinline__ unsigned long long eval_ne(unsigned sb, int4 q) {
   return m;
 }
 
+// Fused reification b <-> (x + p <= y and y + q <= x): the 11 commands of
+// compile_reified (propagation.cpp:415-431) from one read of the 6 words.
+// q = {lbx | lby << 16, lbb, p, q}.  Returns true iff a word changed.
+__device__ __forceinline__ bool eval_reif(unsigned sb, int4 r) {
+  const unsigned ax = sb + (((unsigned)r.x & 0xffffu) << 2), ay = sb + (((unsigned)r.x >> 16) << 2);
+  const unsigned ab = sb + ((unsigned)r.y << 2);
+  const int lx = sld(ax), ux = sld(ax + 4), ly = sld(ay), uy = sld(ay + 4), lb = sld(ab), ub = sld(ab + 4);
+  const int p = r.z, q = r.w;
+  const bool bt = lb > 0, bf = ub <= 0;  // [lb b > 0], [ub b <= 0]
+  int nlb = INT_MIN, nub = INT_MAX, nux = INT_MAX, nly = INT_MIN, nuy = INT_MAX, nlx = INT_MIN;
+  if (small30(lx) & small30(ux) & small30(ly) & small30(uy)) {
+    const bool eA = ux - ly <= -p, eB = uy - lx <= -q;  // entailment of x + p <= y, y + q <= x
+    const bool nA = lx - uy > -p, nB = ly - ux > -q;    // entailment of their negations
+    if (eA & eB) nlb = nub = 1;
+    if (nA | nB) {
+      nlb = max(nlb, 0);
+      nub = min(nub, 0);
+    }
+    if (bt) {  // b = 1 activates x + p <= y and y + q <= x
+      nux = uy - p;
+      nly = lx + p;
+      nuy = ux - q;
+      nlx = ly + q;
+    }
+    if (bf & eA) {  // b = 0 and x + p <= y entailed: y + q <= x must fail, x + 1 - q <= y
+      nux = min(nux, uy - 1 + q);
+      nly = max(nly, lx + 1 - q);
+    }
+    if (bf & eB) {  // symmetric: y + 1 - p <= x
+      nuy = min(nuy, ux - 1 + p);
+      nlx = max(nlx, ly + 1 - p);
+    }
+  } else {  // widened int64 arithmetic of command.cpp:11-27
+    const long long wlx = widen(lx), wux = widen(ux), wly = widen(ly), wuy = widen(uy);
+    const bool eA = wux - wly <= -(long long)p, eB = wuy - wlx <= -(long long)q;
+    const bool nA = wlx - wuy > -(long long)p, nB = wly - wux > -(long long)q;
+    if (eA & eB) nlb = nub = 1;
+    if (nA | nB) {
+      nlb = max(nlb, 0);
+      nub = min(nub, 0);
+    }
+    if (bt) {
+      nux = narrow(wuy - p);
+      nly = narrow(wlx + p);
+      nuy = narrow(wux - q);
+      nlx = narrow(wly + q);
+    }
+    if (bf & eA) {
+      nux = min(nux, narrow(wuy - 1 + q));
+      nly = max(nly, narrow(wlx + 1 - q));
+    }
+    if (bf & eB) {
+      nuy = min(nuy, narrow(wux - 1 + p));
+      nlx = max(nlx, narrow(wly + 1 - p));
+    }
+  }
+  // joins; the snapshot is the pre-check (bounds only move toward top)
+  const bool c1 = nlb > lb, c2 = nub < ub, c3 = nux < ux, c4 = nly > ly, c5 = nuy < uy, c6 = nlx > lx;
+  bool ch = false;
+  if (c1 | c2 | c3 | c4 | c5 | c6) {
+    if (c1) ch |= satom_max(ab, nlb) < nlb;
+    if (c2) ch |= satom_min(ab + 4, nub) > nub;
+    if (c3) ch |= satom_min(ax + 4, nux) > nux;
+    if (c4) ch |= satom_max(ay, nly) < nly;
+    if (c5) ch |= satom_min(ay + 4, nuy) > nuy;
+    if (c6) ch |= satom_max(ax, nlx) < nlx;
+  }
+  return ch;
+}
+
 // ---- propagators -----------------------------------------------------------------
 
 // LinExpr::eval over a flat [k, n, (coef, word)*n] expression (command.cpp:21-27).
@@ -517,6 +587,7 @@ __device__ bool propagate(const G& g, volatile int* S, unsigned sb, const Tab<TS
   for (;;) {
     bool ch = false, fl = false;
     for (int i = g.rank(); i < (int)L.n_ne; i += g.size()) ch |= eval_ne(sb, tab.ld4(L.ne, i)) != 0ull;
+    for (int i = g.rank(); i < (int)L.n_reif; i += g.size()) ch |= eval_reif(sb, tab.ld4(L.reif, i));
     for (int i = g.rank(); i < (int)L.n_unit1; i += g.size()) {
       const int4 q = tab.ld4(L.unit1, i);
       if (unit_guard(sb, q.x, q.y)) ch |= unit_tell(sb, q.z, q.w);

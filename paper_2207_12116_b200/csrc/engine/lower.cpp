@@ -342,7 +342,86 @@ Lowered lower_model(const pccp_model& m) {
     return true;
   };
 
+  // compile_reified(b, and(x + p <= y, y + q <= x)) (propagation.cpp:415-431,
+  // rcpsp.cpp:239-250 with p = 0, q = 1 - d) emits, in order:
+  //   [eA, eB] => b <- (1,1)   [nA] => b <- (0,0)   [nB] => b <- (0,0)
+  //   [lb b > 0] => ub x <- ub y - p, lb y <- lb x + p, ub y <- ub x - q, lb x <- lb y + q
+  //   [ub b <= 0, eA] => ub x <- ub y - (1-q), lb y <- lb x + (1-q)
+  //   [ub b <= 0, eB] => ub y <- ub x - (1-p), lb x <- lb y + (1-p)
+  // with eA: ub x - lb y <= -p, eB: ub y - lb x <= -q, nA: lb x - ub y > -p, nB: lb y - ub x > -q.
+  struct Reif {
+    std::int32_t xy, b, p, q;
+  };
+  std::vector<Reif> reifs;
+  const bool reif_ok = !std::getenv("PCCP_NO_REIF");
+  auto match_reif = [&](std::size_t i) -> bool {
+    if (!reif_ok || i + 11 > cmds.size()) return false;
+    using P = std::pair<std::int32_t, std::uint32_t>;
+    auto guard2 = [](const GuardP& g, int rel, std::int32_t rhs, P t0, P t1) {
+      return g.rel == rel && g.rhs == rhs && g.lhs.k == 0 && g.lhs.terms.size() == 2 && g.lhs.terms[0] == t0 &&
+             g.lhs.terms[1] == t1;
+    };
+    auto guard1 = [](const GuardP& g, int rel, std::uint32_t w) {
+      return g.rel == rel && g.rhs == 0 && g.lhs.k == 0 && g.lhs.terms.size() == 1 &&
+             g.lhs.terms[0] == P{1, w};
+    };
+    auto const_b = [](const CmdP& c, std::uint32_t bw, std::int32_t v) {
+      return c.kind == PCCP_INTERVAL && c.tw == bw && !c.sc && c.lb && c.ub && c.lb->k == v && c.ub->k == v &&
+             c.lb->terms.empty() && c.ub->terms.empty();
+    };
+    auto tell = [](const CmdP& c, std::uint32_t lbw, bool upper, std::int64_t k, std::uint32_t src) {
+      if (c.kind != PCCP_INTERVAL || c.tw != lbw || c.sc) return false;
+      const std::optional<Expr>& e = upper ? c.ub : c.lb;
+      const std::optional<Expr>& o = upper ? c.lb : c.ub;
+      return e && !o && e->k == k && e->terms.size() == 1 && e->terms[0] == P{1, src};
+    };
+    const CmdP& c0 = cmds[i];
+    if (c0.guards.size() != 2 || c0.kind != PCCP_INTERVAL) return false;
+    const GuardP& gA = c0.guards[0];
+    const GuardP& gB = c0.guards[1];
+    if (gA.lhs.terms.size() != 2 || gB.lhs.terms.size() != 2) return false;
+    const std::uint32_t ux = gA.lhs.terms[0].second, ly = gA.lhs.terms[1].second;
+    if (ux == 0 || ly + 1 >= m.n_words || !is_lb[ux - 1] || !is_lb[ly]) return false;
+    const std::uint32_t lx = ux - 1, uy = ly + 1, bw = c0.tw;
+    const std::int64_t p = -std::int64_t{gA.rhs}, q = -std::int64_t{gB.rhs};
+    const std::int64_t lim = (1 << 29);
+    if (p < -lim || p > lim || q < -lim || q > lim) return false;
+    if (lx >= 0xffffu || ly >= 0xffffu || bw >= 0xffffu) return false;
+    const std::int32_t rp = gA.rhs, rq = gB.rhs;
+    if (!guard2(gA, PCCP_LEQ, rp, P{1, ux}, P{-1, ly}) || !guard2(gB, PCCP_LEQ, rq, P{1, uy}, P{-1, lx})) return false;
+    if (!const_b(c0, bw, 1)) return false;
+    const CmdP &c1 = cmds[i + 1], &c2 = cmds[i + 2];
+    if (c1.guards.size() != 1 || !guard2(c1.guards[0], PCCP_GT, rp, P{1, lx}, P{-1, uy}) || !const_b(c1, bw, 0))
+      return false;
+    if (c2.guards.size() != 1 || !guard2(c2.guards[0], PCCP_GT, rq, P{1, ly}, P{-1, ux}) || !const_b(c2, bw, 0))
+      return false;
+    for (int k = 3; k <= 6; ++k) {
+      const CmdP& c = cmds[i + k];
+      if (c.guards.size() != 1 || !guard1(c.guards[0], PCCP_GT, bw)) return false;
+    }
+    if (!tell(cmds[i + 3], lx, true, -p, uy) || !tell(cmds[i + 4], ly, false, p, lx) ||
+        !tell(cmds[i + 5], ly, true, -q, ux) || !tell(cmds[i + 6], lx, false, q, ly))
+      return false;
+    for (int k = 7; k <= 10; ++k) {
+      const CmdP& c = cmds[i + k];
+      if (c.guards.size() != 2 || !guard1(c.guards[0], PCCP_LEQ, bw + 1)) return false;
+      const GuardP& g = c.guards[1];
+      if (k <= 8 ? !guard2(g, PCCP_LEQ, rp, P{1, ux}, P{-1, ly}) : !guard2(g, PCCP_LEQ, rq, P{1, uy}, P{-1, lx}))
+        return false;
+    }
+    if (!tell(cmds[i + 7], lx, true, -(1 - q), uy) || !tell(cmds[i + 8], ly, false, 1 - q, lx) ||
+        !tell(cmds[i + 9], ly, true, -(1 - p), ux) || !tell(cmds[i + 10], lx, false, 1 - p, ly))
+      return false;
+    reifs.push_back(Reif{static_cast<std::int32_t>(lx | (ly << 16)), static_cast<std::int32_t>(bw),
+                         static_cast<std::int32_t>(p), static_cast<std::int32_t>(q)});
+    return true;
+  };
+
   for (std::size_t i = 0; i < cmds.size();) {
+    if (match_reif(i)) {
+      i += 11;
+      continue;
+    }
     if (match_ne(i)) {
       i += 4;
       continue;
@@ -444,6 +523,14 @@ Lowered lower_model(const pccp_model& m) {
     B[L.ne + 4 * i + 2] = nes[i].b;
     B[L.ne + 4 * i + 3] = 0;
   }
+  L.n_reif = static_cast<std::uint32_t>(reifs.size());
+  L.reif = reserve_arr(4 * L.n_reif);
+  for (std::uint32_t i = 0; i < L.n_reif; ++i) {
+    B[L.reif + 4 * i + 0] = reifs[i].xy;
+    B[L.reif + 4 * i + 1] = reifs[i].b;
+    B[L.reif + 4 * i + 2] = reifs[i].p;
+    B[L.reif + 4 * i + 3] = reifs[i].q;
+  }
   L.n_unit1 = static_cast<std::uint32_t>(unit1.size());
   L.unit1 = reserve_arr(4 * L.n_unit1);
   for (std::uint32_t i = 0; i < L.n_unit1; ++i) {
@@ -467,7 +554,7 @@ Lowered lower_model(const pccp_model& m) {
   }
   // Per-word reader lists for the filtered rounds (opt-in, PCCP_FILTERED=1:
   // with fused NE records the eventless loop needs ~30% fewer rounds and wins).
-  L.filtered = (m.n_words <= 64 && smalls.empty() && rows.empty() && generic.empty() &&
+  L.filtered = (m.n_words <= 64 && smalls.empty() && rows.empty() && generic.empty() && reifs.empty() &&
                 std::getenv("PCCP_FILTERED") != nullptr)
                    ? 1u
                    : 0u;

@@ -39,6 +39,9 @@ struct DeviceLayout {
   // Fused not(and(x + a <= y, y + b <= x)) groups: the 4 commands compile_rec
   // emits for it (propagation.cpp:350-360) read and write only lb/ub of x and y.
   std::uint32_t ne, n_ne;                // int4 {lbx | lby << 16, a, b, 0}
+  // Fused compile_reified(b, and(x + p <= y, y + q <= x)): the 11 commands of
+  // propagation.cpp:415-431 over lb/ub of x, y and b (RCPSP overlaps).
+  std::uint32_t reif, n_reif;            // int4 {lbx | lby << 16, lbb, p, q}
   // Filtered rounds (stores of <= 64 words made only of unit records): a
   // round re-evaluates just the records that read a word changed in the
   // previous round (CSR lists per word, entry = record | unit2 << 31).

@@ -58,9 +58,12 @@ def main():
                 r = eng.solve(timeout_s=a.timeout)
                 dt = time.time() - t
                 ok = m.check_solution(r.best_words) if r.best_words is not None else None
-                print(w, s, json.dumps(info))
-                print(w, s, r.status, r.objective, ok, json.dumps(r.stats), r.improvements[:8], f"wall {dt:.3f}s",
-                      f"nodes/s {r.stats['nodes'] / dt:.3e}")
+                st = r.stats
+                last = r.improvements[-1][1] if r.improvements else None
+                print(f"{w} seed={s} {r.status} obj={r.objective} valid={ok} nodes={st['nodes']} rounds={st['rounds']} "
+                      f"wall={dt:.3f}s kernel={st['kernel_ms']:.1f}ms t_best={last} nodes/s={st['nodes'] / dt:.3e} "
+                      f"evals/s={st['evals'] / dt:.3e} sub={st['subproblems']} cta={info['group_threads']}"
+                      f" smem_table={info['table_in_smem']}")
         sys.stdout.flush()
 
 
