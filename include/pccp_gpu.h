@@ -108,6 +108,10 @@ typedef struct pccp_gpu_cfg {
   int32_t shard_count;   /* 0/1 = unsharded */
   int32_t hash;          /* 1: accumulate the order-independent fixed-point hash-sum */
   int32_t verbose;
+  int32_t value_order;   /* DFS branch order: 0 left (x <= mid) first, as dfs() (solver.cpp:139-143);
+                            1 right first; 2 mixed (odd groups right first); -1 = 0.
+                            The explored tree is the same,
+                            so counts, optima and proofs are unchanged; only node order differs. */
 } pccp_gpu_cfg;
 
 typedef struct pccp_limits {
@@ -136,6 +140,8 @@ typedef struct pccp_stats {
   uint64_t h2d_bytes;   /* host->device bytes moved by this call */
   uint64_t d2h_bytes;   /* device->host bytes moved by this call */
   double device_ms;     /* device time of the whole call (CUDA events on the engine stream) */
+  uint64_t bfs_levels;  /* EPS decomposition levels */
+  uint64_t donations;   /* subtrees handed from busy to idle groups (dynamic load balancing) */
 } pccp_stats;
 
 typedef struct pccp_enum_result {
@@ -226,9 +232,9 @@ typedef struct pccp_lowering_info {
 int pccp_gpu_lowering_info(pccp_gpu_ctx* ctx, pccp_lowering_info* out);
 
 /* Host-only: lowers the tables without a device (validation / diagnostics).
- * shape_counts (optional, 5 entries): unit records with <= 1 guard, unit
+ * shape_counts (optional, 6 entries): unit records with <= 1 guard, unit
  * records with 2 guards, commands dropped as never-firing, fused not(and)
- * groups, filtered-rounds flag. */
+ * constraints, filtered-rounds flag, fused reifications. */
 int pccp_lower_only(const pccp_model* model, pccp_lowering_info* out, uint32_t* shape_counts);
 
 #ifdef __cplusplus

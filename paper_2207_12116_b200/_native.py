@@ -48,6 +48,7 @@ class PccpGpuCfg(C.Structure):
         ("shard_count", C.c_int32),
         ("hash", C.c_int32),
         ("verbose", C.c_int32),
+        ("value_order", C.c_int32),
     ]
 
 
@@ -74,6 +75,8 @@ class PccpStats(C.Structure):
         ("h2d_bytes", C.c_uint64),
         ("d2h_bytes", C.c_uint64),
         ("device_ms", C.c_double),
+        ("bfs_levels", C.c_uint64),
+        ("donations", C.c_uint64),
     ]
 
 

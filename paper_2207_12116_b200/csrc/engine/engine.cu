@@ -111,7 +111,7 @@ struct pccp_gpu_ctx {
   int store_stride = 4;
   int table_in_smem = 0;
 
-  DBuf<int> fa, fb, ia, ib, stack, best, io;
+  DBuf<int> fa, fb, ia, ib, stack, best, io, mailbox, waitq;
   DBuf<unsigned char> flags, st;
   DBuf<unsigned> rnd;
   dev::Globals* G = nullptr;
@@ -168,7 +168,7 @@ void plan(pccp_gpu_ctx* c) {
   const int gt = c->cfg.group_threads;
   c->warp = gt == 32 || (gt == 0 && L.n_words <= 256);
   if (c->warp) {
-    c->gpc = c->cfg.groups_per_cta > 0 ? std::min(c->cfg.groups_per_cta, 32) : 8;
+    c->gpc = c->cfg.groups_per_cta > 0 ? std::min(c->cfg.groups_per_cta, 8) : 8;  // MaxThreads<WarpGroup>
     c->block = 32 * c->gpc;
   } else {
     int t = gt;
@@ -232,7 +232,7 @@ struct RunOut {
   dev::Globals g;
   double decompose_ms = 0, kernel_ms = 0, elapsed_ms = 0;
   std::uint64_t subproblems = 0;
-  std::uint64_t bfs_rounds = 0, launches = 0, h2d = 0, d2h = 0;
+  std::uint64_t bfs_rounds = 0, launches = 0, h2d = 0, d2h = 0, levels = 0;
   double device_ms = 0;
 };
 
@@ -333,6 +333,20 @@ void run_search(pccp_gpu_ctx* c, int mode, const int32_t* root_words, int depth_
     P.stack_pool = c->stack.p;
     P.stack_depth = dmax;
     P.entry_stride = entry;
+    // dynamic load balancing: per-group mailboxes + the wait ring
+    P.balance = std::getenv("PCCP_NO_BALANCE") ? 0 : 1;
+    P.n_groups = c->groups();
+    P.mb_stride = (int)align4((std::uint32_t)nw + 3);
+    c->mailbox.ensure((size_t)P.n_groups * (size_t)P.mb_stride);
+    c->waitq.ensure((size_t)P.n_groups);
+    CK(cudaMemsetAsync(c->mailbox.p, 0, (size_t)P.n_groups * P.mb_stride * 4, c->stream));
+    CK(cudaMemsetAsync(c->waitq.p, 0xff, (size_t)P.n_groups * 4, c->stream));
+    const int active = P.n_groups;
+    CK(cudaMemcpyAsync(&c->G->active, &active, sizeof(int), cudaMemcpyHostToDevice, c->stream));
+    P.mailbox = c->mailbox.p;
+    P.value_order = c->cfg.value_order >= 0 ? std::min(c->cfg.value_order, 2) : 0;
+    if (const char* vo = std::getenv("PCCP_VALUE_ORDER")) P.value_order = std::atoi(vo);
+    P.waitq = c->waitq.p;
     C.count = 1;
     dev::k_search<Gp, TS><<<c->ctas, c->block, c->smem, c->stream>>>(M, C, P);
     CK(cudaGetLastError());
@@ -344,6 +358,7 @@ void run_search(pccp_gpu_ctx* c, int mode, const int32_t* root_words, int depth_
   CK(cudaStreamSynchronize(c->stream));
   out.d2h += sizeof(dev::Globals);
   out.launches = c->launches - launches0;
+  out.levels = (std::uint64_t)level;
   float ms = 0;
   CK(cudaEventElapsedTime(&ms, c->ev[0], c->ev[2]));
   out.device_ms = ms;
@@ -379,6 +394,8 @@ void fill_stats(const pccp_gpu_ctx* c, const RunOut& r, pccp_stats& s) {
   s.h2d_bytes = r.h2d;
   s.d2h_bytes = r.d2h;
   s.device_ms = r.device_ms;
+  s.bfs_levels = r.levels;
+  s.donations = r.g.donations;
 }
 
 void check_loaded(const pccp_gpu_ctx* c) {
@@ -446,6 +463,8 @@ void pccp_gpu_close(pccp_gpu_ctx* c) {
   c->ia.release();
   c->ib.release();
   c->stack.release();
+  c->mailbox.release();
+  c->waitq.release();
   c->best.release();
   c->io.release();
   c->flags.release();
@@ -530,6 +549,7 @@ int pccp_lower_only(const pccp_model* m, pccp_lowering_info* o, uint32_t* shape_
       shape_counts[2] = low.n_dropped;
       shape_counts[3] = L.n_ne;
       shape_counts[4] = L.filtered;
+      shape_counts[5] = L.n_reif;
     }
     return PCCP_OK;
   });

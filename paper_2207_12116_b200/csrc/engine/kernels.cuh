@@ -51,6 +51,11 @@ struct Globals {
   int impr_val[64];
   unsigned long long impr_ns[64];
   int error_code;
+  // dynamic load balancing (search.cuh maybe_donate)
+  int hungry;                   // idle groups waiting for a donation
+  int active;                   // groups exploring, or promised a donation
+  unsigned wait_head, wait_tail;
+  unsigned long long donations;
 };
 
 __device__ __forceinline__ unsigned long long globaltimer() {

@@ -209,9 +209,22 @@ struct GroupOf<CtaGroup> {
   static __device__ __forceinline__ int per_cta() { return 1; }
 };
 
+// Launch bounds: warp groups run <= 8 warps per CTA; CTA groups up to 1024
+// threads.  Both give ptxas a 64-register budget (at least 4 CTAs of 8 warps).
+template <class G>
+struct MaxThreads {
+  static constexpr int value = 1024;
+  static constexpr int min_blocks = 1;
+};
+template <>
+struct MaxThreads<WarpGroup> {
+  static constexpr int value = 256;
+  static constexpr int min_blocks = 4;
+};
+
 // ---- K1: batched fixed points (run_sequential on N independent stores) ---------
 template <class G, bool TS>
-__global__ void k_propagate(Model M, int* stores, int n, int stride, unsigned char* status, unsigned* rounds,
+__global__ void __launch_bounds__(MaxThreads<G>::value, MaxThreads<G>::min_blocks) k_propagate(Model M, int* stores, int n, int stride, unsigned char* status, unsigned* rounds,
                             int fold) {
   const Frame f = frame(M);
   const G g = GroupOf<G>::make(f);
@@ -241,7 +254,7 @@ __global__ void k_propagate(Model M, int* stores, int n, int stride, unsigned ch
 
 // ---- the problem root: fold, objective, fixed point, classification ----------------
 template <class G, bool TS>
-__global__ void k_root(Model M, SearchCtl C, int* store, unsigned char* flag) {
+__global__ void __launch_bounds__(MaxThreads<G>::value, MaxThreads<G>::min_blocks) k_root(Model M, SearchCtl C, int* store, unsigned char* flag) {
   const Frame f = frame(M);
   const G g = GroupOf<G>::make(f);
   const Tab<TS> tab = make_tab<TS>(f);
@@ -274,7 +287,7 @@ __global__ void k_root(Model M, SearchCtl C, int* store, unsigned char* flag) {
 // Parent p's children go to slots 2p (left, x <= mid) and 2p+1 (right); the
 // compaction below keeps BFS order, so the frontier is identical on every GPU.
 template <class G, bool TS>
-__global__ void k_expand(Model M, SearchCtl C, const int* parents, const int* parent_idx, int n_par, int stride,
+__global__ void __launch_bounds__(MaxThreads<G>::value, MaxThreads<G>::min_blocks) k_expand(Model M, SearchCtl C, const int* parents, const int* parent_idx, int n_par, int stride,
                          int child_depth, int* children, unsigned char* flags) {
   const Frame f = frame(M);
   const G g = GroupOf<G>::make(f);
@@ -375,15 +388,74 @@ struct SearchParams {
   int* stack_pool;
   int stack_depth;   // entries per group
   int entry_stride;  // words per entry: store + (lbw, mid, depth)
+  // dynamic load balancing (donation of the shallowest pending right branch)
+  int balance;
+  int* mailbox;      // per group: store (n_words) + (unused, depth, state)
+  int mb_stride;
+  int* waitq;        // ring of idle group ids (-1: empty)
+  int n_groups;
+  int value_order;   // 0 left first, 1 right first, 2 odd groups right first
 };
+
+// A pending stack entry stores (parent fixed point, lbw | pending_left << 31,
+// mid, depth); apply its pending branch to a store.
+__device__ __forceinline__ void apply_pending(int* dst, int lbw_tag, int mid) {
+  const int lbw = lbw_tag & 0x7fffffff;
+  if (lbw_tag < 0) {  // pending left branch: x <= mid
+    if (mid < dst[lbw + 1]) dst[lbw + 1] = mid;
+  } else if (mid + 1 > dst[lbw]) {  // pending right branch: x >= mid+1
+    dst[lbw] = mid + 1;
+  }
+}
+
+// Donation: an idle group registers in the wait ring and announces hunger; a
+// busy group that sees hunger and has >= 2 pending right branches claims one
+// unit of hunger, takes the receiver id, marks it active (so termination —
+// no active group — can never be observed mid-handoff), and writes its
+// shallowest pending node (parent fixed point + right decision, not yet
+// propagated) into the receiver's mailbox.  The receiver materialises and
+// counts that node itself, so every node is still processed exactly once.
+template <class G>
+__device__ __forceinline__ void maybe_donate(const G& g, const SearchParams& P, Globals* Gl, int* stk, int nw,
+                                             int& bot, int sp) {
+  if (sp - bot < 2) return;
+  int give = 0;
+  if (g.rank() == 0 && *(volatile int*)&Gl->hungry > 0) {
+    if (atomicAdd(&Gl->hungry, -1) > 0) give = 1;
+    else atomicAdd(&Gl->hungry, 1);
+  }
+  if (!g.bcast0(give)) return;
+  int recv = -1;
+  if (g.rank() == 0) {
+    const unsigned h = atomicAdd(&Gl->wait_head, 1u) % (unsigned)P.n_groups;
+    while ((recv = *(volatile int*)&P.waitq[h]) < 0) {
+    }
+    P.waitq[h] = -1;
+    atomicAdd(&Gl->active, 1);
+    atomicAdd(&Gl->donations, 1ull);
+  }
+  recv = g.bcast0(recv);
+  const int* ent = stk + (size_t)bot * P.entry_stride;
+  int* dst = P.mailbox + (size_t)recv * P.mb_stride;
+  for (int i = g.rank(); i < nw; i += g.size()) dst[i] = ent[i];
+  g.sync();
+  if (g.rank() == 0) {
+    apply_pending(dst, ent[nw], ent[nw + 1]);
+    dst[nw + 1] = ent[nw + 2] + 1;
+    __threadfence();
+    *(volatile int*)&dst[nw + 2] = 1;
+  }
+  ++bot;
+}
 
 // ---- K4 + K6: persistent DFS over the EPS work queue ------------------------------
 // Each group pops subproblem k (this GPU owns frontier i = shard_index +
 // k*shard_count) and explores it depth-first, left branch first (dfs,
 // solver.cpp:122-146).  A branching node pushes (its fixed point, right
-// decision) and descends left in place; a leaf pops.
+// decision) and descends left in place; a leaf pops.  When the queue is
+// empty, idle groups are fed by donations (maybe_donate).
 template <class G, bool TS>
-__global__ void k_search(Model M, SearchCtl C, SearchParams P) {
+__global__ void __launch_bounds__(MaxThreads<G>::value, MaxThreads<G>::min_blocks) k_search(Model M, SearchCtl C, SearchParams P) {
   const Frame f = frame(M);
   const G g = GroupOf<G>::make(f);
   const Tab<TS> tab = make_tab<TS>(f);
@@ -395,33 +467,70 @@ __global__ void k_search(Model M, SearchCtl C, SearchParams P) {
   int* stk = P.stack_pool + (size_t)gid * (size_t)P.stack_depth * (size_t)P.entry_stride;
   Globals* Gl = C.G;
   Cnt cnt;
+  bool queue_open = true;
+  const bool right_first = P.value_order == 1 || (P.value_order == 2 && (gid & 1));
   for (;;) {
-    int k = 0;
-    if (g.rank() == 0) k = (int)atomicAdd(&Gl->cursor, 1u);
-    k = g.bcast0(k);
-    const long long idx = (long long)P.shard_index + (long long)k * (long long)P.shard_count;
-    if (idx >= P.n_frontier) break;
-    int stop = 0;
-    if (g.rank() == 0) stop = *(volatile int*)&Gl->stop;
-    if (g.bcast0(stop)) {
-      if (g.rank() == 0) Gl->incomplete = 1;
-      break;
-    }
-    copy_words(g, S, P.frontier + (size_t)P.frontier_idx[idx] * P.stride, nw);
-    g.sync();
     int depth = P.depth0;
-    int sp = 0;
-    // Enumeration: the frontier node was counted and classified during the
-    // decomposition.  Minimisation: re-materialise it with the current bound,
-    // as dfs() does for its subproblem root.
     bool need_prop = C.mode == 1;
-    bool abandoned = false;
     unsigned long long dirty = 0;  // words changed since the store was last a fixed point
+    if (queue_open) {
+      int k = 0;
+      if (g.rank() == 0) k = (int)atomicAdd(&Gl->cursor, 1u);
+      k = g.bcast0(k);
+      const long long idx = (long long)P.shard_index + (long long)k * (long long)P.shard_count;
+      if (idx >= P.n_frontier) queue_open = false;
+      else {
+        int stop = 0;
+        if (g.rank() == 0) stop = *(volatile int*)&Gl->stop;
+        if (g.bcast0(stop)) {
+          if (g.rank() == 0) Gl->incomplete = 1;
+          break;
+        }
+        copy_words(g, S, P.frontier + (size_t)P.frontier_idx[idx] * P.stride, nw);
+        g.sync();
+      }
+    }
+    if (!queue_open) {
+      if (!P.balance) break;
+      // idle: register, then wait for a donation or for global quiescence
+      int got = 0;
+      if (g.rank() == 0) {
+        atomicAdd(&Gl->active, -1);
+        const unsigned t = atomicAdd(&Gl->wait_tail, 1u) % (unsigned)P.n_groups;
+        *(volatile int*)&P.waitq[t] = gid;
+        __threadfence();
+        atomicAdd(&Gl->hungry, 1);
+        volatile int* state = (volatile int*)&P.mailbox[(size_t)gid * P.mb_stride + nw + 2];
+        for (;;) {
+          if (*state == 1) {
+            got = 1;
+            break;
+          }
+          if (*(volatile int*)&Gl->active == 0 || *(volatile int*)&Gl->stop) break;
+          __nanosleep(200);
+        }
+      }
+      if (!g.bcast0(got)) break;
+      __threadfence();
+      const int* mb = P.mailbox + (size_t)gid * P.mb_stride;
+      copy_words(g, S, mb, nw);
+      depth = *(volatile const int*)&mb[nw + 1];
+      g.sync();
+      if (g.rank() == 0) *(volatile int*)&P.mailbox[(size_t)gid * P.mb_stride + nw + 2] = 0;
+      need_prop = true;
+      dirty = kAllDirty;
+    }
+    int sp = 0, bot = 0;
+    bool abandoned = false;
+    // Enumeration: a frontier node was counted and classified during the
+    // decomposition.  Minimisation: re-materialise it with the current bound,
+    // as dfs() does for its subproblem root.  A donated node is unpropagated.
     if (need_prop) {
-      dirty = join_objective(g, S, L, C);
+      dirty |= join_objective(g, S, L, C);
       g.sync();
     }
     for (;;) {
+      if (P.balance) maybe_donate(g, P, Gl, stk, nw, bot, sp);
       int lbw = 0, mid = 0, e;
       if (need_prop) {
         if (should_stop(g, C)) {
@@ -452,32 +561,35 @@ __global__ void k_search(Model M, SearchCtl C, SearchParams P) {
         }
         int* ent = stk + (size_t)sp * P.entry_stride;
         copy_out(g, ent, S, nw);
-        g.sync();  // the parent fixed point is saved before the left decision lands
+        g.sync();  // the parent fixed point is saved before the first decision lands
         if (g.rank() == 0) {
-          ent[nw] = lbw;
+          ent[nw] = right_first ? (int)((unsigned)lbw | 0x80000000u) : lbw;  // the branch left pending
           ent[nw + 1] = mid;
           ent[nw + 2] = depth;
-          join_min(S, lbw + 1, mid);  // left branch: x <= mid
+          if (right_first) join_max(S, lbw, mid + 1);  // x >= mid+1 first
+          else join_min(S, lbw + 1, mid);              // x <= mid first (dfs(), solver.cpp:139-143)
         }
         ++sp;
         ++depth;
         g.sync();
-        dirty = word_bit(lbw + 1) | join_objective(g, S, L, C);
+        dirty = word_bit(right_first ? lbw : lbw + 1) | join_objective(g, S, L, C);
         g.sync();
         need_prop = true;
         continue;
       }
-      if (sp == 0) break;
+      if (sp == bot) break;
       --sp;
       const int* ent = stk + (size_t)sp * P.entry_stride;
       g.sync();  // no thread still reads the leaf (hash, branch) when it is overwritten
       copy_words(g, S, ent, nw);
       g.sync();
+      const int tag = ent[nw];
       if (g.rank() == 0) {
-        join_max(S, ent[nw], ent[nw + 1] + 1);  // right branch: x >= mid+1
+        if (tag < 0) join_min(S, (tag & 0x7fffffff) + 1, ent[nw + 1]);  // pending x <= mid
+        else join_max(S, tag, ent[nw + 1] + 1);                        // pending x >= mid+1
       }
       depth = ent[nw + 2] + 1;
-      dirty = word_bit(ent[nw]);
+      dirty = word_bit(tag < 0 ? (tag & 0x7fffffff) + 1 : tag);
       g.sync();
       dirty |= join_objective(g, S, L, C);
       g.sync();
@@ -487,7 +599,10 @@ __global__ void k_search(Model M, SearchCtl C, SearchParams P) {
       if (abandoned) Gl->incomplete = 1;
       flush(Gl, cnt);
     }
-    if (abandoned) break;
+    if (abandoned) {
+      if (g.rank() == 0) atomicAdd(&Gl->active, -1);
+      break;
+    }
   }
   if (g.rank() == 0) flush(Gl, cnt);
 }

@@ -46,10 +46,11 @@ class Engine:
     """One device context (one GPU).  Not re-entrant."""
 
     def __init__(self, device: int = 0, *, group_threads: int = 0, groups_per_cta: int = 0, ctas_per_sm: int = 0,
-                 eps_factor: int = 0, shard_index: int = 0, shard_count: int = 1, hash: bool = False):
+                 eps_factor: int = 0, shard_index: int = 0, shard_count: int = 1, hash: bool = False,
+                 value_order: int = -1):
         L = N.lib()
         self.cfg = N.PccpGpuCfg(device, group_threads, groups_per_cta, ctas_per_sm, eps_factor, shard_index,
-                                shard_count, int(hash), 0)
+                                shard_count, int(hash), 0, value_order)
         h = C.c_void_p()
         N.check(L.pccp_gpu_open(C.byref(self.cfg), C.byref(h)))
         self._h = h

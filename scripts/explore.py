@@ -35,7 +35,8 @@ def main():
                 r = eng.enumerate()
                 dt = time.time() - t
             print(w, json.dumps(info))
-            print(w, json.dumps(r), f"wall {dt:.4f}s nodes/s {r['nodes'] / dt:.3e} evals/s {r['evals'] / dt:.3e}")
+            print(w, f"nodes={r['nodes']} sols={r['solutions']} kernel={r['kernel_ms']:.2f}ms dec={r['decompose_ms']:.2f}ms "
+                     f"levels={r['bfs_levels']} don={r['donations']} rounds={r['rounds']} wall={dt:.4f}s nodes/s={r['nodes'] / dt:.3e}")
         elif w.startswith("csp"):
             d = int(w[3:]) if len(w) > 3 else 22
             m = Model.random_csp(1)
@@ -63,7 +64,7 @@ def main():
                 print(f"{w} seed={s} {r.status} obj={r.objective} valid={ok} nodes={st['nodes']} rounds={st['rounds']} "
                       f"wall={dt:.3f}s kernel={st['kernel_ms']:.1f}ms t_best={last} nodes/s={st['nodes'] / dt:.3e} "
                       f"evals/s={st['evals'] / dt:.3e} sub={st['subproblems']} cta={info['group_threads']}"
-                      f" smem_table={info['table_in_smem']}")
+                      f" smem_table={info['table_in_smem']} levels={st['bfs_levels']} dec={st['decompose_ms']:.1f}ms don={st['donations']}")
         sys.stdout.flush()
 
 

@@ -46,7 +46,7 @@ def lower(m):
     L.pccp_lower_only.argtypes = [C.POINTER(N.PccpModel), C.POINTER(N.PccpLoweringInfo), C.c_void_p]
     s, keep = m.tables().as_struct()
     info = N.PccpLoweringInfo()
-    sc = np.zeros(5, np.uint32)
+    sc = np.zeros(6, np.uint32)
     N.check(L.pccp_lower_only(C.byref(s), C.byref(info), sc.ctypes.data_as(C.c_void_p)))
     return info, sc
 
@@ -59,7 +59,8 @@ def test_lowering_shapes():
     info, sc = lower(Model.random_csp(1))
     assert info.n_rows == 690 and info.n_generic == 0
     info, sc = lower(Model.rcpsp_random(1, 30, 4))
-    assert info.n_rows == 128 and info.n_generic == 0 and sc[1] > 0
+    # 930 overlap reifications fuse (11 commands each); precedences are unit records
+    assert info.n_rows == 128 and info.n_generic == 0 and sc[5] == 930 and sc[1] == 0 and sc[0] == 80
     assert abs(lower(Model.nqueens(8))[0].alg_bytes_per_eval - 15.8139) < 1e-3  # Q8 15.8 B
 
 
