@@ -1,0 +1,75 @@
+"""The multi-GPU paths, exercised on one B200 (the only device these boxes
+expose): every shard of the EPS frontier (i mod N) runs as its own context —
+in turn in one process for enumeration, and as two processes sharing the
+incumbent through CUDA IPC + system-scope atomicMin for minimisation.  The
+combined results must equal the single-GPU ones."""
+import os
+import socket
+
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+GOLD_Q10 = dict(nodes=12459, failures=5506, solutions=724, hash_sum=0x1C9C31621038E7A1)
+
+
+@pytest.mark.parametrize("n_shards", [2, 3, 8])
+def test_enumeration_shards_sum_to_the_whole(n_shards, golden):
+    from paper_2207_12116_b200 import Engine, Model
+    from paper_2207_12116_b200.distributed import combine_enum
+    for name, depth in (("nqueens10", -1), ("csp1", 12)):
+        m = Model.nqueens(10) if name == "nqueens10" else Model.random_csp(1)
+        g = golden[name]["enumerate" if depth < 0 else "enumerate_d12"]
+        parts = []
+        for k in range(n_shards):
+            with Engine(0, shard_index=k, shard_count=n_shards, hash=True, eps_factor=2) as e:
+                parts.append(e.load(m).enumerate(depth_cap=depth))
+        tot = combine_enum(parts)
+        for key in ("nodes", "failures", "solutions", "open_leaves", "hash_sum"):
+            assert tot[key] == g[key], (name, n_shards, key)
+        assert tot["exhausted"]
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def _solve_rank(rank, world, port, seed, q):
+    import torch.distributed as dist
+
+    from paper_2207_12116_b200 import Engine, Model
+    from paper_2207_12116_b200.distributed import attach_incumbents, run_solve
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        m = Model.rcpsp_random(seed, 30, 4)
+        e = Engine(0, shard_index=rank, shard_count=world)
+        e.load(m)
+        attach_incumbents(e)
+        dist.barrier()
+        res = run_solve(e, timeout_s=120, check=m.check_solution)
+        q.put((rank, res["status"], res["objective"], res.get("checked"), res["nodes"]))
+        e.close()
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("seed,optimum", [(1, 84), (7, 60)])
+def test_two_process_solve_with_ipc_incumbent(seed, optimum):
+    import torch.multiprocessing as mp
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_solve_rank, args=(r, 2, port, seed, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    out = sorted(q.get(timeout=300) for _ in procs)
+    for p in procs:
+        p.join(timeout=120)
+        assert p.exitcode == 0
+    for rank, status, obj, checked, nodes in out:
+        assert status == "OPTIMAL" and obj == optimum and checked
