@@ -159,6 +159,71 @@ def cpu_reference(w, budget_s, threads):
                 sample=f"first {r['nodes']} nodes of the {w['workload']} DFS on the C oracle port (1 thread)")
 
 
+TTO_SEEDS = (1, 2, 5, 7, 9, 11)  # SURVEY 8(d) config 4 parity seeds
+TTO_OPTIMA = {1: 84, 2: 77, 5: 73, 7: 60, 9: 61, 11: 99}
+TTO_CPU_W1_S = {1: 0.23, 2: 6.4, 5: 0.34, 7: 28.2, 9: 40.9, 11: 3.2}  # reference W=1, survey
+
+
+def time_to_optimum(local, rank, world, dist):
+    """Config 4 (RCPSP 30x4): optimum, time to the first optimal incumbent and
+    time to the proof on the GPU(s).  With N > 1 the incumbent is shared
+    through CUDA IPC + system-scope atomicMin (paper_2207_12116_b200/distributed.py)."""
+    from paper_2207_12116_b200 import Engine, Model
+    from paper_2207_12116_b200.distributed import attach_incumbents, run_solve
+    eng = Engine(local, shard_index=rank, shard_count=world)
+    attached = False
+    out = {}
+    for seed in TTO_SEEDS:
+        m = Model.rcpsp_random(seed, 30, 4)
+        eng.load(m)
+        if world > 1 and not attached:
+            attach_incumbents(eng)
+            attached = True
+        if world > 1:
+            dist.barrier()
+            res = run_solve(eng, timeout_s=120, check=m.check_solution)
+            status, obj, ok = res["status"], res["objective"], res.get("checked")
+            local_r = res["local"]
+        else:
+            r = eng.solve(timeout_s=120)
+            status, obj = r.status, r.objective
+            ok = r.best_words is not None and m.check_solution(r.best_words)
+            local_r = r
+        t_first = min((ms for v, ms in local_r.improvements if v == obj), default=float("inf"))
+        t_proof = local_r.stats["device_ms"]
+        if world > 1:
+            t_first = min(x for x in _gather_obj(dist, t_first))
+            t_proof = max(_gather_obj(dist, t_proof))
+        out[str(seed)] = {"status": status, "objective": obj, "valid": bool(ok),
+                          "matches_reference": obj == TTO_OPTIMA[seed], "t_first_optimal_ms": t_first,
+                          "t_proof_ms": t_proof, "nodes": local_r.stats["nodes"],
+                          "cpu_reference_w1_s": TTO_CPU_W1_S[seed]}
+    eng.close()
+    return {"config": "rcpsp 30 tasks x 4 resources, random_patterson(mt19937_64(seed)), minimise makespan",
+            "note": "node counts differ from the CPU only through search order and incumbent timing",
+            "gpu": out}
+
+
+def _gather_obj(dist, v):
+    out = [None] * dist.get_world_size()
+    dist.all_gather_object(out, v)
+    return out
+
+
+def cpu_time_to_optimum(threads):
+    """The reference solve_parallel (oracle/_ref) with W = host threads on the
+    quick parity seeds (solver.cpp:229-283, EngineConfig Seq, eps_factor 8)."""
+    from oracle import refh
+    if not refh.available():
+        return None
+    out = {}
+    for seed in (1, 5, 11):
+        r = refh.RefModel.rcpsp(seed, 30, 4).solve_parallel(workers=threads, timeout_s=60)
+        out[str(seed)] = {"status": ["OPTIMAL", "SAT", "UNSAT", "UNKNOWN"][r["status"]], "objective": r["objective"],
+                          "t_proof_ms": r["elapsed_ms"], "nodes": r["nodes"], "workers": threads}
+    return out
+
+
 def run_reference_arm(a, w):
     rank = env_int("RANK", 0)
     if rank != 0:
@@ -204,6 +269,7 @@ def main():
     ap.add_argument("--cpu-budget", type=float, default=15.0)
     ap.add_argument("--ref-budget", type=float, default=10.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-tto", action="store_true", help="skip the RCPSP30 time-to-optimum section")
     a = ap.parse_args()
     w = WORKLOADS[a.config]
     if a.impl == "reference":
@@ -304,6 +370,8 @@ def main():
         parity["hash_sum"] = hs == exp["hash_sum"]
         heng.close()
 
+    tto = None if a.no_tto else time_to_optimum(local, rank, world, dist)
+
     if rank != 0:
         if world > 1:
             dist.destroy_process_group()
@@ -347,6 +415,10 @@ def main():
         cb = cpu_reference(w, a.cpu_budget, os.cpu_count() or 1)
         line["cpu_baseline"] = {"value": cb["value"], "unit": "nodes/s", "cores": cb["cores"], "kind": cb["kind"],
                                 "sample": cb["sample"]}
+    if tto is not None:
+        if world == 1 and not a.no_cpu_baseline:
+            tto["cpu_reference"] = cpu_time_to_optimum(os.cpu_count() or 1)
+        line["time_to_optimum"] = tto
     print(json.dumps(line))
     if world > 1:
         dist.destroy_process_group()

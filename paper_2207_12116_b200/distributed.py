@@ -96,4 +96,5 @@ def run_solve(engine, timeout_s: float = 0.0, root=None, group=None,
     res["best_words"] = None if best is None else np.asarray(best, np.int32)
     if check is not None and res["best_words"] is not None:
         res["checked"] = bool(check(res["best_words"]))
+    res["local"] = r  # this rank's SolveResult (improvement log, device timings)
     return res
