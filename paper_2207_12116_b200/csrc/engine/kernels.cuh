@@ -447,8 +447,13 @@ __device__ __forceinline__ bool eval_small(volatile int* S, const int* __restric
 // `coef + lsum - coef*lb(x) > c` with lsum taken from the same reduction.
 // The second read of lb(x) can only be newer than the one summed, which
 // makes the guard weaker, never unsound; at the quiet round both reads agree.
-template <class G>
-__device__ bool eval_rows(const G& g, volatile int* S, const int* __restrict__ T, const DeviceLayout& L) {
+// Lane mapping: consecutive rows (RCPSP: consecutive tasks j of one resource,
+// whose rows share their term list) go to consecutive sub-warps, so one load
+// instruction touches b_{i,j} for a few i and many consecutive j — stride-2
+// words, ~2-way bank conflicts — instead of one column b_{.,j} (n words
+// apart: a single bank when n = 32).
+template <class G, bool TS>
+__device__ bool eval_rows(const G& g, unsigned sb, const Tab<TS>& tab, const DeviceLayout& L) {
   const int R = (int)L.row_lanes;
   const int sub = g.rank() & (R - 1);
   const int per_pass = g.size() / R;
@@ -460,27 +465,28 @@ __device__ bool eval_rows(const G& g, volatile int* S, const int* __restrict__ T
     long long s = 0;
     int beg = 0, end = 0;
     if (act) {
-      beg = T[L.row_off + row];
-      end = T[L.row_off + row + 1];
+      beg = tab.ld1(L.row_off, row);
+      end = tab.ld1(L.row_off, row + 1);
       for (int j = beg + sub; j < end; j += R) {
-        const int x = T[L.row_terms + j];
-        s += tv(tcoef(x), S[tword(x)]);
+        const int x = tab.ld1(L.row_terms, j);
+        s += tv(tcoef(x), sld(sb + ((unsigned)tword(x) << 2)));
       }
     }
     for (int o = R >> 1; o > 0; o >>= 1) s += __shfl_xor_sync(kFull, s, o, R);
     if (act) {
-      const int c = T[L.row_c + row];
+      const int c = tab.ld1(L.row_c, row);
       const int lsum = narrow(s);
       const int cell = lsum > c ? INT_MAX : lsum;  // [lsum > c] => lsum <- +inf
-      if (sub == 0) ch |= join_max(S, T[L.row_lsum + row], cell);
+      if (sub == 0) ch |= sjoin_max(sb + ((unsigned)tab.ld1(L.row_lsum, row) << 2), cell);
       if (c != INT_MAX) {
         const long long wl = tv(1, cell);
         for (int j = beg + sub; j < end; j += R) {
-          const int x = T[L.row_terms + j];
-          const int coef = tcoef(x), w = tword(x);
-          if ((long long)coef + wl + tv(-coef, S[w]) > (long long)c) {
-            ch |= join_max(S, w, 0);
-            ch |= join_min(S, w + 1, 0);
+          const int x = tab.ld1(L.row_terms, j);
+          const int coef = tcoef(x);
+          const unsigned a = sb + ((unsigned)tword(x) << 2);
+          if ((long long)coef + wl + tv(-coef, sld(a)) > (long long)c) {
+            ch |= sjoin_max(a, 0);
+            ch |= sjoin_min(a + 4, 0);
           }
         }
       }
@@ -605,7 +611,7 @@ __device__ bool propagate(const G& g, volatile int* S, unsigned sb, const Tab<TS
       }
     }
     for (int i = g.rank(); i < (int)L.n_small; i += g.size()) ch |= eval_small(S, T, L, i);
-    if (L.n_rows) ch |= eval_rows(g, S, T, L);
+    if (L.n_rows) ch |= eval_rows(g, sb, tab, L);
     for (int i = g.rank(); i < (int)L.n_gen; i += g.size())
       ch |= eval_generic(S, T + L.gen_code + T[L.gen_off + i]);
     for (int i = g.rank(); i < (int)L.n_iv; i += g.size()) {

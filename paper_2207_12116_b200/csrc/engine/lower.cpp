@@ -523,6 +523,15 @@ Lowered lower_model(const pccp_model& m) {
     B[L.ne + 4 * i + 2] = nes[i].b;
     B[L.ne + 4 * i + 3] = 0;
   }
+  // Order the reifications x-major: a warp then reads one x (broadcast) and
+  // consecutive y / b words (2-way bank conflicts).  RCPSP compiles them
+  // j-major (rcpsp.cpp:241-242), which puts b_ij of a warp n words apart —
+  // the same bank for every lane when n = 32.
+  std::stable_sort(reifs.begin(), reifs.end(), [](const Reif& a, const Reif& b) {
+    const std::uint32_t ax = static_cast<std::uint32_t>(a.xy) & 0xffffu, bx = static_cast<std::uint32_t>(b.xy) & 0xffffu;
+    if (ax != bx) return ax < bx;
+    return (static_cast<std::uint32_t>(a.xy) >> 16) < (static_cast<std::uint32_t>(b.xy) >> 16);
+  });
   L.n_reif = static_cast<std::uint32_t>(reifs.size());
   L.reif = reserve_arr(4 * L.n_reif);
   for (std::uint32_t i = 0; i < L.n_reif; ++i) {
@@ -626,8 +635,14 @@ Lowered lower_model(const pccp_model& m) {
     max_terms = std::max<std::uint32_t>(max_terms, static_cast<std::uint32_t>(r.terms.size()));
   }
   L.n_row_terms = n_terms;
+  // ~8 terms per lane: few lanes per row keeps a warp's loads on many rows of
+  // consecutive words (kernels.cuh eval_rows) at a modest serial cost.
   L.row_lanes = 1;
-  while (L.row_lanes < 32 && L.row_lanes < max_terms) L.row_lanes <<= 1;
+  while (L.row_lanes < 32 && L.row_lanes * 8 < max_terms) L.row_lanes <<= 1;
+  if (const char* rl = std::getenv("PCCP_ROW_LANES")) {
+    const unsigned v = static_cast<unsigned>(std::atoi(rl));
+    if (v >= 1 && v <= 32 && (v & (v - 1)) == 0) L.row_lanes = v;
+  }
   L.row_off = reserve_arr(L.n_rows + 1);
   L.row_lsum = reserve_arr(L.n_rows);
   L.row_c = reserve_arr(L.n_rows);
