@@ -1,0 +1,22 @@
+"""A CI-sized workload for compute-sanitizer (memcheck / synccheck / racecheck):
+Q8 enumeration (warp groups), CSP depth 10 (CTA groups, rows), an RCPSP10
+solve (fused reifications, incumbent, donations) and a propagate batch."""
+import os
+import sys
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+
+from paper_2207_12116_b200 import Engine, Model  # noqa: E402
+
+with Engine(0, hash=True, eps_factor=1) as e:
+    r = e.load(Model.nqueens(8)).enumerate()
+    assert (r["nodes"], r["solutions"], r["hash_sum"]) == (779, 92, 0xF1DF80A1FF36FBF6), r
+    r = e.load(Model.random_csp(2, n_vars=60, n_cons=200)).enumerate(depth_cap=8)
+    print("csp", r["nodes"], r["open_leaves"])
+with Engine(0, eps_factor=1) as e:
+    m = Model.rcpsp_random(1, 10, 2)
+    s = e.load(m).solve()
+    assert s.status == "OPTIMAL" and m.check_solution(s.best_words), s.status
+    out, failed, _ = e.propagate_batch([m.bottom()] * 4)
+    print("rcpsp10", s.objective, s.stats["nodes"], failed.tolist())
+print("sanitize workload ok")
