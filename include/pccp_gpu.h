@@ -112,6 +112,16 @@ typedef struct pccp_gpu_cfg {
                             1 right first; 2 mixed (odd groups right first); -1 = 0.
                             The explored tree is the same,
                             so counts, optima and proofs are unchanged; only node order differs. */
+  int32_t var_order;     /* variable selection: 0 = branch() (solver.cpp:19-47), the narrowest
+                            candidate; 1 = smallest lower bound (ties: candidate order).  Not in
+                            the reference (BranchStrategy, solver.hpp:89-91, has candidates only):
+                            a different tree, so node counts differ; optima and UNSAT do not. */
+  int32_t primal_ms;     /* pccp_gpu_solve only, > 0: a primal phase of at most this many ms with
+                            var_order 1 runs first, restarted from the root under obj <= best-1
+                            whenever it improved and then stalled (env PCCP_PRIMAL_STALL_MS,
+                            default max(100, primal_ms/20)); its incumbent (and, if one segment
+                            exhausts its tree, its proof) carries into the exact phase, which
+                            searches the cfg's var_order tree under obj <= best-1.  0 = off. */
 } pccp_gpu_cfg;
 
 typedef struct pccp_limits {
@@ -157,6 +167,11 @@ typedef struct pccp_solve_result {
   int32_t n_improvements;      /* incumbent log length (<= 64 kept) */
   int32_t improvements[64];    /* objective values, in improvement order */
   double improvement_ms[64];   /* device time since search start */
+  int32_t phases;              /* 1, or 2 with a primal phase (cfg.primal_ms) */
+  int32_t primal_proved;       /* the primal phase exhausted its tree: its result is the proof */
+  uint64_t primal_nodes;       /* nodes of the primal phase (included in stats.nodes) */
+  double primal_device_ms;     /* device time of the primal phase */
+  int32_t primal_restarts;     /* primal segments restarted from the root under a better bound */
 } pccp_solve_result;
 
 typedef struct pccp_gpu_ctx pccp_gpu_ctx;

@@ -49,6 +49,8 @@ class PccpGpuCfg(C.Structure):
         ("hash", C.c_int32),
         ("verbose", C.c_int32),
         ("value_order", C.c_int32),
+        ("var_order", C.c_int32),
+        ("primal_ms", C.c_int32),
     ]
 
 
@@ -93,6 +95,11 @@ class PccpSolveResult(C.Structure):
         ("n_improvements", C.c_int32),
         ("improvements", C.c_int32 * 64),
         ("improvement_ms", C.c_double * 64),
+        ("phases", C.c_int32),
+        ("primal_proved", C.c_int32),
+        ("primal_nodes", C.c_uint64),
+        ("primal_device_ms", C.c_double),
+        ("primal_restarts", C.c_int32),
     ]
 
 

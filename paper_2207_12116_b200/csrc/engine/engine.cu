@@ -123,9 +123,11 @@ struct pccp_gpu_ctx {
 
   int groups() const { return ctas * (warp ? gpc : 1); }
 
-  dev::Model model() const {
+  dev::Model model(int var_order = 0, unsigned var_seed = 0) const {
     dev::Model M;
     M.L = low.L;
+    M.L.var_order = (std::uint32_t)var_order;
+    M.L.var_seed = var_seed;
     M.blob = blob.p;
     M.table_in_smem = table_in_smem;
     M.store_stride = store_stride;
@@ -198,14 +200,27 @@ void plan(pccp_gpu_ctx* c) {
   c->ctas = c->n_sm * occ;
 }
 
-void reset_globals(pccp_gpu_ctx* c, const pccp_limits* lim) {
+// keep_incumbent: leave the incumbent cell, the best-store lock and
+// best_value as they are (the exact phase after a primal phase; peers may be
+// pushing into the cell meanwhile, so it is not rewritten from the host).
+void reset_globals(pccp_gpu_ctx* c, const pccp_limits* lim, bool keep_incumbent = false,
+                   unsigned long long stall_ns = 0) {
   dev::Globals h;
   std::memset(&h, 0, sizeof(h));
+  h.stall_ns = stall_ns;
   h.incumbent = INT32_MAX;
   h.best_value = INT32_MAX;
   h.node_limit = lim ? lim->node_limit : ~0ull;
   h.timeout_ns = (lim && lim->timeout_s > 0) ? (unsigned long long)(lim->timeout_s * 1e9) : 0ull;
-  CK(cudaMemcpyAsync(c->G, &h, sizeof(h), cudaMemcpyHostToDevice, c->stream));
+  if (keep_incumbent) {
+    constexpr size_t a = offsetof(dev::Globals, incumbent), b = offsetof(dev::Globals, n_impr);
+    const char* hp = reinterpret_cast<const char*>(&h);
+    char* dp = reinterpret_cast<char*>(c->G);
+    CK(cudaMemcpyAsync(dp, hp, a, cudaMemcpyHostToDevice, c->stream));
+    CK(cudaMemcpyAsync(dp + b, hp + b, sizeof(h) - b, cudaMemcpyHostToDevice, c->stream));
+  } else {
+    CK(cudaMemcpyAsync(c->G, &h, sizeof(h), cudaMemcpyHostToDevice, c->stream));
+  }
   dev::k_init_clock<<<1, 1, 0, c->stream>>>(c->G);
   CK(cudaGetLastError());
   ++c->launches;
@@ -238,7 +253,8 @@ struct RunOut {
 
 template <class Gp, bool TS>
 void run_search(pccp_gpu_ctx* c, int mode, const int32_t* root_words, int depth_cap, const pccp_limits* lim,
-                RunOut& out) {
+                RunOut& out, int var_order = 0, bool keep_incumbent = false, unsigned long long stall_ns = 0,
+                unsigned var_seed = 0) {
   const double t_start = now_ms();
   const std::uint64_t launches0 = c->launches;
   const DeviceLayout& L = c->low.L;
@@ -247,7 +263,7 @@ void run_search(pccp_gpu_ctx* c, int mode, const int32_t* root_words, int depth_
   const int shard_count = std::max(1, c->cfg.shard_count);
   const int shard_index = c->cfg.shard_index;
   if (shard_index < 0 || shard_index >= shard_count) throw ArgError("shard_index out of range");
-  const dev::Model M = c->model();
+  const dev::Model M = c->model(var_order, var_seed);
   dev::SearchCtl C{};
   C.G = c->G;
   C.n_peers = mode == 1 ? c->n_peers : 0;
@@ -259,7 +275,7 @@ void run_search(pccp_gpu_ctx* c, int mode, const int32_t* root_words, int depth_
   c->best.ensure((size_t)std::max(nw, 1));
   C.best_store = c->best.p;
 
-  reset_globals(c, lim);
+  reset_globals(c, lim, keep_incumbent, stall_ns);
   c->fa.ensure((size_t)stride);
   c->ia.ensure(1);
   c->flags.ensure(2);
@@ -396,6 +412,39 @@ void fill_stats(const pccp_gpu_ctx* c, const RunOut& r, pccp_stats& s) {
   s.device_ms = r.device_ms;
   s.bfs_levels = r.levels;
   s.donations = r.g.donations;
+}
+
+// Counters of consecutive searches of one call (primal segments, exact
+// phase); the final search's control state (incumbent, stop) wins.
+void merge_run(RunOut& acc, const RunOut& r, bool first) {
+  if (first) {
+    acc = r;
+    return;
+  }
+  dev::Globals g = r.g;
+  g.nodes += acc.g.nodes;
+  g.failures += acc.g.failures;
+  g.solutions += acc.g.solutions;
+  g.rounds += acc.g.rounds;
+  g.max_depth = std::max(g.max_depth, acc.g.max_depth);
+  g.donations += acc.g.donations;
+  acc.g = g;
+  acc.bfs_rounds += r.bfs_rounds;
+  acc.decompose_ms += r.decompose_ms;
+  acc.kernel_ms += r.kernel_ms;
+  acc.device_ms += r.device_ms;
+  acc.elapsed_ms += r.elapsed_ms;
+  acc.launches += r.launches;
+  acc.h2d += r.h2d;
+  acc.d2h += r.d2h;
+  acc.subproblems += r.subproblems;
+  acc.levels += r.levels;
+}
+
+// The device keeps the last 64 improvements in a ring (record_solution).
+void append_log(const dev::Globals& g, double offset_ms, std::vector<std::pair<int, double>>& log) {
+  const int n = g.n_impr, first = std::max(0, n - 64);
+  for (int k = first; k < n; ++k) log.emplace_back(g.impr_val[k & 63], offset_ms + (double)g.impr_ns[k & 63] * 1e-6);
 }
 
 void check_loaded(const pccp_gpu_ctx* c) {
@@ -631,18 +680,78 @@ int pccp_gpu_solve(pccp_gpu_ctx* c, const int32_t* root, const pccp_limits* lim,
       out->status = PCCP_UNKNOWN;
       return PCCP_OK;
     }
+    const int var_order = std::clamp(c->cfg.var_order, 0, 3);
+    const char* pv = std::getenv("PCCP_PRIMAL_VAR_ORDER");
+    const int primal_order = pv ? std::clamp(std::atoi(pv), 1, 3) : 2;
+    std::vector<std::pair<int, double>> log;  // improvement log over all phases
     RunOut r;
-    dispatch(c, [&]<class Gp, bool TS>() { run_search<Gp, TS>(c, 1, root, -1, lim, r); });
+    out->phases = 1;
+    const double t_call = now_ms();
+    auto left = [&](pccp_limits& l, const RunOut& acc) {  // the caller's limits minus what was used
+      l = lim ? *lim : pccp_limits{0.0, ~0ull};
+      if (l.timeout_s > 0) l.timeout_s -= (now_ms() - t_call) * 1e-3;
+      if (l.node_limit != ~0ull) l.node_limit = l.node_limit > acc.g.nodes ? l.node_limit - acc.g.nodes : 0;
+      return !(lim && lim->timeout_s > 0 && l.timeout_s <= 0) && l.node_limit > 0;
+    };
+    bool proved = false;
+    if (c->cfg.primal_ms > 0) {
+      // Primal phase: smallest-lb dives (complete searches of another tree),
+      // restarted from the root under obj <= best-1 whenever a segment stalls
+      // (no improvement for stall_ms) after improving; bounded by primal_ms
+      // and the caller's limits.
+      const double budget_ms = c->cfg.primal_ms;
+      const char* se = std::getenv("PCCP_PRIMAL_STALL_MS");
+      const double stall_ms = se ? std::atof(se) : std::max(100.0, 0.05 * budget_ms);
+      RunOut acc;
+      for (int seg = 0;; ++seg) {
+        pccp_limits l1;
+        if (!left(l1, acc)) break;
+        const double spent = now_ms() - t_call;
+        if (spent >= budget_ms) break;
+        const double p_s = (budget_ms - spent) * 1e-3;
+        l1.timeout_s = l1.timeout_s > 0 ? std::min(l1.timeout_s, p_s) : p_s;
+        RunOut r1;
+        dispatch(c, [&]<class Gp, bool TS>() {
+          run_search<Gp, TS>(c, 1, root, -1, &l1, r1, primal_order, seg > 0, (unsigned long long)(stall_ms * 1e6),
+                             (unsigned)seg);
+        });
+        append_log(r1.g, acc.device_ms, log);
+        merge_run(acc, r1, seg == 0);
+        if (r1.g.incomplete == 0) {
+          proved = true;
+          break;
+        }
+        if (r1.g.n_impr == 0 || !r1.g.stalled) break;  // nothing new, or out of time
+        out->primal_restarts = seg + 1;
+      }
+      out->primal_nodes = acc.g.nodes;
+      out->primal_device_ms = acc.device_ms;
+      out->primal_proved = proved ? 1 : 0;
+      r = acc;
+    }
+    pccp_limits l2;
+    if (c->cfg.primal_ms <= 0) {
+      dispatch(c, [&]<class Gp, bool TS>() { run_search<Gp, TS>(c, 1, root, -1, lim, r, var_order); });
+      append_log(r.g, 0.0, log);
+    } else if (!proved && left(l2, r)) {
+      RunOut r2;
+      dispatch(c, [&]<class Gp, bool TS>() { run_search<Gp, TS>(c, 1, root, -1, &l2, r2, var_order, true); });
+      append_log(r2.g, r.device_ms, log);
+      merge_run(r, r2, false);
+      out->phases = 2;
+    }
     fill_stats(c, r, out->stats);
     const bool exhausted = r.g.incomplete == 0;
     const bool has = r.g.incumbent != INT32_MAX;
     out->has_objective = has ? 1 : 0;
     out->objective = has ? r.g.incumbent : 0;
     out->status = has ? (exhausted ? PCCP_OPTIMAL : PCCP_SAT) : (exhausted ? PCCP_UNSAT : PCCP_UNKNOWN);
-    out->n_improvements = std::min(r.g.n_impr, 64);
+    // keep the first 32 and the last 32 improvements (the last one is the incumbent)
+    if (log.size() > 64) log.erase(log.begin() + 32, log.end() - 32);
+    out->n_improvements = (int32_t)log.size();
     for (int k = 0; k < out->n_improvements; ++k) {
-      out->improvements[k] = r.g.impr_val[k];
-      out->improvement_ms[k] = (double)r.g.impr_ns[k] * 1e-6;
+      out->improvements[k] = log[k].first;
+      out->improvement_ms[k] = log[k].second;
     }
     if (best_words && has && r.g.best_value == r.g.incumbent)
       CK(cudaMemcpy(best_words, c->best.p, (size_t)c->low.L.n_words * 4, cudaMemcpyDeviceToHost));

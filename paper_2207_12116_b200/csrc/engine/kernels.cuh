@@ -56,6 +56,11 @@ struct Globals {
   int active;                   // groups exploring, or promised a donation
   unsigned wait_head, wait_tail;
   unsigned long long donations;
+  // primal restarts (engine.cu pccp_gpu_solve): stop once an incumbent exists
+  // and none improved it for stall_ns; `stalled` says the stop was this one
+  unsigned long long stall_ns;     // 0: off
+  unsigned long long last_impr_ns; // since t0
+  int stalled;
 };
 
 __device__ __forceinline__ unsigned long long globaltimer() {
@@ -114,6 +119,7 @@ struct WarpGroup {
     return v;
   }
   __device__ __forceinline__ int bcast0(int v) const { return __shfl_sync(kFull, v, 0); }
+  __device__ __forceinline__ unsigned uid() const { return blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); }
 };
 
 struct CtaGroup {
@@ -124,6 +130,7 @@ struct CtaGroup {
   __device__ __forceinline__ int size() const { return n; }
   __device__ __forceinline__ int warp() const { return tid >> 5; }
   __device__ __forceinline__ int warps() const { return n >> 5; }
+  __device__ __forceinline__ unsigned uid() const { return blockIdx.x; }
   __device__ __forceinline__ void sync() const { __syncthreads(); }
   __device__ __forceinline__ void round_begin() const {
     if (tid < 3) ring[tid] = 0;
@@ -632,17 +639,55 @@ __device__ bool propagate(const G& g, volatile int* S, unsigned sb, const Tab<TS
 // branch (solver.cpp:19-47): narrowest candidate with lo < hi, first in
 // candidate order on ties (key = width << 24 | position), mid = floor((lo+hi)/2).
 // Returns 0: none (a solution), 1: decision, -1: unbounded (ModelError).
+// L.var_order > 0 selects by smallest lb instead (the primal-dive extension,
+// not in the reference); ties go to candidate order (1), the smallest ub
+// (2: latest start first, the LST rule of schedule generation), or a
+// pseudo-random priority per group and per L.var_seed (3).  The split, mid
+// and the unbounded check are the reference's in every order.
+__device__ __forceinline__ unsigned mix24(unsigned x) {
+  x ^= x >> 16;
+  x *= 0x7feb352du;
+  x ^= x >> 15;
+  x *= 0x846ca68bu;
+  x ^= x >> 16;
+  return x & 0xffffffu;
+}
 template <class G>
 __device__ int branch(const G& g, volatile int* S, const int* __restrict__ T, const DeviceLayout& L, int& lbw,
                       int& mid) {
   unsigned long long best = ~0ull;
-  for (int i = g.rank(); i < (int)L.n_cand; i += g.size()) {
-    const int w = T[L.cand_lbw + i];
-    const int lo = S[w], hi = S[w + 1];
-    if (lo < hi) {
-      const unsigned long long width = (unsigned long long)((long long)hi - (long long)lo + 1);
-      const unsigned long long key = (width << 24) | (unsigned long long)i;
-      best = key < best ? key : best;
+  const unsigned vo = L.var_order;
+  if (vo <= 1) {
+    for (int i = g.rank(); i < (int)L.n_cand; i += g.size()) {
+      const int w = T[L.cand_lbw + i];
+      const int lo = S[w], hi = S[w + 1];
+      if (lo < hi) {
+        const unsigned long long width = (unsigned long long)((long long)hi - (long long)lo + 1);
+        const unsigned long long k = vo ? (unsigned long long)((unsigned)lo ^ 0x80000000u) : width;
+        const unsigned long long key = (k << 24) | (unsigned long long)i;
+        best = key < best ? key : best;
+      }
+    }
+  } else {
+    unsigned long long m = ~0ull;
+    for (int i = g.rank(); i < (int)L.n_cand; i += g.size()) {
+      const int w = T[L.cand_lbw + i];
+      const int lo = S[w], hi = S[w + 1];
+      const unsigned long long k = (unsigned)lo ^ 0x80000000u;
+      if (lo < hi && k < m) m = k;
+    }
+    m = g.min_u64(m);
+    if (m == ~0ull) return 0;
+    const unsigned salt = mix24(L.var_seed * 0x9e3779b9u + g.uid()) << 8;
+    for (int i = g.rank(); i < (int)L.n_cand; i += g.size()) {
+      const int w = T[L.cand_lbw + i];
+      const int lo = S[w], hi = S[w + 1];
+      if (lo < hi && ((unsigned)lo ^ 0x80000000u) == m) {
+        const unsigned long long k =
+            vo == 2 ? (unsigned long long)((unsigned)hi ^ 0x80000000u) : (unsigned long long)mix24(salt ^ (unsigned)i);
+        const unsigned long long key = (k << 24) | (unsigned long long)i;
+        best = key < best ? key : best;
+      }
     }
   }
   best = g.min_u64(best);

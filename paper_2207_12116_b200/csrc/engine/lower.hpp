@@ -67,6 +67,8 @@ struct DeviceLayout {
   std::uint32_t n_ref_cmds;
   std::uint32_t blob_words;
   std::uint32_t hot_words;  // prefix of the blob read every round (small + rows)
+  std::uint32_t var_order;  // set per launch: 0 first-fail (branch, solver.cpp:19-47), 1-3 smallest lb
+  std::uint32_t var_seed;   // set per launch: var_order 3 tie-break seed
 };
 
 struct Lowered {

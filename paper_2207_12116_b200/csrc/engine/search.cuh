@@ -67,6 +67,12 @@ __device__ __forceinline__ bool should_stop(const G& g, const SearchCtl& C) {
       atomicCAS(&Gl->stop, 0, 1);
       stop = 1;
     }
+    if (!stop && Gl->stall_ns && *(volatile int*)&Gl->incumbent != INT_MAX &&
+        globaltimer() - Gl->t0 - *(volatile unsigned long long*)&Gl->last_impr_ns >= Gl->stall_ns) {
+      Gl->stalled = 1;
+      atomicCAS(&Gl->stop, 0, 1);
+      stop = 1;
+    }
     if (!stop && Gl->node_limit != ~0ull) {
       // one reservation per materialisation; the limit admits exactly node_limit nodes
       if (atomicAdd(&Gl->nodes_reserved, 1ull) >= Gl->node_limit) {
@@ -91,11 +97,10 @@ __device__ void record_solution(const G& g, volatile int* S, const DeviceLayout&
     improved = value < old;
     if (improved) {
       for (int p = 0; p < C.n_peers; ++p) atomicMin_system(C.peers[p], value);
-      const int k = atomicAdd(&Gl->n_impr, 1);
-      if (k < 64) {
-        Gl->impr_val[k] = value;
-        Gl->impr_ns[k] = globaltimer() - Gl->t0;
-      }
+      const int k = atomicAdd(&Gl->n_impr, 1) & 63;  // ring: the last 64 improvements
+      Gl->impr_val[k] = value;
+      Gl->impr_ns[k] = globaltimer() - Gl->t0;
+      atomicMax(&Gl->last_impr_ns, Gl->impr_ns[k]);
       while (atomicCAS(&Gl->best_lock, 0, 1) != 0) {
       }
       if (C.count) ++cnt.sols;

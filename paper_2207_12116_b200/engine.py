@@ -34,6 +34,7 @@ class SolveResult:
     best_words: np.ndarray | None
     improvements: list = field(default_factory=list)  # (objective, ms since search start)
     best_on_peer: bool = False
+    primal: dict | None = None  # {nodes, device_ms, proved} when a primal phase ran (cfg primal_ms)
 
 
 def device_count() -> int:
@@ -47,10 +48,10 @@ class Engine:
 
     def __init__(self, device: int = 0, *, group_threads: int = 0, groups_per_cta: int = 0, ctas_per_sm: int = 0,
                  eps_factor: int = 0, shard_index: int = 0, shard_count: int = 1, hash: bool = False,
-                 value_order: int = -1):
+                 value_order: int = -1, var_order: int = 0, primal_ms: int = 0):
         L = N.lib()
         self.cfg = N.PccpGpuCfg(device, group_threads, groups_per_cta, ctas_per_sm, eps_factor, shard_index,
-                                shard_count, int(hash), 0, value_order)
+                                shard_count, int(hash), 0, value_order, var_order, primal_ms)
         h = C.c_void_p()
         N.check(L.pccp_gpu_open(C.byref(self.cfg), C.byref(h)))
         self._h = h
@@ -136,8 +137,13 @@ class Engine:
         N.check(N.lib().pccp_gpu_solve(self._h, _vp(self._root(root)), C.byref(lim), C.byref(res), _vp(best)))
         imp = [(res.improvements[k], res.improvement_ms[k]) for k in range(res.n_improvements)]
         has = res.has_objective
+        primal = None
+        if self.cfg.primal_ms > 0:
+            primal = {"nodes": res.primal_nodes, "device_ms": res.primal_device_ms, "proved": bool(res.primal_proved),
+                      "restarts": res.primal_restarts}
         return SolveResult(N.STATUS_NAMES[res.status], res.objective if has else None, _stats(res.stats),
-                           best[: self.tables.n_words] if has == 1 else None, imp, best_on_peer=has == 2)
+                           best[: self.tables.n_words] if has == 1 else None, imp, best_on_peer=has == 2,
+                           primal=primal)
 
     # ---- multi-GPU incumbent sharing
     def incumbent_handle(self) -> bytes:

@@ -23,8 +23,12 @@ def main():
     ap.add_argument("--hash", action="store_true")
     ap.add_argument("--timeout", type=float, default=60)
     ap.add_argument("--reps", type=int, default=2)
+    ap.add_argument("--vo", type=int, default=-1, help="value order")
+    ap.add_argument("--var", type=int, default=0, help="var order (1: smallest lb)")
+    ap.add_argument("--primal", type=int, default=0, help="primal phase ms")
     a = ap.parse_args()
-    eng = Engine(0, group_threads=a.gt, groups_per_cta=a.gpc, ctas_per_sm=a.cps, eps_factor=a.eps, hash=a.hash)
+    eng = Engine(0, group_threads=a.gt, groups_per_cta=a.gpc, ctas_per_sm=a.cps, eps_factor=a.eps, hash=a.hash,
+                 value_order=a.vo, var_order=a.var, primal_ms=a.primal)
     for w in a.what:
         if w.startswith("q"):
             m = Model.nqueens(int(w[1:]))
@@ -64,7 +68,8 @@ def main():
                 print(f"{w} seed={s} {r.status} obj={r.objective} valid={ok} nodes={st['nodes']} rounds={st['rounds']} "
                       f"wall={dt:.3f}s kernel={st['kernel_ms']:.1f}ms t_best={last} nodes/s={st['nodes'] / dt:.3e} "
                       f"evals/s={st['evals'] / dt:.3e} sub={st['subproblems']} cta={info['group_threads']}"
-                      f" smem_table={info['table_in_smem']} levels={st['bfs_levels']} dec={st['decompose_ms']:.1f}ms don={st['donations']}")
+                      f" smem_table={info['table_in_smem']} levels={st['bfs_levels']} dec={st['decompose_ms']:.1f}ms don={st['donations']}"
+                      f" primal={r.primal} impr={[(v, round(t, 1)) for v, t in r.improvements[:4]]}..{[(v, round(t, 1)) for v, t in r.improvements[-4:]]}")
         sys.stdout.flush()
 
 
