@@ -204,6 +204,77 @@ def time_to_optimum(local, rank, world, dist):
             "gpu": out}
 
 
+STRETCH_SEEDS = (3, 4, 6, 8, 10, 12)  # unproven by the reference at 60 s (1 core) / 120 s (8 cores)
+STRETCH_CPU_BEST = {3: 62, 4: 74, 6: 71, 8: 73, 10: 91, 12: 112}  # best reference incumbents (W=1 60 s, W=8 120 s)
+
+
+def _solve_on_ranks(eng, m, world, dist, timeout_s):
+    from paper_2207_12116_b200.distributed import run_solve
+    if world > 1:
+        dist.barrier()
+        res = run_solve(eng, timeout_s=timeout_s, check=m.check_solution)
+        return res["status"], res["objective"], res.get("checked"), res["local"]
+    r = eng.solve(timeout_s=timeout_s)
+    ok = r.best_words is not None and m.check_solution(r.best_words)
+    return r.status, r.objective, ok, r
+
+
+def stretch_and_large(local, rank, world, dist, timeout_s, large_timeout_s):
+    """Configs 4 (stretch seeds) and 5 (RCPSP 120x4) with the primal phase
+    (smallest-lb dives, LST tie-break, stall restarts; include/pccp_gpu.h
+    primal_ms) ahead of the reference-order exact search."""
+    from paper_2207_12116_b200 import Engine, Model
+    from paper_2207_12116_b200.distributed import attach_incumbents
+    eng = Engine(local, shard_index=rank, shard_count=world, primal_ms=int(timeout_s * 1e3))
+    if world > 1:
+        attach_incumbents(eng)
+    out = {}
+    for seed in STRETCH_SEEDS:
+        m = Model.rcpsp_random(seed, 30, 4)
+        eng.load(m)
+        status, obj, ok, r = _solve_on_ranks(eng, m, world, dist, timeout_s)
+        t_best = min((ms for v, ms in r.improvements if v == obj), default=None)
+        out[str(seed)] = {"status": status, "objective": obj, "valid": bool(ok), "t_best_ms": t_best,
+                          "t_end_ms": r.stats["device_ms"], "nodes": r.stats["nodes"],
+                          "cpu_reference_best": STRETCH_CPU_BEST[seed]}
+    eng.close()
+    stretch = {"config": "rcpsp 30x4 stretch seeds (unproven by the reference CPU solver)",
+               "timeout_s": timeout_s, "gpu": out}
+
+    m = Model.rcpsp_random(1, 120, 4)
+    eng = Engine(local, shard_index=rank, shard_count=world, primal_ms=int(large_timeout_s * 1e3))
+    eng.load(m)
+    if world > 1:
+        attach_incumbents(eng)
+    failed, root, _ = eng.run_sequential()
+    sink = int(m.tables().slot_word[m.starts()[-1]])
+    status, obj, ok, r = _solve_on_ranks(eng, m, world, dist, large_timeout_s)
+    first = r.improvements[0] if r.improvements else (None, None)
+    t_best = min((ms for v, ms in r.improvements if v == obj), default=None)
+    if world > 1:
+        t_best = min(x for x in _gather_obj(dist, t_best if t_best is not None else float("inf")))
+    eng.close()
+    large = {"config": "rcpsp 120x4 seed 1 (random_patterson(mt19937_64(1), 120, 4)), minimise makespan",
+             "timeout_s": large_timeout_s, "status": status, "objective": obj, "valid": bool(ok),
+             "root_lower_bound": int(root[sink]), "first": {"objective": first[0], "t_ms": first[1]},
+             "t_best_ms": t_best, "nodes": r.stats["nodes"], "nodes_per_s": r.stats["nodes"] / (r.stats["device_ms"] / 1e3),
+             "primal": r.primal,
+             "note": "the reference's branching order reaches no leaf (SURVEY 8d); the primal phase's incumbents "
+                     "are ordinary solutions of the same model, checked by check_solution"}
+    return stretch, large
+
+
+def cpu_large(threads, budget_s):
+    """The reference solve_parallel on RCPSP 120x4 seed 1 for a bounded budget."""
+    from oracle import refh
+    if not refh.available():
+        return None
+    r = refh.RefModel.rcpsp(1, 120, 4).solve_parallel(workers=threads, timeout_s=budget_s)
+    return {"status": ["OPTIMAL", "SAT", "UNSAT", "UNKNOWN"][r["status"]], "objective": r["objective"],
+            "t_ms": r["elapsed_ms"], "nodes": r["nodes"], "nodes_per_s": r["nodes"] / max(r["elapsed_ms"], 1) * 1e3,
+            "workers": threads}
+
+
 def _gather_obj(dist, v):
     out = [None] * dist.get_world_size()
     dist.all_gather_object(out, v)
@@ -269,7 +340,9 @@ def main():
     ap.add_argument("--cpu-budget", type=float, default=15.0)
     ap.add_argument("--ref-budget", type=float, default=10.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--no-tto", action="store_true", help="skip the RCPSP30 time-to-optimum section")
+    ap.add_argument("--no-tto", action="store_true", help="skip the RCPSP time-to-optimum sections")
+    ap.add_argument("--stretch-timeout", type=float, default=10.0)
+    ap.add_argument("--large-timeout", type=float, default=10.0)
     a = ap.parse_args()
     w = WORKLOADS[a.config]
     if a.impl == "reference":
@@ -371,6 +444,8 @@ def main():
         heng.close()
 
     tto = None if a.no_tto else time_to_optimum(local, rank, world, dist)
+    stretch, large = (None, None) if a.no_tto else stretch_and_large(local, rank, world, dist, a.stretch_timeout,
+                                                                     a.large_timeout)
 
     if rank != 0:
         if world > 1:
@@ -419,6 +494,11 @@ def main():
         if world == 1 and not a.no_cpu_baseline:
             tto["cpu_reference"] = cpu_time_to_optimum(os.cpu_count() or 1)
         line["time_to_optimum"] = tto
+    if stretch is not None:
+        line["stretch"] = stretch
+        if world == 1 and not a.no_cpu_baseline:
+            large["cpu_reference"] = cpu_large(os.cpu_count() or 1, a.large_timeout)
+        line["rcpsp120"] = large
     print(json.dumps(line))
     if world > 1:
         dist.destroy_process_group()

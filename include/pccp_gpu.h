@@ -223,6 +223,12 @@ int pccp_gpu_incumbent_handle(pccp_gpu_ctx* ctx, uint8_t* out64);
 int pccp_gpu_attach_peers(pccp_gpu_ctx* ctx, const uint8_t* handles64, int32_t n_handles,
                           int32_t self_index);
 
+/* The same for contexts of one process (one host thread per device, e.g. the
+ * pccp_gpu CLI with --gpus N): peer access is enabled between their devices
+ * and each context pushes improvements into every other context's cell.
+ * Contexts on the same device are linked directly. */
+int pccp_gpu_link_peers(pccp_gpu_ctx* const* ctxs, int32_t n);
+
 /* Information about the lowered model (device tables), for roofline accounting. */
 typedef struct pccp_lowering_info {
   uint32_t n_words;

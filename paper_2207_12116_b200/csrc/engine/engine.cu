@@ -797,4 +797,36 @@ int pccp_gpu_attach_peers(pccp_gpu_ctx* c, const uint8_t* handles, int32_t n, in
   });
 }
 
+int pccp_gpu_link_peers(pccp_gpu_ctx* const* ctxs, int32_t n) {
+  return api([&] {
+    if (n < 0 || (n > 0 && !ctxs)) throw ArgError("null argument");
+    for (int i = 0; i < n; ++i)
+      if (!ctxs[i]) throw ArgError("null context");
+    for (int i = 0; i < n; ++i) {
+      pccp_gpu_ctx* c = ctxs[i];
+      CK(cudaSetDevice(c->device));
+      std::vector<int*> ptrs;
+      for (int j = 0; j < n; ++j) {
+        if (j == i) continue;
+        const int dj = ctxs[j]->device;
+        if (dj != c->device) {
+          int can = 0;
+          CK(cudaDeviceCanAccessPeer(&can, c->device, dj));
+          if (!can) throw CudaError("device " + std::to_string(c->device) + " cannot access peer " + std::to_string(dj));
+          const cudaError_t e = cudaDeviceEnablePeerAccess(dj, 0);
+          if (e == cudaErrorPeerAccessAlreadyEnabled) cudaGetLastError();
+          else CK(e);
+        }
+        ptrs.push_back(&ctxs[j]->G->incumbent);
+      }
+      c->n_peers = (int)ptrs.size();
+      if (!ptrs.empty()) {
+        c->d_peers.ensure(ptrs.size());
+        CK(cudaMemcpy(c->d_peers.p, ptrs.data(), ptrs.size() * sizeof(int*), cudaMemcpyHostToDevice));
+      }
+    }
+    return PCCP_OK;
+  });
+}
+
 }  // extern "C"

@@ -84,6 +84,23 @@ __device__ __forceinline__ bool should_stop(const G& g, const SearchCtl& C) {
   return g.bcast0(stop) != 0;
 }
 
+// The stop flag and the timeout only (no node reservation): checked by the
+// EPS decomposition per parent, as decompose() checks should_stop
+// (solver.cpp:189).
+template <class G>
+__device__ __forceinline__ bool time_stop(const G& g, const SearchCtl& C) {
+  int stop = 0;
+  if (g.rank() == 0) {
+    Globals* Gl = C.G;
+    stop = *(volatile int*)&Gl->stop;
+    if (!stop && Gl->timeout_ns && globaltimer() - Gl->t0 >= Gl->timeout_ns) {
+      atomicCAS(&Gl->stop, 0, 1);
+      stop = 1;
+    }
+  }
+  return g.bcast0(stop) != 0;
+}
+
 // record_solution + Objective::improve (solver.cpp:104-118, solver.hpp:43-49):
 // CAS-min on the incumbent, pushed to every peer GPU's replica; the best
 // store is written under a lock so it always matches best_value.
@@ -304,6 +321,14 @@ __global__ void __launch_bounds__(MaxThreads<G>::value, MaxThreads<G>::min_block
   const DeviceLayout& L = M.L;
   Cnt cnt;
   for (int p = gid; p < n_par; p += ng) {
+    if (time_stop(g, C)) {  // abandoned parent: its subtree is unexplored
+      if (g.rank() == 0) {
+        C.G->incomplete = 1;
+        flags[2 * p] = flags[2 * p + 1] = 0;
+      }
+      g.sync();
+      continue;
+    }
     const int* par = parents + (size_t)parent_idx[p] * stride;
     copy_words(g, S, par, (int)L.n_words);
     g.sync();

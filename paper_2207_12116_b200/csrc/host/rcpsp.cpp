@@ -3,6 +3,9 @@
 #include "rcpsp.hpp"
 
 #include <algorithm>
+#include <cctype>
+#include <climits>
+#include <cstdint>
 #include <random>
 #include <set>
 #include <sstream>
@@ -124,6 +127,237 @@ RcpspInstance parse_patterson(const std::string& text) {
   inst.horizon = static_cast<std::int32_t>(std::min<std::int64_t>(h, kPosInf - 2));
   validate(inst);
   return inst;
+}
+
+namespace {
+
+// A small JSON reader: just enough of RFC 8259 for instance files (objects,
+// arrays, integers, strings, true/false/null).  Values are kept as a tree.
+struct JVal {
+  enum class T { Null, Bool, Num, Str, Arr, Obj } t = T::Null;
+  long long num = 0;
+  bool real = false;  // a number with a fraction or exponent
+  std::string str;
+  std::vector<JVal> arr;
+  std::vector<std::pair<std::string, JVal>> obj;
+  const JVal* get(const std::string& k) const {
+    for (const auto& [key, v] : obj)
+      if (key == k) return &v;
+    return nullptr;
+  }
+};
+
+class JParser {
+ public:
+  explicit JParser(const std::string& s) : s_(s) {}
+  JVal document() {
+    JVal v = value(0);
+    ws();
+    if (i_ != s_.size()) fail("trailing characters");
+    return v;
+  }
+
+ private:
+  [[noreturn]] void fail(const std::string& what) const {
+    throw ModelError("bad json instance: " + what + " at offset " + std::to_string(i_));
+  }
+  void ws() {
+    while (i_ < s_.size() && (s_[i_] == ' ' || s_[i_] == '\t' || s_[i_] == '\n' || s_[i_] == '\r')) ++i_;
+  }
+  bool lit(const char* w) {
+    const std::size_t n = std::char_traits<char>::length(w);
+    if (s_.compare(i_, n, w) != 0) return false;
+    i_ += n;
+    return true;
+  }
+  std::string string() {
+    std::string out;
+    ++i_;  // opening quote
+    while (i_ < s_.size() && s_[i_] != '"') {
+      char c = s_[i_++];
+      if (c == '\\') {
+        if (i_ >= s_.size()) fail("unterminated escape");
+        c = s_[i_++];
+        switch (c) {
+          case 'n': c = '\n'; break;
+          case 't': c = '\t'; break;
+          case 'r': c = '\r'; break;
+          case 'b': c = '\b'; break;
+          case 'f': c = '\f'; break;
+          case 'u':
+            if (i_ + 4 > s_.size()) fail("bad unicode escape");
+            i_ += 4;  // keys of interest are ASCII; keep a placeholder
+            c = '?';
+            break;
+          default: break;  // \" \\ \/
+        }
+      }
+      out.push_back(c);
+    }
+    if (i_ >= s_.size()) fail("unterminated string");
+    ++i_;
+    return out;
+  }
+  JVal value(int depth) {
+    if (depth > 64) fail("nesting too deep");
+    ws();
+    if (i_ >= s_.size()) fail("unexpected end");
+    JVal v;
+    const char c = s_[i_];
+    if (c == '{') {
+      v.t = JVal::T::Obj;
+      ++i_;
+      ws();
+      if (i_ < s_.size() && s_[i_] == '}') {
+        ++i_;
+        return v;
+      }
+      for (;;) {
+        ws();
+        if (i_ >= s_.size() || s_[i_] != '"') fail("expected a key");
+        std::string k = string();
+        ws();
+        if (i_ >= s_.size() || s_[i_] != ':') fail("expected ':'");
+        ++i_;
+        v.obj.emplace_back(std::move(k), value(depth + 1));
+        ws();
+        if (i_ < s_.size() && s_[i_] == ',') {
+          ++i_;
+          continue;
+        }
+        if (i_ < s_.size() && s_[i_] == '}') {
+          ++i_;
+          return v;
+        }
+        fail("expected ',' or '}'");
+      }
+    }
+    if (c == '[') {
+      v.t = JVal::T::Arr;
+      ++i_;
+      ws();
+      if (i_ < s_.size() && s_[i_] == ']') {
+        ++i_;
+        return v;
+      }
+      for (;;) {
+        v.arr.push_back(value(depth + 1));
+        ws();
+        if (i_ < s_.size() && s_[i_] == ',') {
+          ++i_;
+          continue;
+        }
+        if (i_ < s_.size() && s_[i_] == ']') {
+          ++i_;
+          return v;
+        }
+        fail("expected ',' or ']'");
+      }
+    }
+    if (c == '"') {
+      v.t = JVal::T::Str;
+      v.str = string();
+      return v;
+    }
+    if (lit("true")) {
+      v.t = JVal::T::Bool;
+      v.num = 1;
+      return v;
+    }
+    if (lit("false")) {
+      v.t = JVal::T::Bool;
+      return v;
+    }
+    if (lit("null")) return v;
+    if (c == '-' || (c >= '0' && c <= '9')) {
+      const std::size_t b = i_;
+      if (s_[i_] == '-') ++i_;
+      while (i_ < s_.size() && std::isdigit(static_cast<unsigned char>(s_[i_]))) ++i_;
+      while (i_ < s_.size() && (s_[i_] == '.' || s_[i_] == 'e' || s_[i_] == 'E' || s_[i_] == '+' || s_[i_] == '-' ||
+                                std::isdigit(static_cast<unsigned char>(s_[i_])))) {
+        v.real = true;
+        ++i_;
+      }
+      const std::string tok = s_.substr(b, i_ - b);
+      if (tok == "-" || tok.size() > 19) fail("bad number");
+      v.t = JVal::T::Num;
+      v.num = v.real ? static_cast<long long>(std::stod(tok)) : std::stoll(tok);
+      return v;
+    }
+    fail("unexpected character");
+  }
+  const std::string& s_;
+  std::size_t i_ = 0;
+};
+
+std::int32_t jint(const JVal& v, const char* what) {
+  if (v.t != JVal::T::Num || v.real || v.num < INT32_MIN || v.num > INT32_MAX)
+    throw ModelError(std::string("bad json instance: ") + what + " must be a 32-bit integer");
+  return static_cast<std::int32_t>(v.num);
+}
+
+std::vector<std::int32_t> jints(const JVal& v, const char* what) {
+  if (v.t != JVal::T::Arr) throw ModelError(std::string("bad json instance: ") + what + " must be an array");
+  std::vector<std::int32_t> out;
+  for (const JVal& x : v.arr) out.push_back(jint(x, what));
+  return out;
+}
+
+}  // namespace
+
+RcpspInstance parse_json(const std::string& text) {
+  const JVal j = JParser(text).document();
+  if (j.t != JVal::T::Obj) throw ModelError("bad json instance: the document must be an object");
+  const JVal* tasks = j.get("tasks");
+  if (!tasks || tasks->t != JVal::T::Arr) throw ModelError("bad json instance: key 'tasks' not found");
+  RcpspInstance inst;
+  if (const JVal* c = j.get("capacities")) inst.capacity = jints(*c, "capacities");
+  for (const JVal& t : tasks->arr) {
+    if (t.t != JVal::T::Obj) throw ModelError("bad json instance: a task must be an object");
+    const JVal* d = t.get("duration");
+    if (!d) throw ModelError("bad json instance: key 'duration' not found");
+    inst.duration.push_back(jint(*d, "duration"));
+    std::vector<std::int32_t> u;
+    if (const JVal* us = t.get("usages")) u = jints(*us, "usages");
+    u.resize(inst.capacity.size(), 0);  // rcpsp.cpp:155: usages padded/truncated to the resources
+    inst.usage.push_back(std::move(u));
+  }
+  if (const JVal* ps = j.get("precedences")) {
+    if (ps->t != JVal::T::Arr) throw ModelError("bad json instance: precedences must be an array");
+    for (const JVal& p : ps->arr) {
+      const std::vector<std::int32_t> ij = jints(p, "precedence");
+      if (ij.size() != 2) throw ModelError("precedence entries must be pairs");
+      if (ij[0] < 0 || ij[1] < 0) throw ModelError("precedence endpoint out of range");
+      inst.precedences.emplace_back(ij[0], ij[1]);
+    }
+  }
+  if (const JVal* h = j.get("horizon")) {
+    inst.horizon = jint(*h, "horizon");
+  } else {
+    std::int64_t sum = 0;
+    for (std::int32_t d : inst.duration) sum += d;
+    inst.horizon = static_cast<std::int32_t>(std::min<std::int64_t>(sum, kPosInf - 2));
+  }
+  validate(inst);
+  return inst;
+}
+
+std::string patterson_text(const RcpspInstance& inst) {
+  std::ostringstream o;
+  const std::size_t n = inst.tasks();
+  o << n << ' ' << inst.resources() << '\n';
+  for (std::size_t k = 0; k < inst.resources(); ++k) o << (k ? " " : "") << inst.capacity[k];
+  o << '\n';
+  std::vector<std::vector<std::int32_t>> succ(n);
+  for (const auto& [i, j] : inst.precedences) succ[static_cast<std::size_t>(i)].push_back(j + 1);
+  for (std::size_t i = 0; i < n; ++i) {
+    o << inst.duration[i];
+    for (std::int32_t u : inst.usage[i]) o << ' ' << u;
+    o << ' ' << succ[i].size();
+    for (std::int32_t j : succ[i]) o << ' ' << j;
+    o << '\n';
+  }
+  return o.str();
 }
 
 RcpspModel build_rcpsp(const RcpspInstance& inst) {

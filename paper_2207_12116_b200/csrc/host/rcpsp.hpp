@@ -34,6 +34,16 @@ RcpspInstance random_patterson(std::uint64_t seed, int n_real, int resources);
 // Patterson text (rcpsp::parse_patterson, rcpsp.cpp:94-127); throws ModelError.
 RcpspInstance parse_patterson(const std::string& text);
 
+// JSON instance (rcpsp::parse_json_text, rcpsp.cpp:140-168): {"tasks": [{"duration": d,
+// "usages": [...]}, ...], "capacities": [...], "precedences": [[i, j], ...],
+// "horizon": h}; missing usages are 0, a missing horizon is the duration sum.
+// Throws ModelError ("bad json instance: ...").
+RcpspInstance parse_json(const std::string& text);
+
+// Patterson text of an instance (the inverse of parse_patterson; the
+// reference's testsupport::patterson_text, used for file round trips).
+std::string patterson_text(const RcpspInstance& inst);
+
 struct RcpspModel {
   std::unique_ptr<Model> model;
   std::vector<std::int32_t> starts;    // start slot per task
