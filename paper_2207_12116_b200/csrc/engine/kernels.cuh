@@ -224,6 +224,12 @@ __device__ __forceinline__ int sld(unsigned a) {
   asm volatile("ld.volatile.shared.b32 %0, [%1];" : "=r"(v) : "r"(a));
   return v;
 }
+// (lb, ub) of an interval whose lb word is even: one 8-byte load.
+__device__ __forceinline__ int2 sld2(unsigned a) {
+  int2 v;
+  asm volatile("ld.volatile.shared.v2.b32 {%0, %1}, [%2];" : "=r"(v.x), "=r"(v.y) : "r"(a));
+  return v;
+}
 __device__ __forceinline__ int satom_max(unsigned a, int v) {
   int old;
   asm volatile("atom.shared.max.s32 %0, [%1], %2;" : "=r"(old) : "r"(a), "r"(v) : "memory");
@@ -280,8 +286,8 @@ __device__ __forceinline__ bool sjoin_min(unsigned a, int v) {
 // words.  Returns the mask of changed words (bit w of the word index, words
 // >= 64 unmasked: callers that track masks only use stores of <= 64 words).
 __device__ __forceinline__ unsigned long long eval_ne(unsigned sb, int4 q) {
-  const unsigned wx = (unsigned)q.x & 0xffffu, wy = (unsigned)q.x >> 16;
-  const unsigned ax = sb + (wx << 2), ay = sb + (wy << 2);
+  const unsigned wx = (unsigned)q.x >> 2, wy = (unsigned)q.w >> 2;
+  const unsigned ax = sb + (unsigned)q.x, ay = sb + (unsigned)q.w;
   const int lx = sld(ax), ux = sld(ax + 4), ly = sld(ay), uy = sld(ay + 4);
   const int a = q.y, b = q.z;
   unsigned long long m = 0;
@@ -311,6 +317,26 @@ __device__ __forceinline__ unsigned long long eval_ne(unsigned sb, int4 q) {
     }
   }
   return m;
+}
+
+// eval_ne when the host's value-range analysis (ne_fast_ok, lower.cpp) has
+// proved every value read stays inside (-2^30, 2^30): the 32-bit path is then
+// exact with no range checks, and (lb, ub) pairs load as one 8-byte word.
+__device__ __forceinline__ bool eval_ne_fast(unsigned sb, int4 q) {
+  const unsigned ax = sb + (unsigned)q.x, ay = sb + (unsigned)q.w;
+  const int2 X = sld2(ax), Y = sld2(ay);
+  const int a = q.y, b = q.z;
+  const bool g1 = X.y - Y.x <= -a, g2 = Y.y - X.x <= -b;
+  const int v1 = Y.y + b - 1, v2 = X.x + 1 - b, v3 = X.y + a - 1, v4 = Y.x + 1 - a;
+  const bool c1 = g1 & (v1 < X.y), c2 = g1 & (v2 > Y.x), c3 = g2 & (v3 < Y.y), c4 = g2 & (v4 > X.x);
+  bool ch = false;
+  if (c1 | c2 | c3 | c4) {
+    if (c1 && satom_min(ax + 4, v1) > v1) ch = true;
+    if (c2 && satom_max(ay, v2) < v2) ch = true;
+    if (c3 && satom_min(ay + 4, v3) > v3) ch = true;
+    if (c4 && satom_max(ax, v4) < v4) ch = true;
+  }
+  return ch;
 }
 
 // Fused reification b <-> (x + p <= y and y + q <= x): the 11 commands of
@@ -604,7 +630,11 @@ __device__ bool propagate(const G& g, volatile int* S, unsigned sb, const Tab<TS
   bool failed = false;
   for (;;) {
     bool ch = false, fl = false;
-    for (int i = g.rank(); i < (int)L.n_ne; i += g.size()) ch |= eval_ne(sb, tab.ld4(L.ne, i)) != 0ull;
+    if (L.ne_fast) {
+      for (int i = g.rank(); i < (int)L.n_ne; i += g.size()) ch |= eval_ne_fast(sb, tab.ld4(L.ne, i));
+    } else {
+      for (int i = g.rank(); i < (int)L.n_ne; i += g.size()) ch |= eval_ne(sb, tab.ld4(L.ne, i)) != 0ull;
+    }
     for (int i = g.rank(); i < (int)L.n_reif; i += g.size()) ch |= eval_reif(sb, tab.ld4(L.reif, i));
     for (int i = g.rank(); i < (int)L.n_unit1; i += g.size()) {
       const int4 q = tab.ld4(L.unit1, i);

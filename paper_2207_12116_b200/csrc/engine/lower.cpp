@@ -517,12 +517,18 @@ Lowered lower_model(const pccp_model& m) {
   };
   L.n_ne = static_cast<std::uint32_t>(nes.size());
   L.ne = reserve_arr(4 * L.n_ne);
-  for (std::uint32_t i = 0; i < L.n_ne; ++i) {
-    B[L.ne + 4 * i + 0] = nes[i].x;
+  L.ne_even = 1;
+  std::int64_t ne_k = 0;
+  for (std::uint32_t i = 0; i < L.n_ne; ++i) {  // {4 lbx, a, b, 4 lby}: byte offsets into the store
+    const std::uint32_t lx = static_cast<std::uint32_t>(nes[i].x) & 0xffffu, ly = static_cast<std::uint32_t>(nes[i].x) >> 16;
+    B[L.ne + 4 * i + 0] = static_cast<std::int32_t>(4 * lx);
     B[L.ne + 4 * i + 1] = nes[i].a;
     B[L.ne + 4 * i + 2] = nes[i].b;
-    B[L.ne + 4 * i + 3] = 0;
+    B[L.ne + 4 * i + 3] = static_cast<std::int32_t>(4 * ly);
+    if ((lx | ly) & 1u) L.ne_even = 0;
+    ne_k = std::max({ne_k, std::abs(std::int64_t{nes[i].a}), std::abs(std::int64_t{nes[i].b})});
   }
+  L.ne_k = static_cast<std::uint32_t>(std::min<std::int64_t>(ne_k + 1, 1 << 30));
   // Order the reifications x-major: a warp then reads one x (broadcast) and
   // consecutive y / b words (2-way bank conflicts).  RCPSP compiles them
   // j-major (rcpsp.cpp:241-242), which puts b_ij of a warp n words apart —
@@ -727,6 +733,34 @@ Lowered lower_model(const pccp_model& m) {
   L.blob_words = static_cast<std::uint32_t>(B.size());
   if (B.empty()) B.push_back(0);
   return out;
+}
+
+bool ne_fast_ok(const Lowered& low, const std::int32_t* stores, std::size_t n_stores, std::size_t stride) {
+  const DeviceLayout& L = low.L;
+  if (!L.ne_even || L.n_ne == 0) return false;
+  if (L.n_reif || L.n_unit1 || L.n_unit2 || L.n_small || L.n_rows || L.n_gen || L.n_sc || L.filtered) return false;
+  // Start values: a store joined with the fold tells.  Outside a failed round
+  // every interval stays inside its start box (lb only rises, ub only falls);
+  // inside a round a value is a start value plus at most one NE offset per
+  // join of a dependency chain, and a round makes <= 4 * n_ne joins.  The
+  // objective and decision joins stay inside the box (+-1).
+  const std::uint32_t nw = L.n_words;
+  std::vector<std::int32_t> w(nw);
+  std::int64_t bound = 0;
+  for (std::size_t s = 0; s < n_stores; ++s) {
+    std::copy(stores + s * stride, stores + s * stride + nw, w.begin());
+    for (std::uint32_t i = 0; i < L.n_fold; ++i) {
+      const std::int32_t wf = low.blob[L.fold_w + i], v = low.blob[L.fold_v + i];
+      std::int32_t& x = w[static_cast<std::uint32_t>(wf) & 0x7fffffffu];
+      x = wf < 0 ? std::max(x, v) : std::min(x, v);
+    }
+    for (std::uint32_t i = 0; i < nw; ++i) {
+      if (w[i] == INT32_MIN || w[i] == INT32_MAX) return false;
+      bound = std::max(bound, std::abs(std::int64_t{w[i]}));
+    }
+  }
+  const std::int64_t reach = bound + 1 + (4 * std::int64_t{L.n_ne} + 1) * std::int64_t{L.ne_k};
+  return reach < (std::int64_t{1} << 29);
 }
 
 void host_join_decision(const pccp_model& m, std::int32_t* words, const pccp_decision& d) {

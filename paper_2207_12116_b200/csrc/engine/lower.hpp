@@ -38,7 +38,9 @@ struct DeviceLayout {
   std::uint32_t zero_word;               // constant-zero word Z = n_words (store_stride > n_words)
   // Fused not(and(x + a <= y, y + b <= x)) groups: the 4 commands compile_rec
   // emits for it (propagation.cpp:350-360) read and write only lb/ub of x and y.
-  std::uint32_t ne, n_ne;                // int4 {lbx | lby << 16, a, b, 0}
+  std::uint32_t ne, n_ne;                // int4 {4 lbx, a, b, 4 lby} (byte offsets of the lb words)
+  std::uint32_t ne_even;                 // every NE lb word is even: (lb, ub) is one 8-byte load
+  std::uint32_t ne_k;                    // max |a|, |b| over the NE records, + 1
   // Fused compile_reified(b, and(x + p <= y, y + q <= x)): the 11 commands of
   // propagation.cpp:415-431 over lb/ub of x, y and b (RCPSP overlaps).
   std::uint32_t reif, n_reif;            // int4 {lbx | lby << 16, lbb, p, q}
@@ -69,7 +71,9 @@ struct DeviceLayout {
   std::uint32_t hot_words;  // prefix of the blob read every round (small + rows)
   std::uint32_t var_order;  // set per launch: 0 first-fail (branch, solver.cpp:19-47), 1-3 smallest lb
   std::uint32_t var_seed;   // set per launch: var_order 3 tie-break seed
+  std::uint32_t ne_fast;    // set per launch: value-range analysis proved the 32-bit NE path exact
 };
+
 
 struct Lowered {
   DeviceLayout L{};
@@ -82,6 +86,12 @@ struct Lowered {
 
 // Throws std::runtime_error (mapped to PCCP_EMODEL) on malformed tables.
 Lowered lower_model(const pccp_model& m);
+
+// Value-range analysis for NE-only models (engine.cu sets DeviceLayout::ne_fast):
+// true when every store in `stores` (after the fold tells) is finite and
+// bounded so that no NE evaluation can leave (-2^30, 2^30), i.e. the range
+// checks and the widened path of eval_ne can be skipped exactly.
+bool ne_fast_ok(const Lowered& low, const std::int32_t* stores, std::size_t n_stores, std::size_t stride);
 
 // Host-side join of a decision into a store (Decision::as_join +
 // Store::join_in_place on an Interval, solver.hpp:20-23, store.cpp:51-63).

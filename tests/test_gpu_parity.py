@@ -139,6 +139,53 @@ def test_sentinel_and_wide_arithmetic(n, shift, engine):
             assert np.array_equal(w, wo)
 
 
+@pytest.mark.parametrize("shift", [0, 5000, 2**29 - 40000, -(2**29) + 3])
+@pytest.mark.parametrize("n", [8, 14])
+def test_ne_fast_path_finite_boxes(n, shift, engine):
+    """Finite stores: the host's value-range analysis (ne_fast_ok) admits the
+    check-free NE path for small boxes and refuses it near 2^29; either way the
+    fixed points equal the oracle's (and the same run with PCCP_NO_NE_FAST)."""
+    import os
+    t = _strip_init(build(f"nqueens{n}"), n)
+    o = Oracle(t)
+    engine.load(t)
+    rng = np.random.default_rng(n * 7919 + (shift % 1009))
+    stores = []
+    for _ in range(512):
+        s = o.bottom()
+        for w in t.slot_word:
+            a, b = sorted(int(v) + shift for v in rng.integers(-3, n + 1, 2))
+            s[w], s[w + 1] = a, b + int(rng.integers(0, 2))
+        stores.append(s)
+    out, failed, _ = engine.propagate_batch(np.stack(stores))
+    os.environ["PCCP_NO_NE_FAST"] = "1"
+    try:
+        out2, failed2, _ = engine.propagate_batch(np.stack(stores))
+    finally:
+        del os.environ["PCCP_NO_NE_FAST"]
+    assert np.array_equal(failed, failed2)
+    for s, w, w2, f in zip(stores, out, out2, failed):
+        fo, wo, _, _ = o.run_sequential(s)
+        assert f == fo
+        if not f:
+            assert np.array_equal(w, wo) and np.array_equal(w2, wo)
+
+
+@pytest.mark.parametrize("n", [8, 10])
+def test_enumerate_nqueens_without_fast_path(n, golden):
+    import os
+    from paper_2207_12116_b200 import Engine
+    g = golden[f"nqueens{n}"]["enumerate"]
+    os.environ["PCCP_NO_NE_FAST"] = "1"
+    try:
+        with Engine(0, hash=True) as e:
+            res = e.load(build(f"nqueens{n}")).enumerate()
+    finally:
+        del os.environ["PCCP_NO_NE_FAST"]
+    for k in ("nodes", "failures", "solutions", "hash_sum"):
+        assert res[k] == g[k], (n, k)
+
+
 def test_replayed_paths(golden, engine):
     """materialize() of sampled decision paths (with objective bounds) == reference."""
     for name in config_names(golden):
