@@ -125,13 +125,12 @@ def load_peaks():
         return {}
 
 
-def ncu_traffic(workload):
-    """DRAM bytes per launch of k_search from the committed ncu --set full summary."""
+def ncu_kernel(workload):
+    """The committed ncu --set full summary of k_search for a workload (profiles/)."""
     p = os.path.join(ROOT, "profiles", "ncu_summary.json")
     try:
         with open(p) as f:
-            d = json.load(f)
-        return d[workload]["k_search"]["dram_bytes_per_launch"]
+            return json.load(f)[workload]["k_search"]
     except Exception:
         return None
 
@@ -461,7 +460,22 @@ def main():
     smem_peak = 148 * 128 * sm_mhz * 1e6 / 1e9  # GB/s: 148 SMs x 128 B/clk
     b_alg = info["alg_bytes_per_eval"]
     achieved = statistics.mean(se * b_alg / (km / 1e3) / 1e9 / world for se, km in zip(sevals_all, kern_max))
-    traffic = ncu_traffic(w["workload"])
+    nk = ncu_kernel(w["workload"])
+    traffic = nk["dram_bytes_per_launch"] if nk else None
+    kern_s = statistics.mean(kern_max) / 1e3
+    physical = None
+    if nk:  # per-launch ncu counts over this run's live kernel time
+        clk = sm_mhz * 1e6
+        physical = {
+            "smem_gbs": nk["smem_wavefronts"] * 128 / kern_s / 1e9,
+            "smem_frac": nk["smem_wavefronts"] * 128 / kern_s / 1e9 / smem_peak,
+            "issue_frac": nk["warp_instructions"] / kern_s / (148 * 4 * clk),
+            "source": nk["source"],
+            "note": "fused records read each store word once for several reference commands, so the per-command "
+                    "byte model of SURVEY 8(d) (alg_bytes_per_eval) exceeds the physical shared-memory traffic and "
+                    "frac can pass 1; the physical figures are ncu's shared-memory wavefronts (x 128 B) and warp "
+                    "instructions per launch over this run's kernel time: the kernel is instruction-issue bound",
+        }
     line = {
         "metric": "search nodes/sec", "value": value, "unit": "nodes/s", "n_gpus": world, "steps": a.steps,
         "warmup": a.warmup, "ms_per_step": 1e3 * total_dev_s / a.steps, "higher_is_better": True,
@@ -479,7 +493,7 @@ def main():
                      "evals_per_s": statistics.mean(se / (km / 1e3) for se, km in zip(sevals_all, kern_max)),
                      "peak_source": f"148 SMs x 128 B/clk x {sm_mhz:.0f} MHz (SM clock sampled during the run); "
                                     "the path is shared-memory bound (SURVEY 8(d)), HBM/tensor peaks do not apply",
-                     "hbm_peak_gbs": peaks.get("hbm_gbs")},
+                     "hbm_peak_gbs": peaks.get("hbm_gbs"), "physical": physical},
         "parity": {"exact": all(parity.values()), **parity},
         "region_ms": region_ms, "region_wall_s": region_wall,
         "kernel_ms_per_step": statistics.mean(kern_max),

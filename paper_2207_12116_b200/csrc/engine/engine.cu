@@ -110,6 +110,7 @@ struct pccp_gpu_ctx {
   size_t smem = 0;
   int store_stride = 4;
   int table_in_smem = 0;
+  int ne_only = 0;  // lowered to NE records (and fold tells) only: the kNeOnly kernels
 
   DBuf<int> fa, fb, ia, ib, stack, best, io, mailbox, waitq;
   DBuf<unsigned char> flags, st;
@@ -132,36 +133,44 @@ struct pccp_gpu_ctx {
     M.blob = blob.p;
     M.table_in_smem = table_in_smem;
     M.store_stride = store_stride;
+    M.cnt_slots = warp ? gpc : 1;
     return M;
   }
 };
 
 namespace {
 
-template <class Gp, bool TS>
+template <class Gp, bool TS, int F>
 void set_smem_attrs(size_t smem) {
-  CK(cudaFuncSetAttribute(dev::k_propagate<Gp, TS>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-  CK(cudaFuncSetAttribute(dev::k_root<Gp, TS>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-  CK(cudaFuncSetAttribute(dev::k_expand<Gp, TS>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-  CK(cudaFuncSetAttribute(dev::k_search<Gp, TS>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  CK(cudaFuncSetAttribute(dev::k_propagate<Gp, TS, F>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  CK(cudaFuncSetAttribute(dev::k_root<Gp, TS, F>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  CK(cudaFuncSetAttribute(dev::k_expand<Gp, TS, F>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  CK(cudaFuncSetAttribute(dev::k_search<Gp, TS, F>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
 }
 
-template <class Gp, bool TS>
+template <class Gp, bool TS, int F>
 int occupancy(int block, size_t smem) {
   int occ = 0;
-  CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, dev::k_search<Gp, TS>, block, smem));
+  CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, dev::k_search<Gp, TS, F>, block, smem));
   return occ;
 }
 
-// Calls f.template operator()<Group, TableInSmem>() for the context's plan.
-template <class F>
-void dispatch(const pccp_gpu_ctx* c, F&& f) {
-  if (c->warp) {
-    if (c->table_in_smem) f.template operator()<dev::WarpGroup, true>();
-    else f.template operator()<dev::WarpGroup, false>();
+// Calls f.template operator()<Group, TableInSmem, Families>() for the
+// context's plan: warp or CTA groups, tables in shared or global memory, and
+// the NE-only kernel for models lowered to NE records alone (warp groups).
+template <class Fn>
+void dispatch(const pccp_gpu_ctx* c, Fn&& f) {
+  using dev::kAllFamilies;
+  using dev::kNeOnly;
+  if (c->warp && c->ne_only) {
+    if (c->table_in_smem) f.template operator()<dev::WarpGroup, true, kNeOnly>();
+    else f.template operator()<dev::WarpGroup, false, kNeOnly>();
+  } else if (c->warp) {
+    if (c->table_in_smem) f.template operator()<dev::WarpGroup, true, kAllFamilies>();
+    else f.template operator()<dev::WarpGroup, false, kAllFamilies>();
   } else {
-    if (c->table_in_smem) f.template operator()<dev::CtaGroup, true>();
-    else f.template operator()<dev::CtaGroup, false>();
+    if (c->table_in_smem) f.template operator()<dev::CtaGroup, true, kAllFamilies>();
+    else f.template operator()<dev::CtaGroup, false, kAllFamilies>();
   }
 }
 
@@ -183,18 +192,22 @@ void plan(pccp_gpu_ctx* c) {
     c->gpc = 1;
     c->block = t;
   }
-  const size_t base = 72 * 4 + (size_t)(c->warp ? c->gpc : 1) * c->store_stride * 4;
+  const size_t base = 72 * 4 + (size_t)(c->warp ? c->gpc : 1) * (c->store_stride * 4 + 64);  // + one Cnt per group
   const size_t table = (size_t)align4(L.blob_words) * 4;
   if (base > c->smem_optin) throw LimitError("store of " + std::to_string(L.n_words) + " words exceeds shared memory");
+  c->ne_only = L.n_ne > 0 && !L.n_reif && !L.n_unit1 && !L.n_unit2 && !L.n_small && !L.n_rows && !L.n_gen &&
+                       !L.filtered && !std::getenv("PCCP_NO_NE_KERNEL")
+                   ? 1
+                   : 0;
   const char* env = std::getenv("PCCP_TABLE_SMEM");
   bool in_smem = base + table <= 100 * 1024;
   if (env) in_smem = std::atoi(env) != 0 && base + table <= c->smem_optin;
   c->table_in_smem = in_smem ? 1 : 0;
   c->smem = base + (in_smem ? table : 0);
   int occ = 0;
-  dispatch(c, [&]<class Gp, bool TS>() {
-    set_smem_attrs<Gp, TS>(c->smem);
-    occ = occupancy<Gp, TS>(c->block, c->smem);
+  dispatch(c, [&]<class Gp, bool TS, int F>() {
+    set_smem_attrs<Gp, TS, F>(c->smem);
+    occ = occupancy<Gp, TS, F>(c->block, c->smem);
   });
   if (occ < 1) throw LimitError("kernel does not fit on an SM (smem " + std::to_string(c->smem) + " B)");
   if (c->cfg.ctas_per_sm > 0) occ = std::min(occ, c->cfg.ctas_per_sm);
@@ -252,7 +265,7 @@ struct RunOut {
   double device_ms = 0;
 };
 
-template <class Gp, bool TS>
+template <class Gp, bool TS, int F>
 void run_search(pccp_gpu_ctx* c, int mode, const int32_t* root_words, int depth_cap, const pccp_limits* lim,
                 RunOut& out, int var_order = 0, bool keep_incumbent = false, unsigned long long stall_ns = 0,
                 unsigned var_seed = 0) {
@@ -286,7 +299,7 @@ void run_search(pccp_gpu_ctx* c, int mode, const int32_t* root_words, int depth_
   CK(cudaMemcpyAsync(c->ia.p, &zero, 4, cudaMemcpyHostToDevice, c->stream));
   out.h2d += sizeof(dev::Globals) + (std::uint64_t)nw * 4 + 4;
   CK(cudaEventRecord(c->ev[0], c->stream));
-  dev::k_root<Gp, TS><<<1, c->block, c->smem, c->stream>>>(M, C, c->fa.p, c->flags.p);
+  dev::k_root<Gp, TS, F><<<1, c->block, c->smem, c->stream>>>(M, C, c->fa.p, c->flags.p);
   CK(cudaGetLastError());
   ++c->launches;
   unsigned char rflag = 0;
@@ -313,7 +326,7 @@ void run_search(pccp_gpu_ctx* c, int mode, const int32_t* root_words, int depth_
     c->ib.ensure(nchild);
     c->flags.ensure(nchild);
     const int grid = (int)std::min<long long>(c->ctas, (count + (c->warp ? c->gpc : 1) - 1) / (c->warp ? c->gpc : 1));
-    dev::k_expand<Gp, TS><<<grid, c->block, c->smem, c->stream>>>(M, C, c->fa.p, c->ia.p, count, stride, level + 1,
+    dev::k_expand<Gp, TS, F><<<grid, c->block, c->smem, c->stream>>>(M, C, c->fa.p, c->ia.p, count, stride, level + 1,
                                                                 c->fb.p, c->flags.p);
     CK(cudaGetLastError());
     dev::k_compact<<<1, 1024, 0, c->stream>>>(c->flags.p, (int)nchild, c->ib.p, dcount.p);
@@ -365,7 +378,7 @@ void run_search(pccp_gpu_ctx* c, int mode, const int32_t* root_words, int depth_
     if (const char* vo = std::getenv("PCCP_VALUE_ORDER")) P.value_order = std::atoi(vo);
     P.waitq = c->waitq.p;
     C.count = 1;
-    dev::k_search<Gp, TS><<<c->ctas, c->block, c->smem, c->stream>>>(M, C, P);
+    dev::k_search<Gp, TS, F><<<c->ctas, c->block, c->smem, c->stream>>>(M, C, P);
     CK(cudaGetLastError());
     ++c->launches;
     searched = true;
@@ -619,8 +632,8 @@ int pccp_gpu_propagate_batch(pccp_gpu_ctx* c, const int32_t* in, uint32_t n, int
     const dev::Model M = c->model(0, 0, ne_fast_ok(c->low, in, n, nw));
     const int per = c->warp ? c->gpc : 1;
     const int grid = (int)std::min<long long>(c->ctas, ((long long)n + per - 1) / per);
-    dispatch(c, [&]<class Gp, bool TS>() {
-      dev::k_propagate<Gp, TS><<<grid, c->block, c->smem, c->stream>>>(M, c->io.p, (int)n, (int)nw, c->st.p,
+    dispatch(c, [&]<class Gp, bool TS, int F>() {
+      dev::k_propagate<Gp, TS, F><<<grid, c->block, c->smem, c->stream>>>(M, c->io.p, (int)n, (int)nw, c->st.p,
                                                                        c->rnd.p, 1);
     });
     CK(cudaGetLastError());
@@ -663,7 +676,7 @@ int pccp_gpu_enumerate(pccp_gpu_ctx* c, const int32_t* root, int32_t depth_cap, 
     std::memset(out, 0, sizeof(*out));
     if (lim && lim->node_limit == 0) return PCCP_OK;
     RunOut r;
-    dispatch(c, [&]<class Gp, bool TS>() { run_search<Gp, TS>(c, 0, root, depth_cap, lim, r); });
+    dispatch(c, [&]<class Gp, bool TS, int F>() { run_search<Gp, TS, F>(c, 0, root, depth_cap, lim, r); });
     fill_stats(c, r, out->stats);
     out->exhausted = r.g.incomplete ? 0 : 1;
     return PCCP_OK;
@@ -712,8 +725,8 @@ int pccp_gpu_solve(pccp_gpu_ctx* c, const int32_t* root, const pccp_limits* lim,
         const double p_s = (budget_ms - spent) * 1e-3;
         l1.timeout_s = l1.timeout_s > 0 ? std::min(l1.timeout_s, p_s) : p_s;
         RunOut r1;
-        dispatch(c, [&]<class Gp, bool TS>() {
-          run_search<Gp, TS>(c, 1, root, -1, &l1, r1, primal_order, seg > 0, (unsigned long long)(stall_ms * 1e6),
+        dispatch(c, [&]<class Gp, bool TS, int F>() {
+          run_search<Gp, TS, F>(c, 1, root, -1, &l1, r1, primal_order, seg > 0, (unsigned long long)(stall_ms * 1e6),
                              (unsigned)seg);
         });
         append_log(r1.g, acc.device_ms, log);
@@ -732,11 +745,11 @@ int pccp_gpu_solve(pccp_gpu_ctx* c, const int32_t* root, const pccp_limits* lim,
     }
     pccp_limits l2;
     if (c->cfg.primal_ms <= 0) {
-      dispatch(c, [&]<class Gp, bool TS>() { run_search<Gp, TS>(c, 1, root, -1, lim, r, var_order); });
+      dispatch(c, [&]<class Gp, bool TS, int F>() { run_search<Gp, TS, F>(c, 1, root, -1, lim, r, var_order); });
       append_log(r.g, 0.0, log);
     } else if (!proved && left(l2, r)) {
       RunOut r2;
-      dispatch(c, [&]<class Gp, bool TS>() { run_search<Gp, TS>(c, 1, root, -1, &l2, r2, var_order, true); });
+      dispatch(c, [&]<class Gp, bool TS, int F>() { run_search<Gp, TS, F>(c, 1, root, -1, &l2, r2, var_order, true); });
       append_log(r2.g, r.device_ms, log);
       merge_run(r, r2, false);
       out->phases = 2;

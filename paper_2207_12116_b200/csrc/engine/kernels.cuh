@@ -32,6 +32,7 @@ struct Model {
   const int* __restrict__ blob;  // global copy of the tables
   int table_in_smem;             // copy the blob into shared memory at kernel start
   int store_stride;              // words per group store in smem (>= n_words, multiple of 4)
+  int cnt_slots;                 // groups per CTA (one Cnt each in smem)
 };
 
 // Counters and control shared by all groups of one search (global memory).
@@ -618,23 +619,12 @@ __device__ bool propagate_filtered(const WarpGroup& g, volatile int* S, unsigned
   return failed;
 }
 
+// One round of every family but NE (propagate below).
 template <class G, bool TS>
-__device__ bool propagate(const G& g, volatile int* S, unsigned sb, const Tab<TS>& tab, const DeviceLayout& L,
-                          int& rounds, unsigned long long dirty = kAllDirty) {
-  if constexpr (std::is_same<G, WarpGroup>::value) {
-    if (L.filtered) return propagate_filtered(g, S, sb, tab, L, dirty, rounds);
-  }
-  const int* __restrict__ T = tab.p;
-  g.round_begin();
-  int r = 0;
-  bool failed = false;
-  for (;;) {
-    bool ch = false, fl = false;
-    if (L.ne_fast) {
-      for (int i = g.rank(); i < (int)L.n_ne; i += g.size()) ch |= eval_ne_fast(sb, tab.ld4(L.ne, i));
-    } else {
-      for (int i = g.rank(); i < (int)L.n_ne; i += g.size()) ch |= eval_ne(sb, tab.ld4(L.ne, i)) != 0ull;
-    }
+__device__ __forceinline__ bool eval_other_families(const G& g, volatile int* S, unsigned sb, const Tab<TS>& tab,
+                                                    const DeviceLayout& L) {
+    const int* __restrict__ T = tab.p;
+    bool ch = false;
     for (int i = g.rank(); i < (int)L.n_reif; i += g.size()) ch |= eval_reif(sb, tab.ld4(L.reif, i));
     for (int i = g.rank(); i < (int)L.n_unit1; i += g.size()) {
       const int4 q = tab.ld4(L.unit1, i);
@@ -651,6 +641,32 @@ __device__ bool propagate(const G& g, volatile int* S, unsigned sb, const Tab<TS
     if (L.n_rows) ch |= eval_rows(g, sb, tab, L);
     for (int i = g.rank(); i < (int)L.n_gen; i += g.size())
       ch |= eval_generic(S, T + L.gen_code + T[L.gen_off + i]);
+    return ch;
+}
+
+// F selects the command families compiled into the loop: kAllFamilies, or
+// kNeOnly for models lowered to NE records alone (N-Queens): a smaller
+// kernel, fewer registers, more resident groups (engine.cu dispatch).
+constexpr int kAllFamilies = 0, kNeOnly = 1;
+
+template <class G, bool TS, int F = kAllFamilies>
+__device__ bool propagate(const G& g, volatile int* S, unsigned sb, const Tab<TS>& tab, const DeviceLayout& L,
+                          int& rounds, unsigned long long dirty = kAllDirty) {
+  if constexpr (std::is_same<G, WarpGroup>::value && F == kAllFamilies) {
+    if (L.filtered) return propagate_filtered(g, S, sb, tab, L, dirty, rounds);
+  }
+  const int* __restrict__ T = tab.p;
+  g.round_begin();
+  int r = 0;
+  bool failed = false;
+  for (;;) {
+    bool ch = false, fl = false;
+    if (L.ne_fast) {
+      for (int i = g.rank(); i < (int)L.n_ne; i += g.size()) ch |= eval_ne_fast(sb, tab.ld4(L.ne, i));
+    } else {
+      for (int i = g.rank(); i < (int)L.n_ne; i += g.size()) ch |= eval_ne(sb, tab.ld4(L.ne, i)) != 0ull;
+    }
+    if constexpr (F == kAllFamilies) ch |= eval_other_families(g, S, sb, tab, L);
     for (int i = g.rank(); i < (int)L.n_iv; i += g.size()) {
       const int w = T[L.iv_lb + i];
       fl |= S[w] > S[w + 1];
@@ -665,6 +681,7 @@ __device__ bool propagate(const G& g, volatile int* S, unsigned sb, const Tab<TS
   rounds = r;
   return failed;
 }
+
 
 // branch (solver.cpp:19-47): narrowest candidate with lo < hi, first in
 // candidate order on ties (key = width << 24 | position), mid = floor((lo+hi)/2).

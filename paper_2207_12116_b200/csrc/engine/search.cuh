@@ -25,8 +25,11 @@ struct SearchCtl {
   int count;             // accumulate counters (EPS on shard 0 only)
 };
 
+// Per-group counters, kept in shared memory (Frame::cnt) and updated by the
+// group's rank 0 only: 7 u64 held in registers by every lane would cost the
+// search kernels 14 registers each, i.e. resident groups.
 struct Cnt {
-  unsigned long long nodes = 0, fails = 0, sols = 0, open = 0, hash = 0, rounds = 0, maxd = 0;
+  unsigned long long nodes = 0, fails = 0, sols = 0, open = 0, hash = 0, rounds = 0, maxd = 0, pad = 0;
 };
 
 __device__ __forceinline__ void flush(Globals* G, Cnt& c) {
@@ -102,8 +105,10 @@ __device__ __forceinline__ bool time_stop(const G& g, const SearchCtl& C) {
 }
 
 // record_solution + Objective::improve (solver.cpp:104-118, solver.hpp:43-49):
-// CAS-min on the incumbent, pushed to every peer GPU's replica; the best
-// store is written under a lock so it always matches best_value.
+// CAS-min on the incumbent, pushed to every peer GPU's replica.  Under the
+// lock (the reference's solution mutex) a solution that still beats
+// best_value is an improvement: its store is copied, it is counted and it is
+// logged, so the log is strictly decreasing (test_solver.cpp:247-261).
 template <class G>
 __device__ void record_solution(const G& g, volatile int* S, const DeviceLayout& L, const SearchCtl& C, Cnt& cnt) {
   Globals* Gl = C.G;
@@ -114,13 +119,8 @@ __device__ void record_solution(const G& g, volatile int* S, const DeviceLayout&
     improved = value < old;
     if (improved) {
       for (int p = 0; p < C.n_peers; ++p) atomicMin_system(C.peers[p], value);
-      const int k = atomicAdd(&Gl->n_impr, 1) & 63;  // ring: the last 64 improvements
-      Gl->impr_val[k] = value;
-      Gl->impr_ns[k] = globaltimer() - Gl->t0;
-      atomicMax(&Gl->last_impr_ns, Gl->impr_ns[k]);
       while (atomicCAS(&Gl->best_lock, 0, 1) != 0) {
       }
-      if (C.count) ++cnt.sols;
     }
   }
   improved = g.bcast0(improved);
@@ -132,7 +132,15 @@ __device__ void record_solution(const G& g, volatile int* S, const DeviceLayout&
   __threadfence();
   g.sync();
   if (g.rank() == 0) {
-    if (do_copy) *(volatile int*)&Gl->best_value = value;
+    if (do_copy) {
+      *(volatile int*)&Gl->best_value = value;
+      if (C.count) ++cnt.sols;
+      const int k = Gl->n_impr++ & 63;  // ring of the last 64 improvements, written under the lock
+      const unsigned long long t = globaltimer() - Gl->t0;
+      Gl->impr_val[k] = value;
+      Gl->impr_ns[k] = t;
+      *(volatile unsigned long long*)&Gl->last_impr_ns = t;
+    }
     __threadfence();
     atomicExch(&Gl->best_lock, 0);
   }
@@ -144,7 +152,7 @@ template <class G>
 __device__ int classify(const G& g, volatile int* S, const int* __restrict__ T, const DeviceLayout& L,
                         const SearchCtl& C, Cnt& cnt, bool failed, int depth, int& lbw, int& mid) {
   if (failed) {
-    if (C.count) ++cnt.fails;
+    if (C.count && g.rank() == 0) ++cnt.fails;
     return 0;
   }
   if (C.hash && C.count && g.rank() == 0) cnt.hash += store_hash(S, (int)L.n_words);
@@ -158,11 +166,11 @@ __device__ int classify(const G& g, volatile int* S, const int* __restrict__ T, 
   }
   if (b == 0) {  // every candidate fixed: a solution
     if (C.mode == 1) record_solution(g, S, L, C, cnt);
-    else if (C.count) ++cnt.sols;
+    else if (C.count && g.rank() == 0) ++cnt.sols;
     return 0;
   }
   if (C.depth_cap >= 0 && depth >= C.depth_cap) {
-    if (C.count) ++cnt.open;
+    if (C.count && g.rank() == 0) ++cnt.open;
     return 0;
   }
   return 1;
@@ -173,6 +181,7 @@ struct Frame {
   const int* __restrict__ T;
   int* ring;
   unsigned long long* red;
+  Cnt* cnt;  // one per group of the CTA
   int* stores;
 };
 
@@ -192,6 +201,10 @@ __device__ __forceinline__ Frame frame(const Model& M) {
   f.ring = smem + off;
   f.red = reinterpret_cast<unsigned long long*>(smem + off + 4);
   off += 72;
+  f.cnt = reinterpret_cast<Cnt*>(smem + off);
+  for (int i = threadIdx.x; i < M.cnt_slots * (int)(sizeof(Cnt) / 8); i += blockDim.x)
+    reinterpret_cast<unsigned long long*>(f.cnt)[i] = 0ull;
+  off += M.cnt_slots * (int)(sizeof(Cnt) / 4);
   f.stores = smem + off;
   __syncthreads();
   return f;
@@ -232,21 +245,28 @@ struct GroupOf<CtaGroup> {
 };
 
 // Launch bounds: warp groups run <= 8 warps per CTA; CTA groups up to 1024
-// threads.  Both give ptxas a 64-register budget (at least 4 CTAs of 8 warps).
-template <class G>
+// threads.  Both give ptxas a 64-register budget (at least 4 CTAs of 8 warps);
+// the NE-only warp kernel gets 40 (6 CTAs of 8 warps).
+template <class G, int F>
 struct MaxThreads {
   static constexpr int value = 1024;
   static constexpr int min_blocks = 1;
 };
-template <>
-struct MaxThreads<WarpGroup> {
+#ifndef PCCP_WARP_MIN_BLOCKS
+#define PCCP_WARP_MIN_BLOCKS 4
+#endif
+#ifndef PCCP_NE_MIN_BLOCKS
+#define PCCP_NE_MIN_BLOCKS 6
+#endif
+template <int F>
+struct MaxThreads<WarpGroup, F> {
   static constexpr int value = 256;
-  static constexpr int min_blocks = 4;
+  static constexpr int min_blocks = F == kNeOnly ? PCCP_NE_MIN_BLOCKS : PCCP_WARP_MIN_BLOCKS;
 };
 
 // ---- K1: batched fixed points (run_sequential on N independent stores) ---------
-template <class G, bool TS>
-__global__ void __launch_bounds__(MaxThreads<G>::value, MaxThreads<G>::min_blocks) k_propagate(Model M, int* stores, int n, int stride, unsigned char* status, unsigned* rounds,
+template <class G, bool TS, int F>
+__global__ void __launch_bounds__(MaxThreads<G, F>::value, MaxThreads<G, F>::min_blocks) k_propagate(Model M, int* stores, int n, int stride, unsigned char* status, unsigned* rounds,
                             int fold) {
   const Frame f = frame(M);
   const G g = GroupOf<G>::make(f);
@@ -264,7 +284,7 @@ __global__ void __launch_bounds__(MaxThreads<G>::value, MaxThreads<G>::min_block
       g.sync();
     }
     int r = 0;
-    const bool failed = propagate(g, S, sb, tab, M.L, r);
+    const bool failed = propagate<G, TS, F>(g, S, sb, tab, M.L, r);
     copy_out(g, io, S, (int)M.L.n_words);
     if (g.rank() == 0) {
       status[i] = failed ? 1 : 0;
@@ -275,15 +295,15 @@ __global__ void __launch_bounds__(MaxThreads<G>::value, MaxThreads<G>::min_block
 }
 
 // ---- the problem root: fold, objective, fixed point, classification ----------------
-template <class G, bool TS>
-__global__ void __launch_bounds__(MaxThreads<G>::value, MaxThreads<G>::min_blocks) k_root(Model M, SearchCtl C, int* store, unsigned char* flag) {
+template <class G, bool TS, int F>
+__global__ void __launch_bounds__(MaxThreads<G, F>::value, MaxThreads<G, F>::min_blocks) k_root(Model M, SearchCtl C, int* store, unsigned char* flag) {
   const Frame f = frame(M);
   const G g = GroupOf<G>::make(f);
   const Tab<TS> tab = make_tab<TS>(f);
   if (GroupOf<G>::in_cta() != 0 || blockIdx.x != 0) return;
   volatile int* S = f.stores;
   const unsigned sb = init_store(g, S, M.L);
-  Cnt cnt;
+  Cnt& cnt = f.cnt[GroupOf<G>::in_cta()];
   copy_words(g, S, store, (int)M.L.n_words);
   g.sync();
   apply_fold(g, S, f.T, M.L);
@@ -291,8 +311,8 @@ __global__ void __launch_bounds__(MaxThreads<G>::value, MaxThreads<G>::min_block
   join_objective(g, S, M.L, C);
   g.sync();
   int r = 0;
-  const bool failed = propagate(g, S, sb, tab, M.L, r);
-  if (C.count) {
+  const bool failed = propagate<G, TS, F>(g, S, sb, tab, M.L, r);
+  if (C.count && g.rank() == 0) {
     ++cnt.nodes;
     cnt.rounds += (unsigned long long)r;
   }
@@ -308,8 +328,8 @@ __global__ void __launch_bounds__(MaxThreads<G>::value, MaxThreads<G>::min_block
 // ---- K5: one level of the EPS decomposition (decompose, solver.cpp:180-213) ------
 // Parent p's children go to slots 2p (left, x <= mid) and 2p+1 (right); the
 // compaction below keeps BFS order, so the frontier is identical on every GPU.
-template <class G, bool TS>
-__global__ void __launch_bounds__(MaxThreads<G>::value, MaxThreads<G>::min_blocks) k_expand(Model M, SearchCtl C, const int* parents, const int* parent_idx, int n_par, int stride,
+template <class G, bool TS, int F>
+__global__ void __launch_bounds__(MaxThreads<G, F>::value, MaxThreads<G, F>::min_blocks) k_expand(Model M, SearchCtl C, const int* parents, const int* parent_idx, int n_par, int stride,
                          int child_depth, int* children, unsigned char* flags) {
   const Frame f = frame(M);
   const G g = GroupOf<G>::make(f);
@@ -319,7 +339,7 @@ __global__ void __launch_bounds__(MaxThreads<G>::value, MaxThreads<G>::min_block
   const int gid = blockIdx.x * GroupOf<G>::per_cta() + GroupOf<G>::in_cta();
   const int ng = gridDim.x * GroupOf<G>::per_cta();
   const DeviceLayout& L = M.L;
-  Cnt cnt;
+  Cnt& cnt = f.cnt[GroupOf<G>::in_cta()];
   for (int p = gid; p < n_par; p += ng) {
     if (time_stop(g, C)) {  // abandoned parent: its subtree is unexplored
       if (g.rank() == 0) {
@@ -351,8 +371,8 @@ __global__ void __launch_bounds__(MaxThreads<G>::value, MaxThreads<G>::min_block
         dirty |= join_objective(g, S, L, C);
         g.sync();
         int r = 0;
-        const bool failed = propagate(g, S, sb, tab, L, r, dirty);
-        if (C.count) {
+        const bool failed = propagate<G, TS, F>(g, S, sb, tab, L, r, dirty);
+        if (C.count && g.rank() == 0) {
           ++cnt.nodes;
           cnt.rounds += (unsigned long long)r;
           if ((unsigned long long)child_depth > cnt.maxd) cnt.maxd = (unsigned long long)child_depth;
@@ -484,8 +504,8 @@ __device__ __forceinline__ void maybe_donate(const G& g, const SearchParams& P, 
 // solver.cpp:122-146).  A branching node pushes (its fixed point, right
 // decision) and descends left in place; a leaf pops.  When the queue is
 // empty, idle groups are fed by donations (maybe_donate).
-template <class G, bool TS>
-__global__ void __launch_bounds__(MaxThreads<G>::value, MaxThreads<G>::min_blocks) k_search(Model M, SearchCtl C, SearchParams P) {
+template <class G, bool TS, int F>
+__global__ void __launch_bounds__(MaxThreads<G, F>::value, MaxThreads<G, F>::min_blocks) k_search(Model M, SearchCtl C, SearchParams P) {
   const Frame f = frame(M);
   const G g = GroupOf<G>::make(f);
   const Tab<TS> tab = make_tab<TS>(f);
@@ -496,7 +516,7 @@ __global__ void __launch_bounds__(MaxThreads<G>::value, MaxThreads<G>::min_block
   const int nw = (int)L.n_words;
   int* stk = P.stack_pool + (size_t)gid * (size_t)P.stack_depth * (size_t)P.entry_stride;
   Globals* Gl = C.G;
-  Cnt cnt;
+  Cnt& cnt = f.cnt[GroupOf<G>::in_cta()];
   bool queue_open = true;
   const bool right_first = P.value_order == 1 || (P.value_order == 2 && (gid & 1));
   for (;;) {
@@ -568,10 +588,12 @@ __global__ void __launch_bounds__(MaxThreads<G>::value, MaxThreads<G>::min_block
           break;
         }
         int r = 0;
-        const bool failed = propagate(g, S, sb, tab, L, r, dirty);
-        ++cnt.nodes;
-        cnt.rounds += (unsigned long long)r;
-        if ((unsigned long long)depth > cnt.maxd) cnt.maxd = (unsigned long long)depth;
+        const bool failed = propagate<G, TS, F>(g, S, sb, tab, L, r, dirty);
+        if (g.rank() == 0) {
+          ++cnt.nodes;
+          cnt.rounds += (unsigned long long)r;
+          if ((unsigned long long)depth > cnt.maxd) cnt.maxd = (unsigned long long)depth;
+        }
         e = classify(g, S, f.T, L, C, cnt, failed, depth, lbw, mid);
       } else {
         e = branch(g, S, f.T, L, lbw, mid);
