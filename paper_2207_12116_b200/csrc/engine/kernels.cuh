@@ -290,7 +290,7 @@ __device__ __forceinline__ unsigned long long eval_ne(unsigned sb, int4 q) {
   const unsigned wx = (unsigned)q.x >> 2, wy = (unsigned)q.w >> 2;
   const unsigned ax = sb + (unsigned)q.x, ay = sb + (unsigned)q.w;
   const int lx = sld(ax), ux = sld(ax + 4), ly = sld(ay), uy = sld(ay + 4);
-  const int a = q.y, b = q.z;
+  const int a = q.y + 1, b = q.z + 1;
   unsigned long long m = 0;
   auto bit = [](unsigned w) { return 1ull << (w & 63u); };  // any bit flags a change past 64 words
   if (small30(lx) & small30(ux) & small30(ly) & small30(uy)) {
@@ -323,21 +323,53 @@ __device__ __forceinline__ unsigned long long eval_ne(unsigned sb, int4 q) {
 // eval_ne when the host's value-range analysis (ne_fast_ok, lower.cpp) has
 // proved every value read stays inside (-2^30, 2^30): the 32-bit path is then
 // exact with no range checks, and (lb, ub) pairs load as one 8-byte word.
+//
+// With A = a - 1, B = b - 1 (the table's form): x + a <= y is entailed iff
+// ub x + A < lb y, i.e. v3 < lb y; y + b <= x iff v1 < lb x.  The joins need
+// no return value: a candidate that beats the round's snapshot proves the
+// word changed during this round (it was worse when read and is no worse than
+// the candidate after the join), and every change comes from such a join, so
+// "some candidate beat its snapshot" flags exactly the rounds that changed a
+// word — the flag the fixed-point loop needs.
+// Joins without a return value.  When any of a record's four candidates
+// beats its snapshot, all four are issued, the others as the join identity
+// (min with INT_MAX, max with INT_MIN): one branch region per record
+// instead of one per join.
+__device__ __forceinline__ void sred_min(unsigned a, int v) {
+  asm volatile("red.shared.min.s32 [%0], %1;" ::"r"(a), "r"(v) : "memory");
+}
+__device__ __forceinline__ void sred_max(unsigned a, int v) {
+  asm volatile("red.shared.max.s32 [%0], %1;" ::"r"(a), "r"(v) : "memory");
+}
 __device__ __forceinline__ bool eval_ne_fast(unsigned sb, int4 q) {
   const unsigned ax = sb + (unsigned)q.x, ay = sb + (unsigned)q.w;
   const int2 X = sld2(ax), Y = sld2(ay);
-  const int a = q.y, b = q.z;
-  const bool g1 = X.y - Y.x <= -a, g2 = Y.y - X.x <= -b;
-  const int v1 = Y.y + b - 1, v2 = X.x + 1 - b, v3 = X.y + a - 1, v4 = Y.x + 1 - a;
+  const int A = q.y, B = q.z;
+  const int v1 = Y.y + B, v2 = X.x - B, v3 = X.y + A, v4 = Y.x - A;
+  const bool g1 = v3 < Y.x, g2 = v1 < X.x;
   const bool c1 = g1 & (v1 < X.y), c2 = g1 & (v2 > Y.x), c3 = g2 & (v3 < Y.y), c4 = g2 & (v4 > X.x);
-  bool ch = false;
-  if (c1 | c2 | c3 | c4) {
-    if (c1 && satom_min(ax + 4, v1) > v1) ch = true;
-    if (c2 && satom_max(ay, v2) < v2) ch = true;
-    if (c3 && satom_min(ay + 4, v3) > v3) ch = true;
-    if (c4 && satom_max(ax, v4) < v4) ch = true;
+  const bool any = c1 | c2 | c3 | c4;
+  if (any) {
+    sred_min(ax + 4, c1 ? v1 : INT_MAX);
+    sred_max(ay, c2 ? v2 : INT_MIN);
+    sred_min(ay + 4, c3 ? v3 : INT_MAX);
+    sred_max(ax, c4 ? v4 : INT_MIN);
   }
-  return ch;
+  return any;
+}
+
+// One eventless round over the NE records (loop bounds held in registers).
+template <class G, bool TS>
+__device__ __forceinline__ bool ne_round(const G& g, unsigned sb, const Tab<TS>& tab, const DeviceLayout& L) {
+  const int n = (int)L.n_ne;
+  const unsigned off = L.ne;
+  unsigned ch = 0;
+  if (L.ne_fast) {
+    for (int i = g.rank(); i < n; i += g.size()) ch |= (unsigned)eval_ne_fast(sb, tab.ld4(off, i));
+  } else {
+    for (int i = g.rank(); i < n; i += g.size()) ch |= eval_ne(sb, tab.ld4(off, i)) != 0ull;
+  }
+  return ch != 0;
 }
 
 // Fused reification b <-> (x + p <= y and y + q <= x): the 11 commands of
@@ -660,12 +692,7 @@ __device__ bool propagate(const G& g, volatile int* S, unsigned sb, const Tab<TS
   int r = 0;
   bool failed = false;
   for (;;) {
-    bool ch = false, fl = false;
-    if (L.ne_fast) {
-      for (int i = g.rank(); i < (int)L.n_ne; i += g.size()) ch |= eval_ne_fast(sb, tab.ld4(L.ne, i));
-    } else {
-      for (int i = g.rank(); i < (int)L.n_ne; i += g.size()) ch |= eval_ne(sb, tab.ld4(L.ne, i)) != 0ull;
-    }
+    bool ch = ne_round(g, sb, tab, L), fl = false;
     if constexpr (F == kAllFamilies) ch |= eval_other_families(g, S, sb, tab, L);
     for (int i = g.rank(); i < (int)L.n_iv; i += g.size()) {
       const int w = T[L.iv_lb + i];

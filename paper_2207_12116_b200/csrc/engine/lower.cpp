@@ -519,11 +519,11 @@ Lowered lower_model(const pccp_model& m) {
   L.ne = reserve_arr(4 * L.n_ne);
   L.ne_even = 1;
   std::int64_t ne_k = 0;
-  for (std::uint32_t i = 0; i < L.n_ne; ++i) {  // {4 lbx, a, b, 4 lby}: byte offsets into the store
+  for (std::uint32_t i = 0; i < L.n_ne; ++i) {  // {4 lbx, a - 1, b - 1, 4 lby}: byte offsets into the store
     const std::uint32_t lx = static_cast<std::uint32_t>(nes[i].x) & 0xffffu, ly = static_cast<std::uint32_t>(nes[i].x) >> 16;
     B[L.ne + 4 * i + 0] = static_cast<std::int32_t>(4 * lx);
-    B[L.ne + 4 * i + 1] = nes[i].a;
-    B[L.ne + 4 * i + 2] = nes[i].b;
+    B[L.ne + 4 * i + 1] = nes[i].a - 1;
+    B[L.ne + 4 * i + 2] = nes[i].b - 1;
     B[L.ne + 4 * i + 3] = static_cast<std::int32_t>(4 * ly);
     if ((lx | ly) & 1u) L.ne_even = 0;
     ne_k = std::max({ne_k, std::abs(std::int64_t{nes[i].a}), std::abs(std::int64_t{nes[i].b})});

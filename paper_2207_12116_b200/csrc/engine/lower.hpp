@@ -38,7 +38,7 @@ struct DeviceLayout {
   std::uint32_t zero_word;               // constant-zero word Z = n_words (store_stride > n_words)
   // Fused not(and(x + a <= y, y + b <= x)) groups: the 4 commands compile_rec
   // emits for it (propagation.cpp:350-360) read and write only lb/ub of x and y.
-  std::uint32_t ne, n_ne;                // int4 {4 lbx, a, b, 4 lby} (byte offsets of the lb words)
+  std::uint32_t ne, n_ne;                // int4 {4 lbx, a - 1, b - 1, 4 lby} (byte offsets of the lb words)
   std::uint32_t ne_even;                 // every NE lb word is even: (lb, ub) is one 8-byte load
   std::uint32_t ne_k;                    // max |a|, |b| over the NE records, + 1
   // Fused compile_reified(b, and(x + p <= y, y + q <= x)): the 11 commands of
