@@ -124,12 +124,18 @@ struct pccp_gpu_ctx {
 
   int groups() const { return ctas * (warp ? gpc : 1); }
 
-  dev::Model model(int var_order = 0, unsigned var_seed = 0, bool ne_fast = false) const {
+  // Per-launch layout: branching order, and the value-range analyses of the
+  // input stores (lower.cpp ne_fast_ok / rows_fast_ok) that admit the 32-bit
+  // paths (PCCP_NO_FAST=1 disables both, for parity tests).
+  dev::Model model(int var_order = 0, unsigned var_seed = 0, const std::int32_t* stores = nullptr,
+                   std::size_t n_stores = 0, std::size_t stride = 0) const {
     dev::Model M;
     M.L = low.L;
     M.L.var_order = (std::uint32_t)var_order;
     M.L.var_seed = var_seed;
-    M.L.ne_fast = ne_fast && !std::getenv("PCCP_NO_NE_FAST") ? 1u : 0u;
+    const bool fast = stores && n_stores && !std::getenv("PCCP_NO_FAST") && !std::getenv("PCCP_NO_NE_FAST");
+    M.L.ne_fast = fast && ne_fast_ok(low, stores, n_stores, stride) ? 1u : 0u;
+    M.L.rows_fast = fast && rows_fast_ok(low, stores, n_stores, stride) ? 1u : 0u;
     M.blob = blob.p;
     M.table_in_smem = table_in_smem;
     M.store_stride = store_stride;
@@ -277,7 +283,7 @@ void run_search(pccp_gpu_ctx* c, int mode, const int32_t* root_words, int depth_
   const int shard_count = std::max(1, c->cfg.shard_count);
   const int shard_index = c->cfg.shard_index;
   if (shard_index < 0 || shard_index >= shard_count) throw ArgError("shard_index out of range");
-  const dev::Model M = c->model(var_order, var_seed, ne_fast_ok(c->low, root_words, 1, (size_t)nw));
+  const dev::Model M = c->model(var_order, var_seed, root_words, 1, (size_t)nw);
   dev::SearchCtl C{};
   C.G = c->G;
   C.n_peers = mode == 1 ? c->n_peers : 0;
@@ -629,7 +635,7 @@ int pccp_gpu_propagate_batch(pccp_gpu_ctx* c, const int32_t* in, uint32_t n, int
     c->st.ensure(n);
     c->rnd.ensure(n);
     if (nw) CK(cudaMemcpyAsync(c->io.p, in, (size_t)n * nw * 4, cudaMemcpyHostToDevice, c->stream));
-    const dev::Model M = c->model(0, 0, ne_fast_ok(c->low, in, n, nw));
+    const dev::Model M = c->model(0, 0, in, n, nw);
     const int per = c->warp ? c->gpc : 1;
     const int grid = (int)std::min<long long>(c->ctas, ((long long)n + per - 1) / per);
     dispatch(c, [&]<class Gp, bool TS, int F>() {

@@ -518,8 +518,59 @@ __device__ __forceinline__ bool eval_small(volatile int* S, const int* __restric
 // instruction touches b_{i,j} for a few i and many consecutive j — stride-2
 // words, ~2-way bank conflicts — instead of one column b_{.,j} (n words
 // apart: a single bank when n = 32).
+//
+// L.rows_fast (rows_fast_ok on the host): every term reads a word that only
+// constant tells write, bounded so that sums and guards stay inside
+// (-2^29, 2^29): the same rows in plain 32-bit arithmetic, no sentinel tests.
+// An overloaded row (cell = +inf) makes every zeroing guard hold, as tv(1,
+// +inf) does in the widened form.
+template <class G, bool TS>
+__device__ bool eval_rows_fast(const G& g, unsigned sb, const Tab<TS>& tab, const DeviceLayout& L) {
+  const int R = (int)L.row_lanes;
+  const int sub = g.rank() & (R - 1);
+  const int per_pass = g.size() / R;
+  const int my = g.rank() / R;
+  const int n_rows = (int)L.n_rows;
+  const unsigned off_row = L.row_off, off_terms = L.row_terms, off_c = L.row_c, off_lsum = L.row_lsum;
+  unsigned ch = 0;
+  for (int base = 0; base < n_rows; base += per_pass) {
+    const int row = base + my;
+    const bool act = row < n_rows;
+    int s = 0;
+    int beg = 0, end = 0;
+    if (act) {
+      beg = tab.ld1(off_row, row);
+      end = tab.ld1(off_row, row + 1);
+      for (int j = beg + sub; j < end; j += R) {
+        const int x = tab.ld1(off_terms, j);
+        s += tcoef(x) * sld(sb + ((unsigned)tword(x) << 2));
+      }
+    }
+    for (int o = R >> 1; o > 0; o >>= 1) s += __shfl_xor_sync(kFull, s, o, R);
+    if (act) {
+      const int c = tab.ld1(off_c, row);
+      const bool over = s > c;
+      const int cell = over ? INT_MAX : s;  // [lsum > c] => lsum <- +inf
+      if (sub == 0) ch |= sjoin_max(sb + ((unsigned)tab.ld1(off_lsum, row) << 2), cell);
+      if (c != INT_MAX) {
+        for (int j = beg + sub; j < end; j += R) {
+          const int x = tab.ld1(off_terms, j);
+          const int coef = tcoef(x);
+          const unsigned a = sb + ((unsigned)tword(x) << 2);
+          if (over || coef + s - coef * sld(a) > c) {
+            ch |= sjoin_max(a, 0);
+            ch |= sjoin_min(a + 4, 0);
+          }
+        }
+      }
+    }
+  }
+  return ch != 0;
+}
+
 template <class G, bool TS>
 __device__ bool eval_rows(const G& g, unsigned sb, const Tab<TS>& tab, const DeviceLayout& L) {
+  if (L.rows_fast) return eval_rows_fast(g, sb, tab, L);
   const int R = (int)L.row_lanes;
   const int sub = g.rank() & (R - 1);
   const int per_pass = g.size() / R;

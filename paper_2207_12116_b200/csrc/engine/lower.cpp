@@ -158,6 +158,25 @@ Lowered lower_model(const pccp_model& m) {
 
   const std::vector<CmdP> cmds = parse(m);
 
+  // Words joined only with finite constants (value-range analysis for the
+  // rows' 32-bit path, rows_fast_ok): such a word only ever holds its start
+  // value or one of those constants.
+  std::vector<std::uint8_t> nonconst(m.n_words, 0);
+  std::int64_t const_kmax = 0;
+  for (const CmdP& c : cmds) {
+    auto part = [&](const std::optional<Expr>& e, std::uint32_t w) {
+      if (!e || w >= m.n_words) return;
+      if (!e->terms.empty() || e->k == INT32_MIN || e->k == INT32_MAX) nonconst[w] = 1;
+      else const_kmax = std::max(const_kmax, std::abs(std::int64_t{e->k}));
+    };
+    if (c.kind == PCCP_INTERVAL) {
+      part(c.lb, c.tw);
+      part(c.ub, c.tw + 1);
+    } else {
+      part(c.sc, c.tw);
+    }
+  }
+
   // B_alg of SURVEY 8(d): 4*(guard terms) + 4*(fn terms + target words).
   {
     double total = 0;
@@ -663,6 +682,30 @@ Lowered lower_model(const pccp_model& m) {
     }
     B[L.row_off + L.n_rows] = static_cast<std::int32_t>(t);
   }
+  // Rows whose terms all read constant-only words can be summed in 32 bits
+  // once the start values are known to be small (rows_fast_ok).
+  {
+    bool ok = L.n_rows > 0;
+    std::int64_t abs_max = 0;
+    std::vector<std::uint8_t> seen(m.n_words, 0);
+    for (const Row& r : rows) {
+      std::int64_t sum = 0;
+      for (std::int32_t x : r.terms) {
+        const std::uint32_t w = static_cast<std::uint32_t>(x) & kTermWordMask;
+        const std::int32_t coef = x >> kTermWordBits;
+        if (w >= m.n_words || nonconst[w]) ok = false;
+        else if (!seen[w]) {
+          seen[w] = 1;
+          out.row_words.push_back(w);
+        }
+        sum += std::abs(std::int64_t{coef}) + 1;  // + 1: the zeroing guard's own coef
+      }
+      abs_max = std::max(abs_max, sum);
+    }
+    out.rows_const = ok;
+    out.row_abs_max = abs_max;
+    out.const_kmax = const_kmax;
+  }
   L.hot_words = static_cast<std::uint32_t>(B.size());
 
   L.n_fold = static_cast<std::uint32_t>(fold_w.size());
@@ -761,6 +804,27 @@ bool ne_fast_ok(const Lowered& low, const std::int32_t* stores, std::size_t n_st
   }
   const std::int64_t reach = bound + 1 + (4 * std::int64_t{L.n_ne} + 1) * std::int64_t{L.ne_k};
   return reach < (std::int64_t{1} << 29);
+}
+
+bool rows_fast_ok(const Lowered& low, const std::int32_t* stores, std::size_t n_stores, std::size_t stride) {
+  const DeviceLayout& L = low.L;
+  if (!low.rows_const || L.n_rows == 0) return false;
+  const std::uint32_t nw = L.n_words;
+  std::vector<std::int32_t> w(nw);
+  std::int64_t bound = low.const_kmax;
+  for (std::size_t s = 0; s < n_stores; ++s) {
+    std::copy(stores + s * stride, stores + s * stride + nw, w.begin());
+    for (std::uint32_t i = 0; i < L.n_fold; ++i) {
+      const std::int32_t wf = low.blob[L.fold_w + i], v = low.blob[L.fold_v + i];
+      std::int32_t& x = w[static_cast<std::uint32_t>(wf) & 0x7fffffffu];
+      x = wf < 0 ? std::max(x, v) : std::min(x, v);
+    }
+    for (std::uint32_t r : low.row_words) {
+      if (w[r] == INT32_MIN || w[r] == INT32_MAX) return false;
+      bound = std::max(bound, std::abs(std::int64_t{w[r]}));
+    }
+  }
+  return low.row_abs_max * (bound + 1) < (std::int64_t{1} << 29);
 }
 
 void host_join_decision(const pccp_model& m, std::int32_t* words, const pccp_decision& d) {

@@ -72,6 +72,7 @@ struct DeviceLayout {
   std::uint32_t var_order;  // set per launch: 0 first-fail (branch, solver.cpp:19-47), 1-3 smallest lb
   std::uint32_t var_seed;   // set per launch: var_order 3 tie-break seed
   std::uint32_t ne_fast;    // set per launch: value-range analysis proved the 32-bit NE path exact
+  std::uint32_t rows_fast;  // set per launch: the same for the sum rows (rows_fast_ok)
 };
 
 
@@ -81,6 +82,11 @@ struct Lowered {
   std::uint32_t n_dropped = 0;  // commands that can never fire (guard rhs = +inf with '>')
   double alg_bytes_per_eval = 0;  // SURVEY 8(d) B_alg over the reference commands
   std::vector<std::uint8_t> word_up;
+  // value-range analysis of the rows (rows_fast_ok)
+  bool rows_const = false;              // every row term reads a constant-only word
+  std::int64_t row_abs_max = 0;         // max over rows of sum(|coef| + 1)
+  std::int64_t const_kmax = 0;          // max |k| over the constant joins
+  std::vector<std::uint32_t> row_words; // the words the rows read
   std::vector<std::int32_t> slot_of_word;  // for diagnostics
 };
 
@@ -92,6 +98,12 @@ Lowered lower_model(const pccp_model& m);
 // bounded so that no NE evaluation can leave (-2^30, 2^30), i.e. the range
 // checks and the widened path of eval_ne can be skipped exactly.
 bool ne_fast_ok(const Lowered& low, const std::int32_t* stores, std::size_t n_stores, std::size_t stride);
+
+// The same for the fused sum rows (DeviceLayout::rows_fast): every row term
+// reads a word that only constant tells write, so its value is a start value
+// or one of those constants; with those bounded, every row sum and zeroing
+// guard fits in (-2^29, 2^29) and eval_rows can sum in 32 bits exactly.
+bool rows_fast_ok(const Lowered& low, const std::int32_t* stores, std::size_t n_stores, std::size_t stride);
 
 // Host-side join of a decision into a store (Decision::as_join +
 // Store::join_in_place on an Interval, solver.hpp:20-23, store.cpp:51-63).

@@ -171,6 +171,48 @@ def test_ne_fast_path_finite_boxes(n, shift, engine):
             assert np.array_equal(w, wo) and np.array_equal(w2, wo)
 
 
+@pytest.mark.parametrize("seed", [1, 3])
+def test_rows_fast_path_random_boxes(seed, engine):
+    """RCPSP30 stores with random start windows and random 0/1 overlap booleans
+    (after the init tells): the rows' 32-bit path (rows_fast_ok) and the
+    widened path (PCCP_NO_FAST) both equal the C oracle, fixed point and
+    failure; a store with an unbounded boolean must take the widened path."""
+    import os
+    m = build(f"rcpsp30_s{seed}")
+    t = m.tables()
+    o = Oracle(t)
+    engine.load(m)
+    root = o.run_sequential(m.bottom())[1]
+    starts = set(int(t.slot_word[s]) for s in m.starts())
+    rng = np.random.default_rng(seed)
+    stores = []
+    sw = sorted(starts)
+    for k in range(64):
+        s = root.copy()
+        for w in rng.choice(sw, size=int(rng.integers(1, 8)), replace=False):
+            lo, hi = int(s[w]), int(s[w + 1])
+            a = int(rng.integers(lo, min(hi, lo + 10) + 1))
+            b = int(rng.integers(a, min(hi, a + 12) + 1))
+            s[w], s[w + 1] = a, b
+        for w in range(0, t.n_words, 2):
+            if w not in starts and s[w] == 0 and s[w + 1] == 1 and rng.random() < 0.003:
+                v = int(rng.integers(0, 2))
+                s[w], s[w + 1] = v, v
+        stores.append(s)
+    out, failed, _ = engine.propagate_batch(np.stack(stores))
+    os.environ["PCCP_NO_FAST"] = "1"
+    try:
+        out2, failed2, _ = engine.propagate_batch(np.stack(stores))
+    finally:
+        del os.environ["PCCP_NO_FAST"]
+    assert failed.any() and not failed.all()
+    for s, w, w2, f, f2 in zip(stores, out, out2, failed, failed2):
+        fo, wo, _, _ = o.run_sequential(s)
+        assert f == fo == f2
+        if not f:
+            assert np.array_equal(w, wo) and np.array_equal(w2, wo)
+
+
 @pytest.mark.parametrize("n", [8, 10])
 def test_enumerate_nqueens_without_fast_path(n, golden):
     import os
