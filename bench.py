@@ -357,9 +357,17 @@ def main():
     local = env_int("LOCAL_RANK", 0)
     if world != a.gpus:
         raise SystemExit(f"--gpus {a.gpus} but WORLD_SIZE={world}")
+    # PCCP_BENCH_SHARE_DEVICE=1 (tests only): every rank on cuda:0 over gloo, to
+    # exercise the N>1 path (sharding, IPC incumbents, max-over-ranks) on a 1-GPU box
+    shared = os.environ.get("PCCP_BENCH_SHARE_DEVICE") == "1"
+    if shared:
+        local = 0
     torch.cuda.set_device(local)
     if world > 1:
-        dist.init_process_group("nccl", device_id=torch.device(f"cuda:{local}"))
+        if shared:
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=torch.device(f"cuda:{local}"))
 
     def barrier():
         if world > 1:
@@ -369,7 +377,7 @@ def main():
     def allreduce(vals, op):
         if world == 1:
             return vals
-        t = torch.tensor(vals, dtype=torch.float64, device=f"cuda:{local}")
+        t = torch.tensor(vals, dtype=torch.float64, device="cpu" if shared else f"cuda:{local}")
         dist.all_reduce(t, op=op)
         return t.tolist()
 
