@@ -274,6 +274,44 @@ def cpu_large(threads, budget_s):
             "workers": threads}
 
 
+def enumeration_configs(local, rank, world, dist, cpu, threads):
+    """Configs 1 and 3 beside the headline: N-Queens 8 and the random linear CSP
+    (seed 1, depth cap 22), full trees, counts and hash-sums checked against the
+    reference's; the reference itself on the host for comparison."""
+    from paper_2207_12116_b200 import Engine
+    from paper_2207_12116_b200.distributed import combine_enum, _gather
+    cases = [("nqueens8-all-solutions", dict(n=8, depth=-1),
+              dict(nodes=779, failures=298, solutions=92, hash_sum=0xF1DF80A1FF36FBF6)),
+             ("random-linear-csp-seed1-depth22", WORKLOADS["csp"], WORKLOADS["csp"]["expect"])]
+    out = {}
+    for name, w, exp in cases:
+        m = build_model(w)
+        with Engine(local, shard_index=rank, shard_count=world) as eng:
+            eng.load(m)
+            for _ in range(3):
+                r = eng.enumerate(depth_cap=w["depth"])
+            runs = []
+            for _ in range(5):
+                runs.append(eng.enumerate(depth_cap=w["depth"]))
+        with Engine(local, shard_index=rank, shard_count=world, hash=True) as heng:
+            hr = heng.load(m).enumerate(depth_cap=w["depth"])
+        if world > 1:
+            hr = combine_enum(_gather(hr))
+            ms = [max(_gather(r["device_ms"])) for r in runs]
+            nodes = combine_enum(_gather(runs[-1]))["nodes"]
+        else:
+            ms = [r["device_ms"] for r in runs]
+            nodes = runs[-1]["nodes"]
+        d = {"nodes": nodes, "device_ms": statistics.median(ms), "nodes_per_s": nodes / (statistics.median(ms) / 1e3),
+             "parity": all(int(hr[k]) == v for k, v in exp.items())}
+        if cpu:
+            c = cpu_reference(dict(w, workload=name), 3.0, threads)
+            d["cpu_reference"] = {"nodes_per_s": c["value"], "threads": c["cores"], "kind": c["kind"],
+                                  "sample": f"{c['seconds']:.2f} s"}
+        out[name] = d
+    return out
+
+
 def _gather_obj(dist, v):
     out = [None] * dist.get_world_size()
     dist.all_gather_object(out, v)
@@ -451,6 +489,8 @@ def main():
         heng.close()
 
     tto = None if a.no_tto else time_to_optimum(local, rank, world, dist)
+    others = None if a.no_tto else enumeration_configs(local, rank, world, dist,
+                                                       world == 1 and not a.no_cpu_baseline, os.cpu_count() or 1)
     stretch, large = (None, None) if a.no_tto else stretch_and_large(local, rank, world, dist, a.stretch_timeout,
                                                                      a.large_timeout)
 
@@ -516,6 +556,8 @@ def main():
         if world == 1 and not a.no_cpu_baseline:
             tto["cpu_reference"] = cpu_time_to_optimum(os.cpu_count() or 1)
         line["time_to_optimum"] = tto
+    if others is not None:
+        line["other_configs"] = others
     if stretch is not None:
         line["stretch"] = stretch
         if world == 1 and not a.no_cpu_baseline:
