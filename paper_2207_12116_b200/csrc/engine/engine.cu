@@ -125,7 +125,7 @@ struct pccp_gpu_ctx {
   int groups() const { return ctas * (warp ? gpc : 1); }
 
   // Per-launch layout: branching order, and the value-range analyses of the
-  // input stores (lower.cpp ne_fast_ok / rows_fast_ok) that admit the 32-bit
+  // input stores (lower.cpp fast_paths) that admit the 32-bit
   // paths (PCCP_NO_FAST=1 disables both, for parity tests).
   dev::Model model(int var_order = 0, unsigned var_seed = 0, const std::int32_t* stores = nullptr,
                    std::size_t n_stores = 0, std::size_t stride = 0) const {
@@ -133,9 +133,10 @@ struct pccp_gpu_ctx {
     M.L = low.L;
     M.L.var_order = (std::uint32_t)var_order;
     M.L.var_seed = var_seed;
-    const bool fast = stores && n_stores && !std::getenv("PCCP_NO_FAST") && !std::getenv("PCCP_NO_NE_FAST");
-    M.L.ne_fast = fast && ne_fast_ok(low, stores, n_stores, stride) ? 1u : 0u;
-    M.L.rows_fast = fast && rows_fast_ok(low, stores, n_stores, stride) ? 1u : 0u;
+    bool ne = false, rows = false;
+    if (!std::getenv("PCCP_NO_FAST")) fast_paths(low, stores, n_stores, stride, ne, rows);
+    M.L.ne_fast = ne && !std::getenv("PCCP_NO_NE_FAST") ? 1u : 0u;
+    M.L.rows_fast = rows ? 1u : 0u;
     M.blob = blob.p;
     M.table_in_smem = table_in_smem;
     M.store_stride = store_stride;

@@ -320,7 +320,7 @@ __device__ __forceinline__ unsigned long long eval_ne(unsigned sb, int4 q) {
   return m;
 }
 
-// eval_ne when the host's value-range analysis (ne_fast_ok, lower.cpp) has
+// eval_ne when the host's value-range analysis (fast_paths, lower.cpp) has
 // proved every value read stays inside (-2^30, 2^30): the 32-bit path is then
 // exact with no range checks, and (lb, ub) pairs load as one 8-byte word.
 //
@@ -519,9 +519,9 @@ __device__ __forceinline__ bool eval_small(volatile int* S, const int* __restric
 // words, ~2-way bank conflicts — instead of one column b_{.,j} (n words
 // apart: a single bank when n = 32).
 //
-// L.rows_fast (rows_fast_ok on the host): every term reads a word that only
-// constant tells write, bounded so that sums and guards stay inside
-// (-2^29, 2^29): the same rows in plain 32-bit arithmetic, no sentinel tests.
+// L.rows_fast (fast_paths on the host): every term reads a word whose values
+// the value-range analysis bounds, so that sums and guards stay inside
+// (-2^30, 2^30): the same rows in plain 32-bit arithmetic, no sentinel tests.
 // An overloaded row (cell = +inf) makes every zeroing guard hold, as tv(1,
 // +inf) does in the widened form.
 template <class G, bool TS>

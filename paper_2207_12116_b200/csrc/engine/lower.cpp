@@ -158,23 +158,60 @@ Lowered lower_model(const pccp_model& m) {
 
   const std::vector<CmdP> cmds = parse(m);
 
-  // Words joined only with finite constants (value-range analysis for the
-  // rows' 32-bit path, rows_fast_ok): such a word only ever holds its start
-  // value or one of those constants.
-  std::vector<std::uint8_t> nonconst(m.n_words, 0);
-  std::int64_t const_kmax = 0;
+  // Value-range classes of the words (lower.hpp, fast_paths):
+  //   0: written only by finite constant tells — holds its entry value or a constant;
+  //   1: an interval bound written only by constants and affine tells (k +- one
+  //      word whose class is <= 1): NE, reification and precedence tells;
+  //   2: anything else (sums, scaled terms, sentinel constants, scalar cells
+  //      written affinely, generic code).
+  std::vector<std::uint8_t>& cls = out.word_cls;
+  cls.assign(m.n_words, 0);
+  std::vector<std::vector<std::uint32_t>> aff_src(m.n_words);
+  std::vector<std::uint8_t>& read_fast = out.word_read_fast;
+  read_fast.assign(m.n_words, 0);
   for (const CmdP& c : cmds) {
-    auto part = [&](const std::optional<Expr>& e, std::uint32_t w) {
+    auto part = [&](const std::optional<Expr>& e, std::uint32_t w, bool interval) {
       if (!e || w >= m.n_words) return;
-      if (!e->terms.empty() || e->k == INT32_MIN || e->k == INT32_MAX) nonconst[w] = 1;
-      else const_kmax = std::max(const_kmax, std::abs(std::int64_t{e->k}));
+      if (e->terms.empty()) {
+        if (e->k == INT32_MIN || e->k == INT32_MAX) cls[w] = 2;
+        else out.kconst = std::max(out.kconst, std::abs(std::int64_t{e->k}));
+      } else if (interval && e->terms.size() == 1 && std::abs(e->terms[0].first) == 1 &&
+                 e->k != INT32_MIN && e->k != INT32_MAX && e->terms[0].second < m.n_words) {
+        cls[w] = std::max<std::uint8_t>(cls[w], 1);
+        aff_src[w].push_back(e->terms[0].second);
+        read_fast[e->terms[0].second] = 1;
+        out.kaff = std::max(out.kaff, std::abs(std::int64_t{e->k}));
+        ++out.r_aff;
+      } else {
+        cls[w] = 2;
+      }
     };
     if (c.kind == PCCP_INTERVAL) {
-      part(c.lb, c.tw);
-      part(c.ub, c.tw + 1);
+      part(c.lb, c.tw, true);
+      part(c.ub, c.tw + 1, true);
     } else {
-      part(c.sc, c.tw);
+      part(c.sc, c.tw, false);
     }
+  }
+  for (bool changed = true; changed;) {  // an affine word reading an unbounded word is unbounded
+    changed = false;
+    for (std::uint32_t w = 0; w < m.n_words; ++w) {
+      if (cls[w] != 1) continue;
+      for (std::uint32_t src : aff_src[w]) {
+        if (cls[src] == 2) {
+          cls[w] = 2;
+          changed = true;
+          break;
+        }
+      }
+    }
+  }
+  out.word_partner.assign(m.n_words, -1);
+  for (std::uint32_t sl = 0; sl < m.n_slots; ++sl) {
+    if (m.slot_kind[sl] != PCCP_INTERVAL) continue;
+    const std::uint32_t w = m.slot_word[sl];
+    out.word_partner[w] = static_cast<std::int32_t>(w + 1);
+    out.word_partner[w + 1] = static_cast<std::int32_t>(w);
   }
 
   // B_alg of SURVEY 8(d): 4*(guard terms) + 4*(fn terms + target words).
@@ -537,7 +574,6 @@ Lowered lower_model(const pccp_model& m) {
   L.n_ne = static_cast<std::uint32_t>(nes.size());
   L.ne = reserve_arr(4 * L.n_ne);
   L.ne_even = 1;
-  std::int64_t ne_k = 0;
   for (std::uint32_t i = 0; i < L.n_ne; ++i) {  // {4 lbx, a - 1, b - 1, 4 lby}: byte offsets into the store
     const std::uint32_t lx = static_cast<std::uint32_t>(nes[i].x) & 0xffffu, ly = static_cast<std::uint32_t>(nes[i].x) >> 16;
     B[L.ne + 4 * i + 0] = static_cast<std::int32_t>(4 * lx);
@@ -545,9 +581,7 @@ Lowered lower_model(const pccp_model& m) {
     B[L.ne + 4 * i + 2] = nes[i].b - 1;
     B[L.ne + 4 * i + 3] = static_cast<std::int32_t>(4 * ly);
     if ((lx | ly) & 1u) L.ne_even = 0;
-    ne_k = std::max({ne_k, std::abs(std::int64_t{nes[i].a}), std::abs(std::int64_t{nes[i].b})});
   }
-  L.ne_k = static_cast<std::uint32_t>(std::min<std::int64_t>(ne_k + 1, 1 << 30));
   // Order the reifications x-major: a warp then reads one x (broadcast) and
   // consecutive y / b words (2-way bank conflicts).  RCPSP compiles them
   // j-major (rcpsp.cpp:241-242), which puts b_ij of a warp n words apart —
@@ -682,29 +716,34 @@ Lowered lower_model(const pccp_model& m) {
     }
     B[L.row_off + L.n_rows] = static_cast<std::int32_t>(t);
   }
-  // Rows whose terms all read constant-only words can be summed in 32 bits
-  // once the start values are known to be small (rows_fast_ok).
+  // Rows whose terms all read class <= 1 words can be summed in 32 bits once
+  // the entry values are known to be small (fast_paths).
   {
     bool ok = L.n_rows > 0;
-    std::int64_t abs_max = 0;
-    std::vector<std::uint8_t> seen(m.n_words, 0);
     for (const Row& r : rows) {
-      std::int64_t sum = 0;
+      std::int64_t s0 = 0, s1 = 0;
       for (std::int32_t x : r.terms) {
         const std::uint32_t w = static_cast<std::uint32_t>(x) & kTermWordMask;
-        const std::int32_t coef = x >> kTermWordBits;
-        if (w >= m.n_words || nonconst[w]) ok = false;
-        else if (!seen[w]) {
-          seen[w] = 1;
-          out.row_words.push_back(w);
+        const std::int64_t coef = std::abs(std::int64_t{x >> kTermWordBits});
+        if (w >= m.n_words || cls[w] == 2) {
+          ok = false;
+          continue;
         }
-        sum += std::abs(std::int64_t{coef}) + 1;  // + 1: the zeroing guard's own coef
+        read_fast[w] = 1;
+        (cls[w] == 0 ? s0 : s1) += coef;
       }
-      abs_max = std::max(abs_max, sum);
+      out.row_sum0.push_back(s0);
+      out.row_sum1.push_back(s1);
     }
-    out.rows_const = ok;
-    out.row_abs_max = abs_max;
-    out.const_kmax = const_kmax;
+    out.rows_ok = ok;
+  }
+  out.ne_ok = L.n_ne > 0 && L.ne_even;
+  for (std::uint32_t i = 0; i < L.n_ne && out.ne_ok; ++i) {
+    for (std::uint32_t o : {0u, 3u}) {
+      const std::uint32_t lbw = static_cast<std::uint32_t>(B[L.ne + 4 * i + o]) / 4;
+      if (cls[lbw] == 2 || cls[lbw + 1] == 2) out.ne_ok = false;
+      read_fast[lbw] = read_fast[lbw + 1] = 1;
+    }
   }
   L.hot_words = static_cast<std::uint32_t>(B.size());
 
@@ -778,18 +817,22 @@ Lowered lower_model(const pccp_model& m) {
   return out;
 }
 
-bool ne_fast_ok(const Lowered& low, const std::int32_t* stores, std::size_t n_stores, std::size_t stride) {
+// The value-range analysis at run time.  Outside a failed round every
+// interval stays inside its entry box (lb only rises, ub only falls), so at
+// every round start a class-1 word is bounded by B1, the largest entry value
+// of the intervals it belongs to; a class-0 word holds its entry value or a
+// constant (B0).  Inside a round a class-1 value is an entry value plus one
+// affine offset (<= kaff) per link of a dependency chain of affine joins, and
+// a round performs at most r_aff of them: |v| <= max(B0, B1) + r_aff * kaff.
+// Decisions and the objective bound stay inside the box (+-1).
+void fast_paths(const Lowered& low, const std::int32_t* stores, std::size_t n_stores, std::size_t stride,
+                bool& ne_fast, bool& rows_fast) {
+  ne_fast = rows_fast = false;
+  if ((!low.ne_ok && !low.rows_ok) || !stores || !n_stores) return;
   const DeviceLayout& L = low.L;
-  if (!L.ne_even || L.n_ne == 0) return false;
-  if (L.n_reif || L.n_unit1 || L.n_unit2 || L.n_small || L.n_rows || L.n_gen || L.n_sc || L.filtered) return false;
-  // Start values: a store joined with the fold tells.  Outside a failed round
-  // every interval stays inside its start box (lb only rises, ub only falls);
-  // inside a round a value is a start value plus at most one NE offset per
-  // join of a dependency chain, and a round makes <= 4 * n_ne joins.  The
-  // objective and decision joins stay inside the box (+-1).
   const std::uint32_t nw = L.n_words;
   std::vector<std::int32_t> w(nw);
-  std::int64_t bound = 0;
+  std::int64_t b0 = low.kconst, b1 = 0;
   for (std::size_t s = 0; s < n_stores; ++s) {
     std::copy(stores + s * stride, stores + s * stride + nw, w.begin());
     for (std::uint32_t i = 0; i < L.n_fold; ++i) {
@@ -798,33 +841,30 @@ bool ne_fast_ok(const Lowered& low, const std::int32_t* stores, std::size_t n_st
       x = wf < 0 ? std::max(x, v) : std::min(x, v);
     }
     for (std::uint32_t i = 0; i < nw; ++i) {
-      if (w[i] == INT32_MIN || w[i] == INT32_MAX) return false;
-      bound = std::max(bound, std::abs(std::int64_t{w[i]}));
+      const std::uint8_t c = low.word_cls[i];
+      if (c == 2 || !(low.word_read_fast[i] || c == 1)) continue;
+      auto finite = [](std::int32_t v) { return v != INT32_MIN && v != INT32_MAX; };
+      if (c == 0) {
+        if (!finite(w[i])) return;
+        b0 = std::max(b0, std::abs(std::int64_t{w[i]}));
+      } else {  // class 1: the interval's box must be finite on both sides
+        const std::int32_t p = low.word_partner[i];
+        if (p < 0 || !finite(w[i]) || !finite(w[static_cast<std::uint32_t>(p)])) return;
+        b1 = std::max({b1, std::abs(std::int64_t{w[i]}), std::abs(std::int64_t{w[static_cast<std::uint32_t>(p)]})});
+      }
     }
   }
-  const std::int64_t reach = bound + 1 + (4 * std::int64_t{L.n_ne} + 1) * std::int64_t{L.ne_k};
-  return reach < (std::int64_t{1} << 29);
-}
-
-bool rows_fast_ok(const Lowered& low, const std::int32_t* stores, std::size_t n_stores, std::size_t stride) {
-  const DeviceLayout& L = low.L;
-  if (!low.rows_const || L.n_rows == 0) return false;
-  const std::uint32_t nw = L.n_words;
-  std::vector<std::int32_t> w(nw);
-  std::int64_t bound = low.const_kmax;
-  for (std::size_t s = 0; s < n_stores; ++s) {
-    std::copy(stores + s * stride, stores + s * stride + nw, w.begin());
-    for (std::uint32_t i = 0; i < L.n_fold; ++i) {
-      const std::int32_t wf = low.blob[L.fold_w + i], v = low.blob[L.fold_v + i];
-      std::int32_t& x = w[static_cast<std::uint32_t>(wf) & 0x7fffffffu];
-      x = wf < 0 ? std::max(x, v) : std::min(x, v);
-    }
-    for (std::uint32_t r : low.row_words) {
-      if (w[r] == INT32_MIN || w[r] == INT32_MAX) return false;
-      bound = std::max(bound, std::abs(std::int64_t{w[r]}));
-    }
+  const std::int64_t lim = std::int64_t{1} << 30;
+  const std::int64_t bound1 = std::max(b0, b1) + 1 + low.r_aff * low.kaff;
+  if (bound1 >= lim) return;
+  ne_fast = low.ne_ok && bound1 + low.kaff + 2 < lim;
+  if (low.rows_ok) {
+    // |sum| <= S; the zeroing guard coef + sum - coef * v is <= 2 S + |coef|
+    std::int64_t worst = 0;
+    for (std::size_t r = 0; r < low.row_sum0.size(); ++r)
+      worst = std::max(worst, low.row_sum0[r] * (b0 + 1) + low.row_sum1[r] * bound1);
+    rows_fast = 3 * worst + 3 < lim;
   }
-  return low.row_abs_max * (bound + 1) < (std::int64_t{1} << 29);
 }
 
 void host_join_decision(const pccp_model& m, std::int32_t* words, const pccp_decision& d) {

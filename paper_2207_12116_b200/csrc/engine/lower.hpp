@@ -40,7 +40,6 @@ struct DeviceLayout {
   // emits for it (propagation.cpp:350-360) read and write only lb/ub of x and y.
   std::uint32_t ne, n_ne;                // int4 {4 lbx, a - 1, b - 1, 4 lby} (byte offsets of the lb words)
   std::uint32_t ne_even;                 // every NE lb word is even: (lb, ub) is one 8-byte load
-  std::uint32_t ne_k;                    // max |a|, |b| over the NE records, + 1
   // Fused compile_reified(b, and(x + p <= y, y + q <= x)): the 11 commands of
   // propagation.cpp:415-431 over lb/ub of x, y and b (RCPSP overlaps).
   std::uint32_t reif, n_reif;            // int4 {lbx | lby << 16, lbb, p, q}
@@ -72,7 +71,7 @@ struct DeviceLayout {
   std::uint32_t var_order;  // set per launch: 0 first-fail (branch, solver.cpp:19-47), 1-3 smallest lb
   std::uint32_t var_seed;   // set per launch: var_order 3 tie-break seed
   std::uint32_t ne_fast;    // set per launch: value-range analysis proved the 32-bit NE path exact
-  std::uint32_t rows_fast;  // set per launch: the same for the sum rows (rows_fast_ok)
+  std::uint32_t rows_fast;  // set per launch: the same for the sum rows (fast_paths)
 };
 
 
@@ -82,28 +81,26 @@ struct Lowered {
   std::uint32_t n_dropped = 0;  // commands that can never fire (guard rhs = +inf with '>')
   double alg_bytes_per_eval = 0;  // SURVEY 8(d) B_alg over the reference commands
   std::vector<std::uint8_t> word_up;
-  // value-range analysis of the rows (rows_fast_ok)
-  bool rows_const = false;              // every row term reads a constant-only word
-  std::int64_t row_abs_max = 0;         // max over rows of sum(|coef| + 1)
-  std::int64_t const_kmax = 0;          // max |k| over the constant joins
-  std::vector<std::uint32_t> row_words; // the words the rows read
+  // value-range analysis (fast_paths)
+  std::vector<std::uint8_t> word_cls;        // 0 constant-only, 1 affine interval bound, 2 unbounded
+  std::vector<std::uint8_t> word_read_fast;  // read by a row term, an NE record or an affine tell
+  std::vector<std::int32_t> word_partner;    // the other bound of an interval word, -1 for scalars
+  std::int64_t kconst = 0, kaff = 0;         // max |k| over constant / affine tells
+  std::int64_t r_aff = 0;                    // affine tells per round (one per command part)
+  bool rows_ok = false, ne_ok = false;       // every row term / NE word has class <= 1
+  std::vector<std::int64_t> row_sum0, row_sum1;  // per row: sum |coef| over class-0 / class-1 terms
   std::vector<std::int32_t> slot_of_word;  // for diagnostics
 };
 
 // Throws std::runtime_error (mapped to PCCP_EMODEL) on malformed tables.
 Lowered lower_model(const pccp_model& m);
 
-// Value-range analysis for NE-only models (engine.cu sets DeviceLayout::ne_fast):
-// true when every store in `stores` (after the fold tells) is finite and
-// bounded so that no NE evaluation can leave (-2^30, 2^30), i.e. the range
-// checks and the widened path of eval_ne can be skipped exactly.
-bool ne_fast_ok(const Lowered& low, const std::int32_t* stores, std::size_t n_stores, std::size_t stride);
-
-// The same for the fused sum rows (DeviceLayout::rows_fast): every row term
-// reads a word that only constant tells write, so its value is a start value
-// or one of those constants; with those bounded, every row sum and zeroing
-// guard fits in (-2^29, 2^29) and eval_rows can sum in 32 bits exactly.
-bool rows_fast_ok(const Lowered& low, const std::int32_t* stores, std::size_t n_stores, std::size_t stride);
+// Value-range analysis for the exact 32-bit paths (engine.cu sets
+// DeviceLayout::ne_fast / rows_fast per launch from the input stores): true
+// when no NE evaluation can read a value outside (-2^30, 2^30), resp. every
+// row sum and zeroing guard fits in 32 bits.  lower.cpp states the argument.
+void fast_paths(const Lowered& low, const std::int32_t* stores, std::size_t n_stores, std::size_t stride,
+                bool& ne_fast, bool& rows_fast);
 
 // Host-side join of a decision into a store (Decision::as_join +
 // Store::join_in_place on an Interval, solver.hpp:20-23, store.cpp:51-63).
