@@ -745,11 +745,21 @@ __device__ bool propagate(const G& g, volatile int* S, unsigned sb, const Tab<TS
   for (;;) {
     bool ch = ne_round(g, sb, tab, L), fl = false;
     if constexpr (F == kAllFamilies) ch |= eval_other_families(g, S, sb, tab, L);
-    for (int i = g.rank(); i < (int)L.n_iv; i += g.size()) {
-      const int w = T[L.iv_lb + i];
-      fl |= S[w] > S[w + 1];
+    // The scan may see an intermediate state: failure is monotone, and a join
+    // after it changed a word, so the next round scans again (H8).
+    if (L.iv_dense) {
+      const int n_iv = (int)L.n_iv;
+      for (int i = g.rank(); i < n_iv; i += g.size()) {
+        const int2 v = sld2(sb + 8u * (unsigned)i);
+        fl |= v.x > v.y;
+      }
+    } else {
+      for (int i = g.rank(); i < (int)L.n_iv; i += g.size()) {
+        const unsigned a = sb + 4u * (unsigned)tab.ld1(L.iv_lb, i);
+        fl |= sld(a) > sld(a + 4);
+      }
+      for (int i = g.rank(); i < (int)L.n_sc; i += g.size()) fl |= S[T[L.sc_w + i]] == T[L.sc_top + i];
     }
-    for (int i = g.rank(); i < (int)L.n_sc; i += g.size()) fl |= S[T[L.sc_w + i]] == T[L.sc_top + i];
     bool any_ch, any_fl;
     g.round_end(ch, fl, any_ch, any_fl, r);
     ++r;
