@@ -112,11 +112,10 @@ struct pccp_gpu_ctx {
   int table_in_smem = 0;
   int ne_only = 0;  // lowered to NE records (and fold tells) only: the kNeOnly kernels
 
-  DBuf<int> fa, fb, ia, ib, stack, best, io, mailbox, waitq;
+  DBuf<int> fa, fb, ia, ib, stack, best, io, mailbox, waitq, dec;
   DBuf<unsigned char> flags, st;
   DBuf<unsigned> rnd;
   dev::Globals* G = nullptr;
-  int* d_count = nullptr;
   std::vector<void*> opened;
   DBuf<int*> d_peers;
   int n_peers = 0;
@@ -297,7 +296,9 @@ void run_search(pccp_gpu_ctx* c, int mode, const int32_t* root_words, int depth_
   C.best_store = c->best.p;
 
   reset_globals(c, lim, keep_incumbent, stall_ns);
-  c->fa.ensure((size_t)stride);
+  // the root store is frontier buffer 0 of the decomposition (capacity 2*target)
+  const long long target_cap = (long long)(c->cfg.eps_factor > 0 ? c->cfg.eps_factor : 8) * c->groups() * shard_count;
+  c->fa.ensure((size_t)stride * (size_t)std::max<long long>(1, std::min<long long>(2 * target_cap, 1ll << 29)));
   c->ia.ensure(1);
   c->flags.ensure(2);
   std::vector<std::int32_t> root(root_words, root_words + nw);
@@ -316,37 +317,58 @@ void run_search(pccp_gpu_ctx* c, int mode, const int32_t* root_words, int depth_
   out.d2h += 1 + (std::uint64_t)nw * 4;
 
   // EPS decomposition: whole BFS levels until the frontier holds target nodes.
+  // Levels are enqueued in batches without host round trips: each level's
+  // size lives on the device (dev::DecState) and a level past the target is a
+  // no-op; level L reads ping-pong buffer L&1 and writes (L+1)&1.  Children of
+  // fewer than `target` parents need at most 2*target slots.
   const int eps = c->cfg.eps_factor > 0 ? c->cfg.eps_factor : 8;
-  const long long target = (long long)eps * c->groups() * shard_count;
+  const long long target_ll = (long long)eps * c->groups() * shard_count;
+  if (target_ll > (1ll << 28)) throw LimitError("EPS target too large");
+  const int target = (int)target_ll;
   int count = rflag ? 1 : 0;
   int level = 0;
-  c->d_count = nullptr;
-  DBuf<int> dcount;
-  dcount.ensure(1);
-  while (count > 0 && count < target) {
-    dev::Globals probe;
-    CK(cudaMemcpyAsync(&probe.stop, &c->G->stop, sizeof(int), cudaMemcpyDeviceToHost, c->stream));
-    CK(cudaStreamSynchronize(c->stream));
-    if (probe.stop == 2) break;
-    const size_t nchild = 2 * (size_t)count;
-    c->fb.ensure(nchild * stride);
-    c->ib.ensure(nchild);
-    c->flags.ensure(nchild);
-    const int grid = (int)std::min<long long>(c->ctas, (count + (c->warp ? c->gpc : 1) - 1) / (c->warp ? c->gpc : 1));
-    dev::k_expand<Gp, TS, F><<<grid, c->block, c->smem, c->stream>>>(M, C, c->fa.p, c->ia.p, count, stride, level + 1,
-                                                                c->fb.p, c->flags.p);
-    CK(cudaGetLastError());
-    dev::k_compact<<<1, 1024, 0, c->stream>>>(c->flags.p, (int)nchild, c->ib.p, dcount.p);
-    CK(cudaGetLastError());
-    c->launches += 2;
-    CK(cudaMemcpyAsync(&count, dcount.p, 4, cudaMemcpyDeviceToHost, c->stream));
-    CK(cudaStreamSynchronize(c->stream));
-    out.d2h += 8;
-    std::swap(c->fa, c->fb);
-    std::swap(c->ia, c->ib);
-    ++level;
+  if (count > 0 && count < target) {
+    c->fb.ensure(2 * (size_t)target * stride);
+    c->ib.ensure(2 * (size_t)target);
+    c->ia.ensure(2 * (size_t)target);  // may reallocate: index 0 of the root frontier is rewritten
+    CK(cudaMemcpyAsync(c->ia.p, &zero, 4, cudaMemcpyHostToDevice, c->stream));
+    c->flags.ensure(2 * (size_t)target);
+    c->dec.ensure(2);
+    const dev::DecState st0{count, 0};
+    CK(cudaMemcpyAsync(c->dec.p, &st0, sizeof(st0), cudaMemcpyHostToDevice, c->stream));
+    dev::DecState* d_st = reinterpret_cast<dev::DecState*>(c->dec.p);
+    int* FB[2] = {c->fa.p, c->fb.p};
+    int* IB[2] = {c->ia.p, c->ib.p};
+    const int per = c->warp ? c->gpc : 1;
+    const int grid = (int)std::min<long long>(c->ctas, (target + per - 1) / per);
+    int enq = 0;  // levels enqueued
+    for (;;) {
+      const int batch = enq < 8 ? 4 : 2;  // early levels are tiny; later ones are checked sooner
+      for (int b = 0; b < batch; ++b, ++enq) {
+        const int src = enq & 1, dst = src ^ 1;
+        dev::k_expand<Gp, TS, F><<<grid, c->block, c->smem, c->stream>>>(M, C, FB[src], IB[src], d_st, target, stride,
+                                                                         FB[dst], c->flags.p);
+        CK(cudaGetLastError());
+        dev::k_compact<<<1, 1024, 0, c->stream>>>(c->flags.p, IB[dst], d_st, C, target);
+        CK(cudaGetLastError());
+        c->launches += 2;
+      }
+      dev::DecState st;
+      int stop = 0;
+      CK(cudaMemcpyAsync(&st, d_st, sizeof(st), cudaMemcpyDeviceToHost, c->stream));
+      CK(cudaMemcpyAsync(&stop, &c->G->stop, sizeof(int), cudaMemcpyDeviceToHost, c->stream));
+      CK(cudaStreamSynchronize(c->stream));
+      out.d2h += sizeof(st) + 4;
+      count = st.count;
+      level = st.levels;
+      if (count <= 0 || count >= target || stop == 2 || level < enq) break;
+    }
+    // the final frontier is in buffer level & 1
+    if (level & 1) {
+      std::swap(c->fa, c->fb);
+      std::swap(c->ia, c->ib);
+    }
   }
-  dcount.release();
   CK(cudaEventRecord(c->ev[1], c->stream));
   CK(cudaMemcpyAsync(&out.bfs_rounds, &c->G->rounds, 8, cudaMemcpyDeviceToHost, c->stream));
   CK(cudaStreamSynchronize(c->stream));
@@ -535,6 +557,7 @@ void pccp_gpu_close(pccp_gpu_ctx* c) {
   c->stack.release();
   c->mailbox.release();
   c->waitq.release();
+  c->dec.release();
   c->best.release();
   c->io.release();
   c->flags.release();

@@ -328,9 +328,27 @@ __global__ void __launch_bounds__(MaxThreads<G, F>::value, MaxThreads<G, F>::min
 // ---- K5: one level of the EPS decomposition (decompose, solver.cpp:180-213) ------
 // Parent p's children go to slots 2p (left, x <= mid) and 2p+1 (right); the
 // compaction below keeps BFS order, so the frontier is identical on every GPU.
+// The level's size and depth come from the device (DecState, written by the
+// previous k_compact), so the host can enqueue several levels without a
+// round trip; a level whose frontier is empty or already has `target` nodes,
+// or that follows a model error, is a no-op (and so is every later one).
+struct DecState {
+  int count;   // current frontier size
+  int levels;  // levels expanded so far
+};
+
+__device__ __forceinline__ bool dec_done(const DecState* st, const SearchCtl& C, int target) {
+  const int n = *(volatile const int*)&st->count;
+  return n <= 0 || n >= target || *(volatile const int*)&C.G->stop == 2;
+}
+
 template <class G, bool TS, int F>
-__global__ void __launch_bounds__(MaxThreads<G, F>::value, MaxThreads<G, F>::min_blocks) k_expand(Model M, SearchCtl C, const int* parents, const int* parent_idx, int n_par, int stride,
-                         int child_depth, int* children, unsigned char* flags) {
+__global__ void __launch_bounds__(MaxThreads<G, F>::value, MaxThreads<G, F>::min_blocks) k_expand(Model M, SearchCtl C, const int* parents, const int* parent_idx, const DecState* st, int target, int stride,
+                         int* children, unsigned char* flags) {
+  if (dec_done(st, C, target)) return;
+  const int n_par = st->count;
+  const int child_depth = st->levels + 1;
+  if ((int)blockIdx.x * GroupOf<G>::per_cta() >= n_par) return;  // no parent for this CTA
   const Frame f = frame(M);
   const G g = GroupOf<G>::make(f);
   const Tab<TS> tab = make_tab<TS>(f);
@@ -395,9 +413,11 @@ __global__ void __launch_bounds__(MaxThreads<G, F>::value, MaxThreads<G, F>::min
 }
 
 // Stable compaction of the child flags into the next frontier's index list.
-__global__ void k_compact(const unsigned char* flags, int n, int* idx, int* count) {
+__global__ void k_compact(const unsigned char* flags, int* idx, DecState* st, SearchCtl C, int target) {
   __shared__ int wsum[32];
   __shared__ int base;
+  if (dec_done(st, C, target)) return;
+  const int n = 2 * st->count;
   const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
   if (tid == 0) base = 0;
   __syncthreads();
@@ -423,7 +443,10 @@ __global__ void k_compact(const unsigned char* flags, int n, int* idx, int* coun
     if (tid == 0) base += wsum[31];
     __syncthreads();
   }
-  if (tid == 0) *count = base;
+  if (tid == 0) {
+    st->count = base;
+    st->levels += 1;
+  }
 }
 
 __global__ void k_init_clock(Globals* G) { G->t0 = globaltimer(); }

@@ -349,3 +349,18 @@ def test_unsat_below_healthy_root(engine):
     failed, _, _ = engine.run_sequential()
     assert not failed
     assert engine.solve().status == "UNSAT"
+
+
+@pytest.mark.parametrize("dom_hi", [100, 10**6, 10**8, 2**30])
+def test_value_range_analysis_large_domains(dom_hi, hengine):
+    """Random linear CSPs whose domains grow until the value-range analysis must
+    refuse the 32-bit row path (|sum| would pass 2^30) and then past the
+    reference's own 2^30 fast range: depth-capped enumeration counts and
+    hash-sums equal the C oracle's in every case."""
+    from paper_2207_12116_b200 import Model
+    m = Model.random_csp(5, n_vars=40, n_cons=120, dom_hi=dom_hi)
+    t = m.tables()
+    want = Oracle(t).enumerate(m.bottom(), depth_cap=9)
+    got = hengine.load(m).enumerate(depth_cap=9)
+    for k in ("nodes", "failures", "solutions", "open_leaves", "hash_sum"):
+        assert got[k] == want[k], (dom_hi, k, got[k], want[k])
