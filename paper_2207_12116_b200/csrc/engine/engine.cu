@@ -319,29 +319,44 @@ void run_search(pccp_gpu_ctx* c, int mode, const int32_t* root_words, int depth_
   // EPS decomposition: whole BFS levels until the frontier holds target nodes.
   // Levels are enqueued in batches without host round trips: each level's
   // size lives on the device (dev::DecState) and a level past the target is a
-  // no-op; level L reads ping-pong buffer L&1 and writes (L+1)&1.  Children of
-  // fewer than `target` parents need at most 2*target slots.
+  // no-op; within a phase, level L reads ping-pong buffer L&1 and writes
+  // (L+1)&1.  Children of fewer than `target` parents need 2*target slots.
+  //
+  // With N shards the decomposition has two phases.  Phase A is identical on
+  // every GPU (counted on shard 0 only) and stops at `groups * N` nodes; each
+  // GPU keeps the positions i = shard (mod N) of that frontier, and phase B
+  // expands only those (counted by their owner) to `eps * groups` nodes.  So
+  // each GPU expands its own share, not the whole job's frontier, and every
+  // tree node is still materialised exactly once across the GPUs.
   const int eps = c->cfg.eps_factor > 0 ? c->cfg.eps_factor : 8;
-  const long long target_ll = (long long)eps * c->groups() * shard_count;
-  if (target_ll > (1ll << 28)) throw LimitError("EPS target too large");
-  const int target = (int)target_ll;
+  const long long target_ll = (long long)eps * c->groups();
+  const long long target_a_ll = shard_count > 1 ? (long long)c->groups() * shard_count : 0;
+  if (std::max(target_ll, target_a_ll) > (1ll << 28)) throw LimitError("EPS target too large");
   int count = rflag ? 1 : 0;
   int level = 0;
-  if (count > 0 && count < target) {
-    c->fb.ensure(2 * (size_t)target * stride);
-    c->ib.ensure(2 * (size_t)target);
-    c->ia.ensure(2 * (size_t)target);  // may reallocate: index 0 of the root frontier is rewritten
+  const int cap = (int)std::max(target_ll, target_a_ll);
+  if (count > 0) {
+    c->fb.ensure(2 * (size_t)cap * stride);
+    c->ib.ensure(2 * (size_t)cap);
+    c->ia.ensure(2 * (size_t)cap);  // may reallocate: index 0 of the root frontier is rewritten
     CK(cudaMemcpyAsync(c->ia.p, &zero, 4, cudaMemcpyHostToDevice, c->stream));
-    c->flags.ensure(2 * (size_t)target);
+    c->flags.ensure(2 * (size_t)cap);
     c->dec.ensure(2);
-    const dev::DecState st0{count, 0};
+  }
+  dev::DecState* d_st = reinterpret_cast<dev::DecState*>(c->dec.p);
+  const int per = c->warp ? c->gpc : 1;
+  // Expand the frontier in (fa, ia) until it holds `target` nodes; the result
+  // is left in (fa, ia).  Returns false after a model error.
+  auto expand_until = [&](int target) -> bool {
+    if (count <= 0 || count >= target) return true;
+    const dev::DecState st0{count, level};
     CK(cudaMemcpyAsync(c->dec.p, &st0, sizeof(st0), cudaMemcpyHostToDevice, c->stream));
-    dev::DecState* d_st = reinterpret_cast<dev::DecState*>(c->dec.p);
     int* FB[2] = {c->fa.p, c->fb.p};
     int* IB[2] = {c->ia.p, c->ib.p};
-    const int per = c->warp ? c->gpc : 1;
     const int grid = (int)std::min<long long>(c->ctas, (target + per - 1) / per);
-    int enq = 0;  // levels enqueued
+    const int level0 = level;
+    int enq = 0;  // levels enqueued in this phase
+    int stop = 0;
     for (;;) {
       const int batch = enq < 8 ? 4 : 2;  // early levels are tiny; later ones are checked sooner
       for (int b = 0; b < batch; ++b, ++enq) {
@@ -354,20 +369,35 @@ void run_search(pccp_gpu_ctx* c, int mode, const int32_t* root_words, int depth_
         c->launches += 2;
       }
       dev::DecState st;
-      int stop = 0;
       CK(cudaMemcpyAsync(&st, d_st, sizeof(st), cudaMemcpyDeviceToHost, c->stream));
       CK(cudaMemcpyAsync(&stop, &c->G->stop, sizeof(int), cudaMemcpyDeviceToHost, c->stream));
       CK(cudaStreamSynchronize(c->stream));
       out.d2h += sizeof(st) + 4;
       count = st.count;
       level = st.levels;
-      if (count <= 0 || count >= target || stop == 2 || level < enq) break;
+      if (count <= 0 || count >= target || stop == 2 || level - level0 < enq) break;
     }
-    // the final frontier is in buffer level & 1
-    if (level & 1) {
+    if ((level - level0) & 1) {  // the frontier is in buffer (levels of this phase) & 1
       std::swap(c->fa, c->fb);
       std::swap(c->ia, c->ib);
     }
+    return stop != 2;
+  };
+  if (shard_count > 1) {
+    if (expand_until((int)target_a_ll) && count > 0) {
+      const int mine = count > shard_index ? (count - shard_index + shard_count - 1) / shard_count : 0;
+      if (mine > 0) {
+        dev::k_shard_filter<<<(mine + 255) / 256, 256, 0, c->stream>>>(c->ia.p, c->ib.p, shard_index, shard_count, mine);
+        CK(cudaGetLastError());
+        ++c->launches;
+        std::swap(c->ia, c->ib);
+      }
+      count = mine;
+      C.count = 1;  // phase B and the search: every node below here is this GPU's alone
+      expand_until((int)target_ll);
+    }
+  } else {
+    expand_until((int)target_ll);
   }
   CK(cudaEventRecord(c->ev[1], c->stream));
   CK(cudaMemcpyAsync(&out.bfs_rounds, &c->G->rounds, 8, cudaMemcpyDeviceToHost, c->stream));
@@ -387,8 +417,8 @@ void run_search(pccp_gpu_ctx* c, int mode, const int32_t* root_words, int depth_
     P.n_frontier = count;
     P.stride = stride;
     P.depth0 = level;
-    P.shard_index = shard_index;
-    P.shard_count = shard_count;
+    P.shard_index = 0;  // the frontier is already this GPU's share (phase B)
+    P.shard_count = 1;
     P.stack_pool = c->stack.p;
     P.stack_depth = dmax;
     P.entry_stride = entry;

@@ -449,6 +449,12 @@ __global__ void k_compact(const unsigned char* flags, int* idx, DecState* st, Se
   }
 }
 
+// Positions shard + k * shards of the shared frontier's index list.
+__global__ void k_shard_filter(const int* idx, int* out, int shard, int shards, int n_out) {
+  const int k = blockIdx.x * blockDim.x + threadIdx.x;
+  if (k < n_out) out[k] = idx[shard + k * shards];
+}
+
 __global__ void k_init_clock(Globals* G) { G->t0 = globaltimer(); }
 
 struct SearchParams {
