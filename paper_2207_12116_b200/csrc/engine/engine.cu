@@ -7,6 +7,7 @@
 #include <cmath>
 #include <cstddef>
 #include <cstdlib>
+#include <cstdio>
 #include <cstring>
 #include <stdexcept>
 #include <string>
@@ -375,6 +376,8 @@ void run_search(pccp_gpu_ctx* c, int mode, const int32_t* root_words, int depth_
       out.d2h += sizeof(st) + 4;
       count = st.count;
       level = st.levels;
+      if (std::getenv("PCCP_DEBUG_DEC"))
+        fprintf(stderr, "dec batch: enq=%d level=%d count=%d t=%.3f ms\n", enq, level, count, now_ms() - t_start);
       if (count <= 0 || count >= target || stop == 2 || level - level0 < enq) break;
     }
     if ((level - level0) & 1) {  // the frontier is in buffer (levels of this phase) & 1

@@ -185,16 +185,42 @@ struct Frame {
   int* stores;
 };
 
+// The command tables are staged into shared memory by the bulk-copy engine
+// (cp.async.bulk, TMA's 1-D form): thread 0 arms an mbarrier with the byte
+// count and issues the copies; the CTA sets up the rest meanwhile and waits
+// on the barrier's phase 0.
+__device__ __forceinline__ void stage_table(const int* blob, int* dst, unsigned bytes) {
+  __shared__ __align__(8) unsigned long long tbar;
+  const unsigned mb = (unsigned)__cvta_generic_to_shared(&tbar);
+  const unsigned sd = (unsigned)__cvta_generic_to_shared(dst);
+  if (threadIdx.x == 0) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(mb) : "memory");
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(mb), "r"(bytes) : "memory");
+    constexpr unsigned kChunk = 32768;
+    for (unsigned o = 0; o < bytes; o += kChunk) {
+      const unsigned n = bytes - o < kChunk ? bytes - o : kChunk;
+      asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+                   ::"r"(sd + o), "l"(reinterpret_cast<const char*>(blob) + o), "r"(n), "r"(mb)
+                   : "memory");
+    }
+  }
+  __syncthreads();  // the barrier is initialised before anyone waits on it
+  asm volatile(
+      "{\n .reg .pred done;\n WAIT_%=:\n"
+      " mbarrier.try_wait.parity.shared::cta.b64 done, [%0], 0;\n"
+      " @!done bra WAIT_%=;\n}" ::"r"(mb)
+      : "memory");
+}
+
 __device__ __forceinline__ Frame frame(const Model& M) {
   extern __shared__ __align__(16) int smem[];
   Frame f;
   int off = 0;
   f.T = M.blob;
   if (M.table_in_smem) {
-    const int4* src = reinterpret_cast<const int4*>(M.blob);
-    int4* dst = reinterpret_cast<int4*>(smem);
     const int n4 = ((int)M.L.blob_words + 3) >> 2;
-    for (int i = threadIdx.x; i < n4; i += blockDim.x) dst[i] = src[i];
+    stage_table(M.blob, smem, (unsigned)n4 * 16u);
     f.T = smem;
     off = n4 * 4;
   }
