@@ -112,8 +112,9 @@ struct pccp_gpu_ctx {
   int store_stride = 4;
   int table_in_smem = 0;
   int ne_only = 0;  // lowered to NE records (and fold tells) only: the kNeOnly kernels
+  int dec_ctas = 0;  // grid of the persistent decomposition kernel
 
-  DBuf<int> fa, fb, ia, ib, stack, best, io, mailbox, waitq, dec;
+  DBuf<int> fa, fb, ia, ib, stack, best, io, mailbox, waitq, dec, chunk;
   DBuf<unsigned char> flags, st;
   DBuf<unsigned> rnd;
   dev::Globals* G = nullptr;
@@ -151,7 +152,7 @@ template <class Gp, bool TS, int F>
 void set_smem_attrs(size_t smem) {
   CK(cudaFuncSetAttribute(dev::k_propagate<Gp, TS, F>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   CK(cudaFuncSetAttribute(dev::k_root<Gp, TS, F>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-  CK(cudaFuncSetAttribute(dev::k_expand<Gp, TS, F>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  CK(cudaFuncSetAttribute(dev::k_decompose<Gp, TS, F>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   CK(cudaFuncSetAttribute(dev::k_search<Gp, TS, F>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
 }
 
@@ -159,6 +160,13 @@ template <class Gp, bool TS, int F>
 int occupancy(int block, size_t smem) {
   int occ = 0;
   CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, dev::k_search<Gp, TS, F>, block, smem));
+  return occ;
+}
+
+template <class Gp, bool TS, int F>
+int occupancy_decompose(int block, size_t smem) {
+  int occ = 0;
+  CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, dev::k_decompose<Gp, TS, F>, block, smem));
   return occ;
 }
 
@@ -212,13 +220,17 @@ void plan(pccp_gpu_ctx* c) {
   c->table_in_smem = in_smem ? 1 : 0;
   c->smem = base + (in_smem ? table : 0);
   int occ = 0;
+  int occ_dec = 0;
   dispatch(c, [&]<class Gp, bool TS, int F>() {
     set_smem_attrs<Gp, TS, F>(c->smem);
     occ = occupancy<Gp, TS, F>(c->block, c->smem);
+    occ_dec = occupancy_decompose<Gp, TS, F>(c->block, c->smem);
   });
+  if (occ_dec < 1) throw LimitError("decomposition kernel does not fit on an SM");
   if (occ < 1) throw LimitError("kernel does not fit on an SM (smem " + std::to_string(c->smem) + " B)");
   if (c->cfg.ctas_per_sm > 0) occ = std::min(occ, c->cfg.ctas_per_sm);
   c->ctas = c->n_sm * occ;
+  c->dec_ctas = c->n_sm * std::min(occ_dec, std::max(1, occ));  // co-resident (cooperative launch)
 }
 
 // keep_incumbent: leave the incumbent cell, the best-store lock and
@@ -345,41 +357,40 @@ void run_search(pccp_gpu_ctx* c, int mode, const int32_t* root_words, int depth_
     c->dec.ensure(2);
   }
   dev::DecState* d_st = reinterpret_cast<dev::DecState*>(c->dec.p);
-  const int per = c->warp ? c->gpc : 1;
-  // Expand the frontier in (fa, ia) until it holds `target` nodes; the result
-  // is left in (fa, ia).  Returns false after a model error.
+  // Expand the frontier in (fa, ia) until it holds `target` nodes, in one
+  // cooperative launch of the persistent decomposition kernel; the result is
+  // left in (fa, ia).  Returns false after a model error.
   auto expand_until = [&](int target) -> bool {
     if (count <= 0 || count >= target) return true;
+    const int grid = c->dec_ctas;
+    c->chunk.ensure((size_t)grid + 2);
     const dev::DecState st0{count, level};
     CK(cudaMemcpyAsync(c->dec.p, &st0, sizeof(st0), cudaMemcpyHostToDevice, c->stream));
-    int* FB[2] = {c->fa.p, c->fb.p};
-    int* IB[2] = {c->ia.p, c->ib.p};
-    const int grid = (int)std::min<long long>(c->ctas, (target + per - 1) / per);
+    CK(cudaMemsetAsync(c->chunk.p + grid, 0, 2 * sizeof(int), c->stream));  // grid barrier words
+    int* fb0 = c->fa.p;
+    int* fb1 = c->fb.p;
+    int* ib0 = c->ia.p;
+    int* ib1 = c->ib.p;
+    unsigned char* flags = c->flags.p;
+    int* chunk_count = c->chunk.p;
+    unsigned* bar = reinterpret_cast<unsigned*>(c->chunk.p + grid);
+    int tgt = target, strd = stride;
+    void* args[] = {(void*)&M, (void*)&C, (void*)&fb0, (void*)&fb1, (void*)&ib0, (void*)&ib1, (void*)&d_st,
+                    (void*)&tgt, (void*)&strd, (void*)&flags, (void*)&chunk_count, (void*)&bar};
     const int level0 = level;
-    int enq = 0;  // levels enqueued in this phase
+    CK(cudaLaunchCooperativeKernel((const void*)dev::k_decompose<Gp, TS, F>, dim3(grid), dim3(c->block), args,
+                                   c->smem, c->stream));
+    ++c->launches;
+    dev::DecState st;
     int stop = 0;
-    for (;;) {
-      const int batch = enq < 8 ? 4 : 2;  // early levels are tiny; later ones are checked sooner
-      for (int b = 0; b < batch; ++b, ++enq) {
-        const int src = enq & 1, dst = src ^ 1;
-        dev::k_expand<Gp, TS, F><<<grid, c->block, c->smem, c->stream>>>(M, C, FB[src], IB[src], d_st, target, stride,
-                                                                         FB[dst], c->flags.p);
-        CK(cudaGetLastError());
-        dev::k_compact<<<1, 1024, 0, c->stream>>>(c->flags.p, IB[dst], d_st, C, target);
-        CK(cudaGetLastError());
-        c->launches += 2;
-      }
-      dev::DecState st;
-      CK(cudaMemcpyAsync(&st, d_st, sizeof(st), cudaMemcpyDeviceToHost, c->stream));
-      CK(cudaMemcpyAsync(&stop, &c->G->stop, sizeof(int), cudaMemcpyDeviceToHost, c->stream));
-      CK(cudaStreamSynchronize(c->stream));
-      out.d2h += sizeof(st) + 4;
-      count = st.count;
-      level = st.levels;
-      if (std::getenv("PCCP_DEBUG_DEC"))
-        fprintf(stderr, "dec batch: enq=%d level=%d count=%d t=%.3f ms\n", enq, level, count, now_ms() - t_start);
-      if (count <= 0 || count >= target || stop == 2 || level - level0 < enq) break;
-    }
+    CK(cudaMemcpyAsync(&st, d_st, sizeof(st), cudaMemcpyDeviceToHost, c->stream));
+    CK(cudaMemcpyAsync(&stop, &c->G->stop, sizeof(int), cudaMemcpyDeviceToHost, c->stream));
+    CK(cudaStreamSynchronize(c->stream));
+    out.d2h += sizeof(st) + 4;
+    count = st.count;
+    level = st.levels;
+    if (std::getenv("PCCP_DEBUG_DEC"))
+      fprintf(stderr, "decompose: level=%d count=%d t=%.3f ms\n", level, count, now_ms() - t_start);
     if ((level - level0) & 1) {  // the frontier is in buffer (levels of this phase) & 1
       std::swap(c->fa, c->fb);
       std::swap(c->ia, c->ib);
@@ -591,6 +602,7 @@ void pccp_gpu_close(pccp_gpu_ctx* c) {
   c->mailbox.release();
   c->waitq.release();
   c->dec.release();
+  c->chunk.release();
   c->best.release();
   c->io.release();
   c->flags.release();

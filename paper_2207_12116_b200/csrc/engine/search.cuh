@@ -351,39 +351,47 @@ __global__ void __launch_bounds__(MaxThreads<G, F>::value, MaxThreads<G, F>::min
   }
 }
 
-// ---- K5: one level of the EPS decomposition (decompose, solver.cpp:180-213) ------
-// Parent p's children go to slots 2p (left, x <= mid) and 2p+1 (right); the
-// compaction below keeps BFS order, so the frontier is identical on every GPU.
-// The level's size and depth come from the device (DecState, written by the
-// previous k_compact), so the host can enqueue several levels without a
-// round trip; a level whose frontier is empty or already has `target` nodes,
-// or that follows a model error, is a no-op (and so is every later one).
+// ---- K5: the EPS decomposition (decompose, solver.cpp:180-213) ----------------
+// Whole BFS levels in one persistent launch: every CTA is resident (the grid
+// is the kernel's occupancy), levels are separated by a software grid
+// barrier, and the compaction into the next frontier runs in-kernel, so a
+// level costs a few microseconds of synchronisation instead of two launches
+// and a host round trip.  Parent p's children go to slots 2p (left, x <= mid)
+// and 2p+1 (right); the stable compaction keeps BFS order, so the frontier is
+// identical on every GPU.  Levels run while the frontier is non-empty, below
+// `target` and no model error has stopped the search.
 struct DecState {
   int count;   // current frontier size
   int levels;  // levels expanded so far
 };
 
-__device__ __forceinline__ bool dec_done(const DecState* st, const SearchCtl& C, int target) {
-  const int n = *(volatile const int*)&st->count;
-  return n <= 0 || n >= target || *(volatile const int*)&C.G->stop == 2;
+// Sense-reversing grid barrier over gridDim.x resident CTAs (bar[0] arrivals,
+// bar[1] generation).  Every CTA must call it the same number of times.
+__device__ __forceinline__ void grid_sync(unsigned* bar) {
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    const unsigned gen = *(volatile unsigned*)&bar[1];
+    __threadfence();
+    if (atomicAdd(&bar[0], 1u) == gridDim.x - 1) {
+      *(volatile unsigned*)&bar[0] = 0;
+      __threadfence();
+      atomicAdd(&bar[1], 1u);
+    } else {
+      while (*(volatile unsigned*)&bar[1] == gen) __nanosleep(32);
+    }
+    __threadfence();
+  }
+  __syncthreads();
 }
 
+// Both children of every parent of one level (one group per parent).
 template <class G, bool TS, int F>
-__global__ void __launch_bounds__(MaxThreads<G, F>::value, MaxThreads<G, F>::min_blocks) k_expand(Model M, SearchCtl C, const int* parents, const int* parent_idx, const DecState* st, int target, int stride,
-                         int* children, unsigned char* flags) {
-  if (dec_done(st, C, target)) return;
-  const int n_par = st->count;
-  const int child_depth = st->levels + 1;
-  if ((int)blockIdx.x * GroupOf<G>::per_cta() >= n_par) return;  // no parent for this CTA
-  const Frame f = frame(M);
-  const G g = GroupOf<G>::make(f);
-  const Tab<TS> tab = make_tab<TS>(f);
-  volatile int* S = f.stores + GroupOf<G>::in_cta() * M.store_stride;
-  const unsigned sb = init_store(g, S, M.L);
+__device__ void expand_level(const G& g, volatile int* S, unsigned sb, const Tab<TS>& tab, const Frame& f,
+                             const DeviceLayout& L, const SearchCtl& C, Cnt& cnt, const int* parents,
+                             const int* parent_idx, int n_par, int stride, int child_depth, int* children,
+                             unsigned char* flags) {
   const int gid = blockIdx.x * GroupOf<G>::per_cta() + GroupOf<G>::in_cta();
   const int ng = gridDim.x * GroupOf<G>::per_cta();
-  const DeviceLayout& L = M.L;
-  Cnt& cnt = f.cnt[GroupOf<G>::in_cta()];
   for (int p = gid; p < n_par; p += ng) {
     if (time_stop(g, C)) {  // abandoned parent: its subtree is unexplored
       if (g.rank() == 0) {
@@ -435,44 +443,109 @@ __global__ void __launch_bounds__(MaxThreads<G, F>::value, MaxThreads<G, F>::min
       g.sync();
     }
   }
-  if (g.rank() == 0) flush(C.G, cnt);
 }
 
-// Stable compaction of the child flags into the next frontier's index list.
-__global__ void k_compact(const unsigned char* flags, int* idx, DecState* st, SearchCtl C, int target) {
-  __shared__ int wsum[32];
-  __shared__ int base;
-  if (dec_done(st, C, target)) return;
-  const int n = 2 * st->count;
-  const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
-  if (tid == 0) base = 0;
+// Stable compaction of flags[0, n) into idx, CTA b owning chunk b: pass 1
+// counts each chunk, pass 2 (after a grid barrier) scans its chunk from the
+// sum of the earlier chunks.  Returns the total on every thread.
+__device__ int grid_compact(const unsigned char* flags, int n, int* idx, int* chunk_count, unsigned* bar) {
+  __shared__ int wsum[33];
+  const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5, nw = (int)(blockDim.x >> 5);
+  const int chunk = (n + (int)gridDim.x - 1) / (int)gridDim.x;
+  const int lo = min(n, (int)blockIdx.x * chunk), hi = min(n, lo + chunk);
+  int mine = 0;
+  for (int i = lo + tid; i < hi; i += blockDim.x) mine += flags[i] ? 1 : 0;
+  mine = __reduce_add_sync(kFull, mine);
+  if (lane == 0) wsum[wid] = mine;
   __syncthreads();
-  for (int start = 0; start < n; start += blockDim.x) {
+  if (tid == 0) {
+    int t = 0;
+    for (int w = 0; w < nw; ++w) t += wsum[w];
+    chunk_count[blockIdx.x] = t;
+  }
+  grid_sync(bar);
+  // offset of this chunk and the total, from the chunk counts
+  int before = 0, total = 0;
+  for (int b = tid; b < (int)gridDim.x; b += blockDim.x) {
+    const int v = *(volatile int*)&chunk_count[b];
+    total += v;
+    if (b < (int)blockIdx.x) before += v;
+  }
+  before = __reduce_add_sync(kFull, before);
+  total = __reduce_add_sync(kFull, total);
+  __syncthreads();
+  if (lane == 0) wsum[wid] = before;
+  __syncthreads();
+  if (tid == 0) {
+    int t = 0;
+    for (int w = 0; w < nw; ++w) t += wsum[w];
+    wsum[32] = t;
+  }
+  __syncthreads();
+  int base = wsum[32];
+  __syncthreads();
+  if (lane == 0) wsum[wid] = total;
+  __syncthreads();
+  if (tid == 0) {
+    int t = 0;
+    for (int w = 0; w < nw; ++w) t += wsum[w];
+    wsum[32] = t;
+  }
+  __syncthreads();
+  total = wsum[32];
+  __syncthreads();
+  for (int start = lo; start < hi; start += blockDim.x) {
     const int i = start + tid;
-    const bool f = i < n && flags[i];
-    const unsigned m = __ballot_sync(kFull, f);
-    const int pre = __popc(m & ((1u << lane) - 1u));
+    const bool fl = i < hi && flags[i];
+    const unsigned m = __ballot_sync(kFull, fl);
     if (lane == 0) wsum[wid] = __popc(m);
     __syncthreads();
-    if (wid == 0) {
-      int v = lane < (int)(blockDim.x >> 5) ? wsum[lane] : 0;
-      for (int o = 1; o < 32; o <<= 1) {
-        const int u = __shfl_up_sync(kFull, v, o);
-        if (lane >= o) v += u;
+    if (tid == 0) {
+      int t = 0;
+      for (int w = 0; w < nw; ++w) {
+        const int c = wsum[w];
+        wsum[w] = t;
+        t += c;
       }
-      wsum[lane] = v;
+      wsum[32] = t;
     }
     __syncthreads();
-    const int woff = wid == 0 ? 0 : wsum[wid - 1];
-    if (f) idx[base + woff + pre] = i;
-    __syncthreads();
-    if (tid == 0) base += wsum[31];
+    if (fl) idx[base + wsum[wid] + __popc(m & ((1u << lane) - 1u))] = i;
+    base += wsum[32];
     __syncthreads();
   }
-  if (tid == 0) {
-    st->count = base;
-    st->levels += 1;
+  return total;
+}
+
+template <class G, bool TS, int F>
+__global__ void __launch_bounds__(MaxThreads<G, F>::value, MaxThreads<G, F>::min_blocks)
+    k_decompose(Model M, SearchCtl C, int* fb0, int* fb1, int* ib0, int* ib1, DecState* st, int target, int stride,
+                unsigned char* flags, int* chunk_count, unsigned* bar) {
+  const Frame f = frame(M);
+  const G g = GroupOf<G>::make(f);
+  const Tab<TS> tab = make_tab<TS>(f);
+  volatile int* S = f.stores + GroupOf<G>::in_cta() * M.store_stride;
+  const unsigned sb = init_store(g, S, M.L);
+  Cnt& cnt = f.cnt[GroupOf<G>::in_cta()];
+  int* FB[2] = {fb0, fb1};
+  int* IB[2] = {ib0, ib1};
+  int count = *(volatile int*)&st->count;
+  int levels = *(volatile int*)&st->levels;
+  for (int k = 0;; ++k) {
+    if (count <= 0 || count >= target || *(volatile int*)&C.G->stop == 2) break;  // uniform across the grid
+    const int src = k & 1, dst = src ^ 1;
+    expand_level<G, TS, F>(g, S, sb, tab, f, M.L, C, cnt, FB[src], IB[src], count, stride, levels + 1, FB[dst],
+                           flags);
+    grid_sync(bar);
+    count = grid_compact(flags, 2 * count, IB[dst], chunk_count, bar);
+    ++levels;
+    if (blockIdx.x == 0 && threadIdx.x == 0) {
+      st->count = count;
+      st->levels = levels;
+    }
+    grid_sync(bar);  // every CTA has read the chunk counts and agrees on `count`
   }
+  if (g.rank() == 0) flush(C.G, cnt);
 }
 
 // Positions shard + k * shards of the shared frontier's index list.
