@@ -341,31 +341,47 @@ __device__ __forceinline__ void sred_min(unsigned a, int v) {
 __device__ __forceinline__ void sred_max(unsigned a, int v) {
   asm volatile("red.shared.max.s32 [%0], %1;" ::"r"(a), "r"(v) : "memory");
 }
-__device__ __forceinline__ bool eval_ne_fast(unsigned sb, int4 q) {
+// Sets ch when a candidate beat its snapshot (inside the join branch, so
+// the flag costs nothing on the common no-change path).
+__device__ __forceinline__ void eval_ne_fast(unsigned sb, int4 q, unsigned& ch) {
   const unsigned ax = sb + (unsigned)q.x, ay = sb + (unsigned)q.w;
   const int2 X = sld2(ax), Y = sld2(ay);
   const int A = q.y, B = q.z;
   const int v1 = Y.y + B, v2 = X.x - B, v3 = X.y + A, v4 = Y.x - A;
   const bool g1 = v3 < Y.x, g2 = v1 < X.x;
   const bool c1 = g1 & (v1 < X.y), c2 = g1 & (v2 > Y.x), c3 = g2 & (v3 < Y.y), c4 = g2 & (v4 > X.x);
-  const bool any = c1 | c2 | c3 | c4;
-  if (any) {
+  if (c1 | c2 | c3 | c4) {
     sred_min(ax + 4, c1 ? v1 : INT_MAX);
     sred_max(ay, c2 ? v2 : INT_MIN);
     sred_min(ay + 4, c3 ? v3 : INT_MAX);
     sred_max(ax, c4 ? v4 : INT_MIN);
+    ch = 1u;
   }
-  return any;
 }
 
-// One eventless round over the NE records (loop bounds held in registers).
+__device__ __forceinline__ int4 lds128(unsigned a) {
+  int4 r;
+  asm("ld.shared.v4.b32 {%0, %1, %2, %3}, [%4];" : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w) : "r"(a));
+  return r;
+}
+
+// One eventless round over the NE records.  With the table in shared memory
+// the loop walks record addresses directly (one add and one compare per
+// record).
 template <class G, bool TS>
 __device__ __forceinline__ bool ne_round(const G& g, unsigned sb, const Tab<TS>& tab, const DeviceLayout& L) {
   const int n = (int)L.n_ne;
   const unsigned off = L.ne;
   unsigned ch = 0;
   if (L.ne_fast) {
-    for (int i = g.rank(); i < n; i += g.size()) ch |= (unsigned)eval_ne_fast(sb, tab.ld4(off, i));
+    if constexpr (TS) {
+      const unsigned step = 16u * (unsigned)g.size();
+      const unsigned end = tab.base + 4u * off + 16u * (unsigned)n;
+      for (unsigned a = tab.base + 4u * off + 16u * (unsigned)g.rank(); a < end; a += step)
+        eval_ne_fast(sb, lds128(a), ch);
+    } else {
+      for (int i = g.rank(); i < n; i += g.size()) eval_ne_fast(sb, tab.ld4(off, i), ch);
+    }
   } else {
     for (int i = g.rank(); i < n; i += g.size()) ch |= eval_ne(sb, tab.ld4(off, i)) != 0ull;
   }
