@@ -377,8 +377,13 @@ __device__ __forceinline__ bool ne_round(const G& g, unsigned sb, const Tab<TS>&
     if constexpr (TS) {
       const unsigned step = 16u * (unsigned)g.size();
       const unsigned end = tab.base + 4u * off + 16u * (unsigned)n;
-      for (unsigned a = tab.base + 4u * off + 16u * (unsigned)g.rank(); a < end; a += step)
-        eval_ne_fast(sb, lds128(a), ch);
+      unsigned a = tab.base + 4u * off + 16u * (unsigned)g.rank();
+      for (; a + step < end; a += 2 * step) {  // two records per trip: loads of both issued first
+        const int4 q0 = lds128(a), q1 = lds128(a + step);
+        eval_ne_fast(sb, q0, ch);
+        eval_ne_fast(sb, q1, ch);
+      }
+      if (a < end) eval_ne_fast(sb, lds128(a), ch);
     } else {
       for (int i = g.rank(); i < n; i += g.size()) eval_ne_fast(sb, tab.ld4(off, i), ch);
     }
