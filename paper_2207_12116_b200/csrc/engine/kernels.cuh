@@ -449,18 +449,21 @@ __device__ __forceinline__ bool eval_reif(unsigned sb, int4 r) {
       nlx = max(nlx, narrow(wly + 1 - p));
     }
   }
-  // joins; the snapshot is the pre-check (bounds only move toward top)
+  // Joins; the snapshot is the pre-check (bounds only move toward top).  As in
+  // eval_ne_fast, a candidate that beats its snapshot proves a change this
+  // round, so the joins need no return value: all six are issued under one
+  // branch, the non-improving ones as the join identity.
   const bool c1 = nlb > lb, c2 = nub < ub, c3 = nux < ux, c4 = nly > ly, c5 = nuy < uy, c6 = nlx > lx;
-  bool ch = false;
   if (c1 | c2 | c3 | c4 | c5 | c6) {
-    if (c1) ch |= satom_max(ab, nlb) < nlb;
-    if (c2) ch |= satom_min(ab + 4, nub) > nub;
-    if (c3) ch |= satom_min(ax + 4, nux) > nux;
-    if (c4) ch |= satom_max(ay, nly) < nly;
-    if (c5) ch |= satom_min(ay + 4, nuy) > nuy;
-    if (c6) ch |= satom_max(ax, nlx) < nlx;
+    sred_max(ab, c1 ? nlb : INT_MIN);
+    sred_min(ab + 4, c2 ? nub : INT_MAX);
+    sred_min(ax + 4, c3 ? nux : INT_MAX);
+    sred_max(ay, c4 ? nly : INT_MIN);
+    sred_min(ay + 4, c5 ? nuy : INT_MAX);
+    sred_max(ax, c6 ? nlx : INT_MIN);
+    return true;
   }
-  return ch;
+  return false;
 }
 
 // ---- propagators -----------------------------------------------------------------
