@@ -134,10 +134,11 @@ struct pccp_gpu_ctx {
     M.L = low.L;
     M.L.var_order = (std::uint32_t)var_order;
     M.L.var_seed = var_seed;
-    bool ne = false, rows = false;
-    if (!std::getenv("PCCP_NO_FAST")) fast_paths(low, stores, n_stores, stride, ne, rows);
+    bool ne = false, rows = false, reif = false;
+    if (!std::getenv("PCCP_NO_FAST")) fast_paths(low, stores, n_stores, stride, ne, rows, reif);
     M.L.ne_fast = ne && !std::getenv("PCCP_NO_NE_FAST") ? 1u : 0u;
     M.L.rows_fast = rows ? 1u : 0u;
+    M.L.reif_fast = reif ? 1u : 0u;
     M.blob = blob.p;
     M.table_in_smem = table_in_smem;
     M.store_stride = store_stride;

@@ -396,6 +396,9 @@ __device__ __forceinline__ bool ne_round(const G& g, unsigned sb, const Tab<TS>&
 // Fused reification b <-> (x + p <= y and y + q <= x): the 11 commands of
 // compile_reified (propagation.cpp:415-431) from one read of the 6 words.
 // q = {lbx | lby << 16, lbb, p, q}.  Returns true iff a word changed.
+// Fast: the host's value-range analysis (fast_paths) proved every x/y value
+// read stays inside (-2^30, 2^30), so the 32-bit branch is taken unchecked.
+template <bool Fast>
 __device__ __forceinline__ bool eval_reif(unsigned sb, int4 r) {
   const unsigned ax = sb + (((unsigned)r.x & 0xffffu) << 2), ay = sb + (((unsigned)r.x >> 16) << 2);
   const unsigned ab = sb + ((unsigned)r.y << 2);
@@ -403,7 +406,7 @@ __device__ __forceinline__ bool eval_reif(unsigned sb, int4 r) {
   const int p = r.z, q = r.w;
   const bool bt = lb > 0, bf = ub <= 0;  // [lb b > 0], [ub b <= 0]
   int nlb = INT_MIN, nub = INT_MAX, nux = INT_MAX, nly = INT_MIN, nuy = INT_MAX, nlx = INT_MIN;
-  if (small30(lx) & small30(ux) & small30(ly) & small30(uy)) {
+  if (Fast || (small30(lx) & small30(ux) & small30(ly) & small30(uy))) {
     const bool eA = ux - ly <= -p, eB = uy - lx <= -q;  // entailment of x + p <= y, y + q <= x
     const bool nA = lx - uy > -p, nB = ly - ux > -q;    // entailment of their negations
     if (eA & eB) nlb = nub = 1;
@@ -732,7 +735,11 @@ __device__ __forceinline__ bool eval_other_families(const G& g, volatile int* S,
                                                     const DeviceLayout& L) {
     const int* __restrict__ T = tab.p;
     bool ch = false;
-    for (int i = g.rank(); i < (int)L.n_reif; i += g.size()) ch |= eval_reif(sb, tab.ld4(L.reif, i));
+    if (L.reif_fast) {
+      for (int i = g.rank(); i < (int)L.n_reif; i += g.size()) ch |= eval_reif<true>(sb, tab.ld4(L.reif, i));
+    } else {
+      for (int i = g.rank(); i < (int)L.n_reif; i += g.size()) ch |= eval_reif<false>(sb, tab.ld4(L.reif, i));
+    }
     for (int i = g.rank(); i < (int)L.n_unit1; i += g.size()) {
       const int4 q = tab.ld4(L.unit1, i);
       if (unit_guard(sb, q.x, q.y)) ch |= unit_tell(sb, q.z, q.w);

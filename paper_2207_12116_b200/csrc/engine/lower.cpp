@@ -745,6 +745,16 @@ Lowered lower_model(const pccp_model& m) {
       read_fast[lbw] = read_fast[lbw + 1] = 1;
     }
   }
+  out.reif_ok = L.n_reif > 0;
+  for (std::uint32_t i = 0; i < L.n_reif && out.reif_ok; ++i) {
+    const std::uint32_t xy = static_cast<std::uint32_t>(B[L.reif + 4 * i]);
+    for (std::uint32_t lbw : {xy & 0xffffu, xy >> 16}) {
+      if (lbw + 1 >= m.n_words || cls[lbw] == 2 || cls[lbw + 1] == 2) out.reif_ok = false;
+      else read_fast[lbw] = read_fast[lbw + 1] = 1;
+    }
+    out.reif_k = std::max({out.reif_k, std::abs(std::int64_t{B[L.reif + 4 * i + 2]}),
+                           std::abs(std::int64_t{B[L.reif + 4 * i + 3]})});
+  }
   L.hot_words = static_cast<std::uint32_t>(B.size());
 
   L.n_fold = static_cast<std::uint32_t>(fold_w.size());
@@ -831,9 +841,9 @@ Lowered lower_model(const pccp_model& m) {
 // a round performs at most r_aff of them: |v| <= max(B0, B1) + r_aff * kaff.
 // Decisions and the objective bound stay inside the box (+-1).
 void fast_paths(const Lowered& low, const std::int32_t* stores, std::size_t n_stores, std::size_t stride,
-                bool& ne_fast, bool& rows_fast) {
-  ne_fast = rows_fast = false;
-  if ((!low.ne_ok && !low.rows_ok) || !stores || !n_stores) return;
+                bool& ne_fast, bool& rows_fast, bool& reif_fast) {
+  ne_fast = rows_fast = reif_fast = false;
+  if ((!low.ne_ok && !low.rows_ok && !low.reif_ok) || !stores || !n_stores) return;
   const DeviceLayout& L = low.L;
   const std::uint32_t nw = L.n_words;
   std::vector<std::int32_t> w(nw);
@@ -863,6 +873,7 @@ void fast_paths(const Lowered& low, const std::int32_t* stores, std::size_t n_st
   const std::int64_t bound1 = std::max(b0, b1) + 1 + low.r_aff * low.kaff;
   if (bound1 >= lim) return;
   ne_fast = low.ne_ok && bound1 + low.kaff + 2 < lim;
+  reif_fast = low.reif_ok && bound1 + low.reif_k + 2 < lim;
   if (low.rows_ok) {
     // |sum| <= S; the zeroing guard coef + sum - coef * v is <= 2 S + |coef|
     std::int64_t worst = 0;
