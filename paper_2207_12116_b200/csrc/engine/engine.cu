@@ -376,8 +376,20 @@ void run_search(pccp_gpu_ctx* c, int mode, const int32_t* root_words, int depth_
     int* chunk_count = c->chunk.p;
     unsigned* bar = reinterpret_cast<unsigned*>(c->chunk.p + grid);
     int tgt = target, strd = stride;
+    const bool dbg = std::getenv("PCCP_DEBUG_DEC") != nullptr;
+    DBuf<unsigned long long> profbuf;
+    unsigned long long* prof = nullptr;
+    if (dbg) {
+      profbuf.ensure(240 + 32);
+      CK(cudaMemsetAsync(profbuf.p, 0, (240 + 32) * 8, c->stream));
+      prof = profbuf.p;
+      unsigned long long* tl = profbuf.p + 240;
+      CK(cudaMemcpyToSymbolAsync(dev::g_dbg_tl, &tl, sizeof(tl), 0, cudaMemcpyHostToDevice, c->stream));
+      unsigned long long* tr = profbuf.p + 240 + 24;
+      CK(cudaMemcpyToSymbolAsync(dev::g_dbg_round, &tr, sizeof(tr), 0, cudaMemcpyHostToDevice, c->stream));
+    }
     void* args[] = {(void*)&M, (void*)&C, (void*)&fb0, (void*)&fb1, (void*)&ib0, (void*)&ib1, (void*)&d_st,
-                    (void*)&tgt, (void*)&strd, (void*)&flags, (void*)&chunk_count, (void*)&bar};
+                    (void*)&tgt, (void*)&strd, (void*)&flags, (void*)&chunk_count, (void*)&bar, (void*)&prof};
     const int level0 = level;
     CK(cudaLaunchCooperativeKernel((const void*)dev::k_decompose<Gp, TS, F>, dim3(grid), dim3(c->block), args,
                                    c->smem, c->stream));
@@ -390,8 +402,28 @@ void run_search(pccp_gpu_ctx* c, int mode, const int32_t* root_words, int depth_
     out.d2h += sizeof(st) + 4;
     count = st.count;
     level = st.levels;
-    if (std::getenv("PCCP_DEBUG_DEC"))
-      fprintf(stderr, "decompose: level=%d count=%d t=%.3f ms\n", level, count, now_ms() - t_start);
+    if (dbg) {
+      fprintf(stderr, "decompose: level=%d count=%d t=%.3f ms grid=%d\n", level, count, now_ms() - t_start, grid);
+      unsigned long long h[240];
+      CK(cudaMemcpy(h, prof, sizeof(h), cudaMemcpyDeviceToHost));
+      unsigned long long tl[32];
+      CK(cudaMemcpy(tl, prof + 240, sizeof(tl), cudaMemcpyDeviceToHost));
+      fprintf(stderr, "  last parent of CTA 0: copy %.1f branch %.1f | L: join %.1f prop %.1f (r=%llu) classify %.1f out %.1f"
+                      " | R: join %.1f prop %.1f (r=%llu) classify %.1f out %.1f us\n",
+              (tl[1] - tl[0]) * 1e-3, (tl[2] - tl[1]) * 1e-3, (tl[3] - tl[2]) * 1e-3, (tl[4] - tl[3]) * 1e-3, tl[20],
+              (tl[5] - tl[4]) * 1e-3, (tl[6] - tl[5]) * 1e-3, (tl[8] - tl[6]) * 1e-3, (tl[9] - tl[8]) * 1e-3, tl[21],
+              (tl[10] - tl[9]) * 1e-3, (tl[11] - tl[10]) * 1e-3);
+      fprintf(stderr, "  last round of CTA 0: reif+ne %.2f unit1 %.2f small %.2f rows %.2f gen+scan %.2f end %.2f us\n",
+              0.0, (tl[25] - tl[24]) * 1e-3, (tl[26] - tl[25]) * 1e-3, (tl[27] - tl[26]) * 1e-3,
+              (tl[28] - tl[27]) * 1e-3, (tl[29] - tl[28]) * 1e-3);
+      unsigned long long* zero = nullptr;
+      CK(cudaMemcpyToSymbol(dev::g_dbg_tl, &zero, sizeof(zero)));
+      CK(cudaMemcpyToSymbol(dev::g_dbg_round, &zero, sizeof(zero)));
+      for (int k = 0; k < 60 && h[4 * k]; ++k)
+        fprintf(stderr, "  level %2d: expand %7.1f us  compact %6.1f us  barrier %5.1f us\n", k,
+                (h[4 * k + 1] - h[4 * k]) * 1e-3, (h[4 * k + 2] - h[4 * k + 1]) * 1e-3,
+                (h[4 * k + 3] - h[4 * k + 2]) * 1e-3);
+    }
     if ((level - level0) & 1) {  // the frontier is in buffer (levels of this phase) & 1
       std::swap(c->fa, c->fb);
       std::swap(c->ia, c->ib);

@@ -551,6 +551,14 @@ __device__ __forceinline__ bool eval_small(volatile int* S, const int* __restric
 // (-2^30, 2^30): the same rows in plain 32-bit arithmetic, no sentinel tests.
 // An overloaded row (cell = +inf) makes every zeroing guard hold, as tv(1,
 // +inf) does in the widened form.
+//
+// Latency: a lane's terms (at most kRowTerms, lower.cpp sizes row_lanes so)
+// are loaded in two batches — every table entry, then every store word —
+// instead of a dependent load chain per term, and the zeroing guards reuse
+// the values summed.  That is sound (the summed values are lower bounds of
+// the current ones, so a guard that holds on them holds now) and it is the
+// fixed point's: at the quiet round every read is of the final store.
+constexpr int kRowTerms = 8;
 template <class G, bool TS>
 __device__ bool eval_rows_fast(const G& g, unsigned sb, const Tab<TS>& tab, const DeviceLayout& L) {
   const int R = (int)L.row_lanes;
@@ -564,15 +572,19 @@ __device__ bool eval_rows_fast(const G& g, unsigned sb, const Tab<TS>& tab, cons
     const int row = base + my;
     const bool act = row < n_rows;
     int s = 0;
-    int beg = 0, end = 0;
+    int x[kRowTerms], v[kRowTerms];
+    int end = 0, j0 = 0;
     if (act) {
-      beg = tab.ld1(off_row, row);
+      j0 = tab.ld1(off_row, row) + sub;
       end = tab.ld1(off_row, row + 1);
-      for (int j = beg + sub; j < end; j += R) {
-        const int x = tab.ld1(off_terms, j);
-        s += tcoef(x) * sld(sb + ((unsigned)tword(x) << 2));
-      }
     }
+    const int n_my = end > j0 ? (end - j0 + R - 1) / R : 0;  // this lane's terms (<= kRowTerms)
+#pragma unroll
+    for (int t = 0; t < kRowTerms; ++t) x[t] = t < n_my ? tab.ld1(off_terms, j0 + t * R) : 0;
+#pragma unroll
+    for (int t = 0; t < kRowTerms; ++t) v[t] = t < n_my ? sld(sb + ((unsigned)tword(x[t]) << 2)) : 0;
+#pragma unroll
+    for (int t = 0; t < kRowTerms; ++t) s += tcoef(x[t]) * v[t];
     for (int o = R >> 1; o > 0; o >>= 1) s += __shfl_xor_sync(kFull, s, o, R);
     if (act) {
       const int c = tab.ld1(off_c, row);
@@ -580,11 +592,11 @@ __device__ bool eval_rows_fast(const G& g, unsigned sb, const Tab<TS>& tab, cons
       const int cell = over ? INT_MAX : s;  // [lsum > c] => lsum <- +inf
       if (sub == 0) ch |= sjoin_max(sb + ((unsigned)tab.ld1(off_lsum, row) << 2), cell);
       if (c != INT_MAX) {
-        for (int j = beg + sub; j < end; j += R) {
-          const int x = tab.ld1(off_terms, j);
-          const int coef = tcoef(x);
-          const unsigned a = sb + ((unsigned)tword(x) << 2);
-          if (over || coef + s - coef * sld(a) > c) {
+#pragma unroll
+        for (int t = 0; t < kRowTerms; ++t) {
+          const int coef = tcoef(x[t]);
+          if (t < n_my && (over || coef + s - coef * v[t] > c)) {
+            const unsigned a = sb + ((unsigned)tword(x[t]) << 2);
             ch |= sjoin_max(a, 0);
             ch |= sjoin_min(a + 4, 0);
           }
@@ -729,6 +741,14 @@ __device__ bool propagate_filtered(const WarpGroup& g, volatile int* S, unsigned
   return failed;
 }
 
+// Build with -DPCCP_DEBUG_TIMELINE (PCCP_NVFLAGS) for the PCCP_DEBUG_DEC timelines.
+__device__ unsigned long long* g_dbg_round = nullptr;  // one round's timeline (CTA 0)
+__device__ __forceinline__ void dbg_r(int k) {
+#ifdef PCCP_DEBUG_TIMELINE
+  if (g_dbg_round && blockIdx.x == 0 && threadIdx.x == 0) g_dbg_round[k] = globaltimer();
+#endif
+}
+
 // One round of every family but NE (propagate below).
 template <class G, bool TS>
 __device__ __forceinline__ bool eval_other_families(const G& g, volatile int* S, unsigned sb, const Tab<TS>& tab,
@@ -740,10 +760,12 @@ __device__ __forceinline__ bool eval_other_families(const G& g, volatile int* S,
     } else {
       for (int i = g.rank(); i < (int)L.n_reif; i += g.size()) ch |= eval_reif<false>(sb, tab.ld4(L.reif, i));
     }
+    dbg_r(0);
     for (int i = g.rank(); i < (int)L.n_unit1; i += g.size()) {
       const int4 q = tab.ld4(L.unit1, i);
       if (unit_guard(sb, q.x, q.y)) ch |= unit_tell(sb, q.z, q.w);
     }
+    dbg_r(1);
     for (int i = g.rank(); i < (int)L.n_unit2; i += g.size()) {
       const int4 q = tab.ld4(L.unit2, i);
       if (unit_guard(sb, q.x, q.y)) {
@@ -752,7 +774,9 @@ __device__ __forceinline__ bool eval_other_families(const G& g, volatile int* S,
       }
     }
     for (int i = g.rank(); i < (int)L.n_small; i += g.size()) ch |= eval_small(S, T, L, i);
+    dbg_r(2);
     if (L.n_rows) ch |= eval_rows(g, sb, tab, L);
+    dbg_r(3);
     for (int i = g.rank(); i < (int)L.n_gen; i += g.size())
       ch |= eval_generic(S, T + L.gen_code + T[L.gen_off + i]);
     return ch;
@@ -791,8 +815,10 @@ __device__ bool propagate(const G& g, volatile int* S, unsigned sb, const Tab<TS
       }
       for (int i = g.rank(); i < (int)L.n_sc; i += g.size()) fl |= S[T[L.sc_w + i]] == T[L.sc_top + i];
     }
+    dbg_r(4);
     bool any_ch, any_fl;
     g.round_end(ch, fl, any_ch, any_fl, r);
+    dbg_r(5);
     ++r;
     if (any_fl) { failed = true; break; }
     if (!any_ch) break;

@@ -385,6 +385,13 @@ __device__ __forceinline__ void grid_sync(unsigned* bar) {
 }
 
 // Both children of every parent of one level (one group per parent).
+__device__ unsigned long long* g_dbg_tl = nullptr;  // PCCP_DEBUG_TIMELINE: CTA 0's last parent
+__device__ __forceinline__ void dbg_mark(int k) {
+#ifdef PCCP_DEBUG_TIMELINE
+  if (g_dbg_tl && blockIdx.x == 0 && threadIdx.x == 0 && k < 32) g_dbg_tl[k] = globaltimer();
+#endif
+}
+
 template <class G, bool TS, int F>
 __device__ void expand_level(const G& g, volatile int* S, unsigned sb, const Tab<TS>& tab, const Frame& f,
                              const DeviceLayout& L, const SearchCtl& C, Cnt& cnt, const int* parents,
@@ -402,11 +409,14 @@ __device__ void expand_level(const G& g, volatile int* S, unsigned sb, const Tab
       continue;
     }
     const int* par = parents + (size_t)parent_idx[p] * stride;
+    dbg_mark(0);
     copy_words(g, S, par, (int)L.n_words);
     g.sync();
+    dbg_mark(1);
     int lbw = 0, mid = 0;
     const int b = branch(g, S, f.T, L, lbw, mid);
     g.sync();  // every thread has read S before rank 0 joins the decision
+    dbg_mark(2);
     for (int side = 0; side < 2; ++side) {
       unsigned char keep = 0;
       if (b == 1) {
@@ -423,7 +433,12 @@ __device__ void expand_level(const G& g, volatile int* S, unsigned sb, const Tab
         dirty |= join_objective(g, S, L, C);
         g.sync();
         int r = 0;
+        dbg_mark(3 + 5 * side);
         const bool failed = propagate<G, TS, F>(g, S, sb, tab, L, r, dirty);
+        dbg_mark(4 + 5 * side);
+#ifdef PCCP_DEBUG_TIMELINE
+        if (g_dbg_tl && blockIdx.x == 0 && threadIdx.x == 0) g_dbg_tl[20 + side] = r;
+#endif
         if (C.count && g.rank() == 0) {
           ++cnt.nodes;
           cnt.rounds += (unsigned long long)r;
@@ -431,10 +446,12 @@ __device__ void expand_level(const G& g, volatile int* S, unsigned sb, const Tab
         }
         int clbw, cmid;
         const int e = classify(g, S, f.T, L, C, cnt, failed, child_depth, clbw, cmid);
+        dbg_mark(5 + 5 * side);
         if (e == 1) {
           copy_out(g, children + (size_t)(2 * p + side) * stride, S, (int)L.n_words);
           keep = 1;
         }
+        dbg_mark(6 + 5 * side);
       } else if (b < 0 && g.rank() == 0) {
         C.G->error_code = 1;
         atomicExch(&C.G->stop, 2);
@@ -520,7 +537,7 @@ __device__ int grid_compact(const unsigned char* flags, int n, int* idx, int* ch
 template <class G, bool TS, int F>
 __global__ void __launch_bounds__(MaxThreads<G, F>::value, MaxThreads<G, F>::min_blocks)
     k_decompose(Model M, SearchCtl C, int* fb0, int* fb1, int* ib0, int* ib1, DecState* st, int target, int stride,
-                unsigned char* flags, int* chunk_count, unsigned* bar) {
+                unsigned char* flags, int* chunk_count, unsigned* bar, unsigned long long* prof) {
   const Frame f = frame(M);
   const G g = GroupOf<G>::make(f);
   const Tab<TS> tab = make_tab<TS>(f);
@@ -534,16 +551,21 @@ __global__ void __launch_bounds__(MaxThreads<G, F>::value, MaxThreads<G, F>::min
   for (int k = 0;; ++k) {
     if (count <= 0 || count >= target || *(volatile int*)&C.G->stop == 2) break;  // uniform across the grid
     const int src = k & 1, dst = src ^ 1;
+    const bool rec = prof && blockIdx.x == 0 && threadIdx.x == 0 && k < 60;  // PCCP_DEBUG_DEC timeline
+    if (rec) prof[4 * k] = globaltimer();
     expand_level<G, TS, F>(g, S, sb, tab, f, M.L, C, cnt, FB[src], IB[src], count, stride, levels + 1, FB[dst],
                            flags);
     grid_sync(bar);
+    if (rec) prof[4 * k + 1] = globaltimer();
     count = grid_compact(flags, 2 * count, IB[dst], chunk_count, bar);
+    if (rec) prof[4 * k + 2] = globaltimer();
     ++levels;
     if (blockIdx.x == 0 && threadIdx.x == 0) {
       st->count = count;
       st->levels = levels;
     }
     grid_sync(bar);  // every CTA has read the chunk counts and agrees on `count`
+    if (rec) prof[4 * k + 3] = globaltimer();
   }
   if (g.rank() == 0) flush(C.G, cnt);
 }
