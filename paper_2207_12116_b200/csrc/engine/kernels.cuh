@@ -566,31 +566,32 @@ __device__ bool eval_rows_fast(const G& g, unsigned sb, const Tab<TS>& tab, cons
   const int per_pass = g.size() / R;
   const int my = g.rank() / R;
   const int n_rows = (int)L.n_rows;
-  const unsigned off_row = L.row_off, off_terms = L.row_terms, off_c = L.row_c, off_lsum = L.row_lsum;
+  const unsigned off_meta = L.row_meta, off_terms = L.row_terms;
   unsigned ch = 0;
   for (int base = 0; base < n_rows; base += per_pass) {
     const int row = base + my;
     const bool act = row < n_rows;
     int s = 0;
     int x[kRowTerms], v[kRowTerms];
-    int end = 0, j0 = 0;
-    if (act) {
-      j0 = tab.ld1(off_row, row) + sub;
-      end = tab.ld1(off_row, row + 1);
-    }
+    const int4 meta = act ? tab.ld4(off_meta, row) : make_int4(0, 0, INT_MAX, 0);  // {beg, end, c, lsum}
+    const int j0 = meta.x + sub, end = meta.y, c = meta.z;
+    const unsigned alsum = sb + ((unsigned)meta.w << 2);
     const int n_my = end > j0 ? (end - j0 + R - 1) / R : 0;  // this lane's terms (<= kRowTerms)
 #pragma unroll
     for (int t = 0; t < kRowTerms; ++t) x[t] = t < n_my ? tab.ld1(off_terms, j0 + t * R) : 0;
+    const int lsum_now = act && sub == 0 ? sld(alsum) : INT_MAX;  // snapshot for the lsum join
 #pragma unroll
     for (int t = 0; t < kRowTerms; ++t) v[t] = t < n_my ? sld(sb + ((unsigned)tword(x[t]) << 2)) : 0;
 #pragma unroll
     for (int t = 0; t < kRowTerms; ++t) s += tcoef(x[t]) * v[t];
     for (int o = R >> 1; o > 0; o >>= 1) s += __shfl_xor_sync(kFull, s, o, R);
     if (act) {
-      const int c = tab.ld1(off_c, row);
       const bool over = s > c;
       const int cell = over ? INT_MAX : s;  // [lsum > c] => lsum <- +inf
-      if (sub == 0) ch |= sjoin_max(sb + ((unsigned)tab.ld1(off_lsum, row) << 2), cell);
+      if (sub == 0 && cell > lsum_now) {     // beats the snapshot: a change this round (eval_ne_fast)
+        sred_max(alsum, cell);
+        ch = 1u;
+      }
       if (c != INT_MAX) {
 #pragma unroll
         for (int t = 0; t < kRowTerms; ++t) {

@@ -715,6 +715,14 @@ Lowered lower_model(const pccp_model& m) {
       for (std::int32_t x : rows[r].terms) B[L.row_terms + t++] = x;
     }
     B[L.row_off + L.n_rows] = static_cast<std::int32_t>(t);
+    // the same per row as one int4 {first term, end, c, lsum word} (eval_rows_fast)
+    L.row_meta = reserve_arr(4 * L.n_rows);
+    for (std::uint32_t r = 0; r < L.n_rows; ++r) {
+      B[L.row_meta + 4 * r + 0] = B[L.row_off + r];
+      B[L.row_meta + 4 * r + 1] = B[L.row_off + r + 1];
+      B[L.row_meta + 4 * r + 2] = rows[r].c;
+      B[L.row_meta + 4 * r + 3] = static_cast<std::int32_t>(rows[r].lsum);
+    }
   }
   // Rows whose terms all read class <= 1 words can be summed in 32 bits once
   // the entry values are known to be small (fast_paths).

@@ -53,6 +53,7 @@ struct DeviceLayout {
   std::uint32_t fold_w, fold_v;  // fold_w: word | (up << 31)
   std::uint32_t n_fold;
   std::uint32_t row_off, row_lsum, row_c, row_terms;
+  std::uint32_t row_meta;  // int4 per row: {first term, end, c, lsum word}
   std::uint32_t n_rows, n_row_terms, row_lanes;  // lanes per row (power of two <= 32)
   std::uint32_t gen_off;                          // offsets into gen_code
   std::uint32_t gen_code;
