@@ -134,8 +134,9 @@ struct pccp_gpu_ctx {
     M.L = low.L;
     M.L.var_order = (std::uint32_t)var_order;
     M.L.var_seed = var_seed;
-    bool ne = false, rows = false, reif = false;
-    if (!std::getenv("PCCP_NO_FAST")) fast_paths(low, stores, n_stores, stride, ne, rows, reif);
+    bool ne = false, rows = false, reif = false, unit = false;
+    if (!std::getenv("PCCP_NO_FAST")) fast_paths(low, stores, n_stores, stride, ne, rows, reif, unit);
+    M.L.unit_fast = unit ? 1u : 0u;
     M.L.ne_fast = ne && !std::getenv("PCCP_NO_NE_FAST") ? 1u : 0u;
     M.L.rows_fast = rows ? 1u : 0u;
     M.L.reif_fast = reif ? 1u : 0u;

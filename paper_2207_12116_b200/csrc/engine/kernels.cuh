@@ -273,6 +273,35 @@ __device__ __forceinline__ bool unit_tell(unsigned sb, int k, int w) {
   return val < cur && satom_min(a, val) > val;
 }
 
+// Shared-memory joins without a return value.
+__device__ __forceinline__ void sred_min(unsigned a, int v) {
+  asm volatile("red.shared.min.s32 [%0], %1;" ::"r"(a), "r"(v) : "memory");
+}
+__device__ __forceinline__ void sred_max(unsigned a, int v) {
+  asm volatile("red.shared.max.s32 [%0], %1;" ::"r"(a), "r"(v) : "memory");
+}
+
+// Unit record under L.unit_fast (the value-range analysis bounds every word
+// it reads): all four words loaded at once, 32-bit arithmetic, and the tell
+// joined without a return value when it beats the target's snapshot (a
+// change this round, as in eval_ne_fast).  g2 (unit2 records) is the second
+// guard {a | b << 16, T}, or T = INT_MAX for none.
+__device__ __forceinline__ void eval_unit_fast(unsigned sb, int4 q, int2 g2, unsigned& ch) {
+  const unsigned tw = (unsigned)q.w & 0x7fffu, f = ((unsigned)q.w >> 15) & 0x7fffu;
+  const unsigned at = sb + (tw << 2);
+  const int va = sld(sb + (((unsigned)q.x & 0xffffu) << 2)), vb = sld(sb + (((unsigned)q.x >> 16) << 2));
+  const int vf = sld(sb + (f << 2)), cur = sld(at);
+  const int wa = sld(sb + (((unsigned)g2.x & 0xffffu) << 2)), wb = sld(sb + (((unsigned)g2.x >> 16) << 2));
+  if (va - vb <= q.y && wa - wb <= g2.y) {
+    const int val = (q.w & 0x40000000) ? q.z - vf : q.z + vf;
+    if (q.w < 0 ? val > cur : val < cur) {
+      if (q.w < 0) sred_max(at, val);
+      else sred_min(at, val);
+      ch = 1u;
+    }
+  }
+}
+
 __device__ __forceinline__ bool sjoin_max(unsigned a, int v) {
   const int cur = sld(a);
   return v > cur && satom_max(a, v) < v;
@@ -335,12 +364,6 @@ __device__ __forceinline__ unsigned long long eval_ne(unsigned sb, int4 q) {
 // beats its snapshot, all four are issued, the others as the join identity
 // (min with INT_MAX, max with INT_MIN): one branch region per record
 // instead of one per join.
-__device__ __forceinline__ void sred_min(unsigned a, int v) {
-  asm volatile("red.shared.min.s32 [%0], %1;" ::"r"(a), "r"(v) : "memory");
-}
-__device__ __forceinline__ void sred_max(unsigned a, int v) {
-  asm volatile("red.shared.max.s32 [%0], %1;" ::"r"(a), "r"(v) : "memory");
-}
 // Sets ch when a candidate beat its snapshot (inside the join branch, so
 // the flag costs nothing on the common no-change path).
 __device__ __forceinline__ void eval_ne_fast(unsigned sb, int4 q, unsigned& ch) {
@@ -762,18 +785,27 @@ __device__ __forceinline__ bool eval_other_families(const G& g, volatile int* S,
       for (int i = g.rank(); i < (int)L.n_reif; i += g.size()) ch |= eval_reif<false>(sb, tab.ld4(L.reif, i));
     }
     dbg_r(0);
-    for (int i = g.rank(); i < (int)L.n_unit1; i += g.size()) {
-      const int4 q = tab.ld4(L.unit1, i);
-      if (unit_guard(sb, q.x, q.y)) ch |= unit_tell(sb, q.z, q.w);
-    }
-    dbg_r(1);
-    for (int i = g.rank(); i < (int)L.n_unit2; i += g.size()) {
-      const int4 q = tab.ld4(L.unit2, i);
-      if (unit_guard(sb, q.x, q.y)) {
-        const int2 q2 = tab.ld2(L.unit2g, i);
-        if (unit_guard(sb, q2.x, q2.y)) ch |= unit_tell(sb, q.z, q.w);
+    if (L.unit_fast) {
+      unsigned uch = 0;
+      const int2 none = make_int2(0, INT_MAX);  // S[0] - S[0] <= INT_MAX: no second guard
+      for (int i = g.rank(); i < (int)L.n_unit1; i += g.size()) eval_unit_fast(sb, tab.ld4(L.unit1, i), none, uch);
+      for (int i = g.rank(); i < (int)L.n_unit2; i += g.size())
+        eval_unit_fast(sb, tab.ld4(L.unit2, i), tab.ld2(L.unit2g, i), uch);
+      ch |= uch != 0;
+    } else {
+      for (int i = g.rank(); i < (int)L.n_unit1; i += g.size()) {
+        const int4 q = tab.ld4(L.unit1, i);
+        if (unit_guard(sb, q.x, q.y)) ch |= unit_tell(sb, q.z, q.w);
+      }
+      for (int i = g.rank(); i < (int)L.n_unit2; i += g.size()) {
+        const int4 q = tab.ld4(L.unit2, i);
+        if (unit_guard(sb, q.x, q.y)) {
+          const int2 q2 = tab.ld2(L.unit2g, i);
+          if (unit_guard(sb, q2.x, q2.y)) ch |= unit_tell(sb, q.z, q.w);
+        }
       }
     }
+    dbg_r(1);
     for (int i = g.rank(); i < (int)L.n_small; i += g.size()) ch |= eval_small(S, T, L, i);
     dbg_r(2);
     if (L.n_rows) ch |= eval_rows(g, sb, tab, L);

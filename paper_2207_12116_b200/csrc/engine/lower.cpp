@@ -753,6 +753,30 @@ Lowered lower_model(const pccp_model& m) {
       read_fast[lbw] = read_fast[lbw + 1] = 1;
     }
   }
+  // unit records: guard words a, b (and the second guard's), tell source f
+  out.unit_ok = L.n_unit1 + L.n_unit2 > 0;
+  {
+    auto ok_word = [&](std::uint32_t w) {  // the constant-zero word Z = n_words is always fine
+      if (w == m.n_words) return true;
+      if (w > m.n_words || cls[w] == 2) return false;
+      read_fast[w] = 1;
+      return true;
+    };
+    auto scan = [&](std::uint32_t off, std::uint32_t n) {
+      for (std::uint32_t i = 0; i < n && out.unit_ok; ++i) {
+        const std::uint32_t x = static_cast<std::uint32_t>(B[off + 4 * i]);
+        const std::uint32_t w = static_cast<std::uint32_t>(B[off + 4 * i + 3]);
+        if (!ok_word(x & 0xffffu) || !ok_word(x >> 16) || !ok_word((w >> 15) & 0x7fffu)) out.unit_ok = false;
+        out.unit_k = std::max(out.unit_k, std::abs(std::int64_t{B[off + 4 * i + 2]}));
+      }
+    };
+    scan(L.unit1, L.n_unit1);
+    scan(L.unit2, L.n_unit2);
+    for (std::uint32_t i = 0; i < L.n_unit2 && out.unit_ok; ++i) {
+      const std::uint32_t x = static_cast<std::uint32_t>(B[L.unit2g + 2 * i]);
+      if (!ok_word(x & 0xffffu) || !ok_word(x >> 16)) out.unit_ok = false;
+    }
+  }
   out.reif_ok = L.n_reif > 0;
   for (std::uint32_t i = 0; i < L.n_reif && out.reif_ok; ++i) {
     const std::uint32_t xy = static_cast<std::uint32_t>(B[L.reif + 4 * i]);
@@ -849,9 +873,9 @@ Lowered lower_model(const pccp_model& m) {
 // a round performs at most r_aff of them: |v| <= max(B0, B1) + r_aff * kaff.
 // Decisions and the objective bound stay inside the box (+-1).
 void fast_paths(const Lowered& low, const std::int32_t* stores, std::size_t n_stores, std::size_t stride,
-                bool& ne_fast, bool& rows_fast, bool& reif_fast) {
-  ne_fast = rows_fast = reif_fast = false;
-  if ((!low.ne_ok && !low.rows_ok && !low.reif_ok) || !stores || !n_stores) return;
+                bool& ne_fast, bool& rows_fast, bool& reif_fast, bool& unit_fast) {
+  ne_fast = rows_fast = reif_fast = unit_fast = false;
+  if ((!low.ne_ok && !low.rows_ok && !low.reif_ok && !low.unit_ok) || !stores || !n_stores) return;
   const DeviceLayout& L = low.L;
   const std::uint32_t nw = L.n_words;
   std::vector<std::int32_t> w(nw);
@@ -882,6 +906,7 @@ void fast_paths(const Lowered& low, const std::int32_t* stores, std::size_t n_st
   if (bound1 >= lim) return;
   ne_fast = low.ne_ok && bound1 + low.kaff + 2 < lim;
   reif_fast = low.reif_ok && bound1 + low.reif_k + 2 < lim;
+  unit_fast = low.unit_ok && bound1 + low.unit_k + 2 < lim;
   if (low.rows_ok) {
     // |sum| <= S; the zeroing guard coef + sum - coef * v is <= 2 S + |coef|
     std::int64_t worst = 0;

@@ -75,6 +75,7 @@ struct DeviceLayout {
   std::uint32_t ne_fast;    // set per launch: value-range analysis proved the 32-bit NE path exact
   std::uint32_t rows_fast;  // set per launch: the same for the sum rows (fast_paths)
   std::uint32_t reif_fast;  // set per launch: the same for the reification records (fast_paths)
+  std::uint32_t unit_fast;  // set per launch: the same for the unit records (fast_paths)
 };
 
 
@@ -93,6 +94,8 @@ struct Lowered {
   bool rows_ok = false, ne_ok = false;       // every row term / NE word has class <= 1
   bool reif_ok = false;                      // every reification x/y bound has class <= 1
   std::int64_t reif_k = 0;                   // max |p|, |q| over the reifications
+  bool unit_ok = false;                      // every unit-record word read has class <= 1
+  std::int64_t unit_k = 0;                   // max |k| over the unit tells
   std::vector<std::int64_t> row_sum0, row_sum1;  // per row: sum |coef| over class-0 / class-1 terms
   std::vector<std::int32_t> slot_of_word;  // for diagnostics
 };
@@ -105,7 +108,7 @@ Lowered lower_model(const pccp_model& m);
 // when no NE evaluation can read a value outside (-2^30, 2^30), resp. every
 // row sum and zeroing guard fits in 32 bits.  lower.cpp states the argument.
 void fast_paths(const Lowered& low, const std::int32_t* stores, std::size_t n_stores, std::size_t stride,
-                bool& ne_fast, bool& rows_fast, bool& reif_fast);
+                bool& ne_fast, bool& rows_fast, bool& reif_fast, bool& unit_fast);
 
 // Host-side join of a decision into a store (Decision::as_join +
 // Store::join_in_place on an Interval, solver.hpp:20-23, store.cpp:51-63).

@@ -364,3 +364,19 @@ def test_value_range_analysis_large_domains(dom_hi, hengine):
     got = hengine.load(m).enumerate(depth_cap=9)
     for k in ("nodes", "failures", "solutions", "open_leaves", "hash_sum"):
         assert got[k] == want[k], (dom_hi, k, got[k], want[k])
+
+
+def test_enumerate_csp_depth12_without_fast_paths(golden):
+    """Config 3 through the widened unit/row/reification paths (PCCP_NO_FAST):
+    the same golden counts and hash-sum as the 32-bit paths."""
+    import os
+    from paper_2207_12116_b200 import Engine
+    g = golden["csp1"]["enumerate_d12"]
+    os.environ["PCCP_NO_FAST"] = "1"
+    try:
+        with Engine(0, hash=True) as e:
+            res = e.load(build("csp1")).enumerate(depth_cap=12)
+    finally:
+        del os.environ["PCCP_NO_FAST"]
+    for k in ("nodes", "failures", "solutions", "open_leaves", "hash_sum"):
+        assert res[k] == g[k], k
