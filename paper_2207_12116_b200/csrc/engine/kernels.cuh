@@ -846,7 +846,8 @@ __device__ bool propagate(const G& g, volatile int* S, unsigned sb, const Tab<TS
         const unsigned a = sb + 4u * (unsigned)tab.ld1(L.iv_lb, i);
         fl |= sld(a) > sld(a + 4);
       }
-      for (int i = g.rank(); i < (int)L.n_sc; i += g.size()) fl |= S[T[L.sc_w + i]] == T[L.sc_top + i];
+      for (int i = g.rank(); i < (int)L.n_sc; i += g.size())
+        fl |= sld(sb + 4u * (unsigned)tab.ld1(L.sc_w, i)) == tab.ld1(L.sc_top, i);
     }
     dbg_r(4);
     bool any_ch, any_fl;
