@@ -56,14 +56,17 @@ __device__ __forceinline__ unsigned long long join_objective(const G& g, volatil
     const int best = *(volatile int*)&C.G->incumbent;
     if (best != INT_MAX) moved = join_min(S, L.obj_lbw + 1, best - 1) ? 1 : 0;
   }
+  // Only the filtered rounds use the dirty mask; the eventless loop needs no
+  // broadcast (callers sync before propagating).
+  if (!L.filtered) return 0ull;
   return g.bcast0(moved) ? word_bit(L.obj_lbw + 1) : 0ull;
 }
 
 // SharedControl::should_stop (solver.cpp:68-76): stop flag, timeout, node limit.
-template <class G>
-__device__ __forceinline__ bool should_stop(const G& g, const SearchCtl& C) {
+// The limit checks of one materialisation, on the group's rank 0.
+__device__ __forceinline__ int stop_rank0(const SearchCtl& C) {
   int stop = 0;
-  if (g.rank() == 0) {
+  {
     Globals* Gl = C.G;
     stop = *(volatile int*)&Gl->stop;
     if (!stop && Gl->timeout_ns && globaltimer() - Gl->t0 >= Gl->timeout_ns) {
@@ -84,7 +87,12 @@ __device__ __forceinline__ bool should_stop(const G& g, const SearchCtl& C) {
       }
     }
   }
-  return g.bcast0(stop) != 0;
+  return stop;
+}
+
+template <class G>
+__device__ __forceinline__ bool should_stop(const G& g, const SearchCtl& C) {
+  return g.bcast0(g.rank() == 0 ? stop_rank0(C) : 0) != 0;
 }
 
 // The stop flag and the timeout only (no node reservation): checked by the
@@ -615,16 +623,18 @@ __device__ __forceinline__ void apply_pending(int* dst, int lbw_tag, int mid) {
 // shallowest pending node (parent fixed point + right decision, not yet
 // propagated) into the receiver's mailbox.  The receiver materialises and
 // counts that node itself, so every node is still processed exactly once.
+// Rank 0: claim one unit of hunger (1) or not (0).
+__device__ __forceinline__ int claim_donation_rank0(Globals* Gl) {
+  if (*(volatile int*)&Gl->hungry <= 0) return 0;
+  if (atomicAdd(&Gl->hungry, -1) > 0) return 1;
+  atomicAdd(&Gl->hungry, 1);
+  return 0;
+}
+
+// After a claim: take the receiver from the wait ring and hand it the
+// shallowest pending node.
 template <class G>
-__device__ __forceinline__ void maybe_donate(const G& g, const SearchParams& P, Globals* Gl, int* stk, int nw,
-                                             int& bot, int sp) {
-  if (sp - bot < 2) return;
-  int give = 0;
-  if (g.rank() == 0 && *(volatile int*)&Gl->hungry > 0) {
-    if (atomicAdd(&Gl->hungry, -1) > 0) give = 1;
-    else atomicAdd(&Gl->hungry, 1);
-  }
-  if (!g.bcast0(give)) return;
+__device__ __forceinline__ void hand_over(const G& g, const SearchParams& P, Globals* Gl, int* stk, int nw, int& bot) {
   int recv = -1;
   if (g.rank() == 0) {
     const unsigned h = atomicAdd(&Gl->wait_head, 1u) % (unsigned)P.n_groups;
@@ -653,7 +663,7 @@ __device__ __forceinline__ void maybe_donate(const G& g, const SearchParams& P, 
 // k*shard_count) and explores it depth-first, left branch first (dfs,
 // solver.cpp:122-146).  A branching node pushes (its fixed point, right
 // decision) and descends left in place; a leaf pops.  When the queue is
-// empty, idle groups are fed by donations (maybe_donate).
+// empty, idle groups are fed by donations (claim_donation_rank0, hand_over).
 template <class G, bool TS, int F>
 __global__ void __launch_bounds__(MaxThreads<G, F>::value, MaxThreads<G, F>::min_blocks) k_search(Model M, SearchCtl C, SearchParams P) {
   const Frame f = frame(M);
@@ -730,10 +740,17 @@ __global__ void __launch_bounds__(MaxThreads<G, F>::value, MaxThreads<G, F>::min
       g.sync();
     }
     for (;;) {
-      if (P.balance) maybe_donate(g, P, Gl, stk, nw, bot, sp);
+      // one broadcast per node for the donation claim and the limit checks
+      int ctl = 0;
+      if (g.rank() == 0) {
+        if (P.balance && sp - bot >= 2) ctl |= claim_donation_rank0(Gl) << 1;
+        if (need_prop) ctl |= stop_rank0(C);
+      }
+      ctl = g.bcast0(ctl);
+      if (ctl & 2) hand_over(g, P, Gl, stk, nw, bot);
       int lbw = 0, mid = 0, e;
       if (need_prop) {
-        if (should_stop(g, C)) {
+        if (ctl & 1) {
           abandoned = true;
           break;
         }
@@ -773,7 +790,7 @@ __global__ void __launch_bounds__(MaxThreads<G, F>::value, MaxThreads<G, F>::min
         }
         ++sp;
         ++depth;
-        g.sync();
+        // rank 0 made the decision join and makes the objective join: one sync
         dirty = word_bit(right_first ? lbw : lbw + 1) | join_objective(g, S, L, C);
         g.sync();
         need_prop = true;
@@ -792,8 +809,7 @@ __global__ void __launch_bounds__(MaxThreads<G, F>::value, MaxThreads<G, F>::min
       }
       depth = ent[nw + 2] + 1;
       dirty = word_bit(tag < 0 ? (tag & 0x7fffffff) + 1 : tag);
-      g.sync();
-      dirty |= join_objective(g, S, L, C);
+      dirty |= join_objective(g, S, L, C);  // rank 0, after its decision join
       g.sync();
       need_prop = true;
     }
