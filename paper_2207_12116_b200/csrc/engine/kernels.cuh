@@ -112,6 +112,11 @@ struct WarpGroup {
   }
   __device__ __forceinline__ bool any(bool p) const { return __any_sync(kFull, p); }
   __device__ __forceinline__ unsigned long long min_u64(unsigned long long v) const {
+    // all keys below 2^32 (small widths / bounds, or none): one redux.min
+    if (__all_sync(kFull, (v >> 32) == 0ull || v == ~0ull)) {
+      const unsigned m = __reduce_min_sync(kFull, v == ~0ull ? 0xffffffffu : (unsigned)v);
+      return m == 0xffffffffu ? ~0ull : (unsigned long long)m;
+    }
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) {
       const unsigned long long u = __shfl_xor_sync(kFull, v, o);
