@@ -193,9 +193,15 @@ def time_to_optimum(local, rank, world, dist):
         if world > 1:
             t_first = min(x for x in _gather_obj(dist, t_first))
             t_proof = max(_gather_obj(dist, t_proof))
+        st = local_r.stats
+        b_alg = eng.lowering_info()["alg_bytes_per_eval"]
+        sm_mhz = load_peaks().get("sm_max_mhz", 1965.0)
+        ev_s = st["search_evals"] / (st["kernel_ms"] / 1e3) if st["kernel_ms"] > 0 else 0.0
         out[str(seed)] = {"status": status, "objective": obj, "valid": bool(ok),
                           "matches_reference": obj == TTO_OPTIMA[seed], "t_first_optimal_ms": t_first,
                           "t_proof_ms": t_proof, "nodes": local_r.stats["nodes"],
+                          "k_search": {"ms": st["kernel_ms"], "evals_per_s": ev_s,
+                                       "smem_frac_alg": ev_s * b_alg / (148 * 128 * sm_mhz * 1e6)},
                           "cpu_reference_w1_s": TTO_CPU_W1_S[seed]}
     eng.close()
     return {"config": "rcpsp 30 tasks x 4 resources, random_patterson(mt19937_64(seed)), minimise makespan",
@@ -304,6 +310,11 @@ def enumeration_configs(local, rank, world, dist, cpu, threads):
             nodes = runs[-1]["nodes"]
         d = {"nodes": nodes, "device_ms": statistics.median(ms), "nodes_per_s": nodes / (statistics.median(ms) / 1e3),
              "parity": all(int(hr[k]) == v for k, v in exp.items())}
+        if world == 1:
+            r = runs[-1]
+            if r["kernel_ms"] > 0:
+                ev_s = r["search_evals"] / (r["kernel_ms"] / 1e3)
+                d["k_search"] = {"ms": r["kernel_ms"], "decompose_ms": r["decompose_ms"], "evals_per_s": ev_s}
         if cpu:
             c = cpu_reference(dict(w, workload=name), 3.0, threads)
             d["cpu_reference"] = {"nodes_per_s": c["value"], "threads": c["cores"], "kind": c["kind"],
