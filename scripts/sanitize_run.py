@@ -1,6 +1,7 @@
 """A CI-sized workload for compute-sanitizer (memcheck / synccheck / racecheck):
 Q8 enumeration (warp groups), CSP depth 10 (CTA groups, rows), an RCPSP10
-solve (fused reifications, incumbent, donations) and a propagate batch."""
+solve (fused reifications, incumbent, donations), a propagate batch, a
+primal-phase solve and a randomised-order enumeration."""
 import os
 import sys
 
@@ -19,4 +20,12 @@ with Engine(0, eps_factor=1) as e:
     assert s.status == "OPTIMAL" and m.check_solution(s.best_words), s.status
     out, failed, _ = e.propagate_batch([m.bottom()] * 4)
     print("rcpsp10", s.objective, s.stats["nodes"], failed.tolist())
+with Engine(0, eps_factor=1, primal_ms=300) as e:  # primal segments, restarts, keep-incumbent resets
+    m = Model.rcpsp_random(2, 10, 2)
+    s = e.load(m).solve(timeout_s=60)  # the sanitizers slow the search down by orders of magnitude
+    assert s.status in ("OPTIMAL", "SAT") and m.check_solution(s.best_words), s.status
+    print("primal", s.objective, s.primal)
+with Engine(0, eps_factor=1, var_order=3) as e:  # randomised branching
+    r = e.load(Model.nqueens(6)).enumerate()
+    assert r["solutions"] == 4, r
 print("sanitize workload ok")
