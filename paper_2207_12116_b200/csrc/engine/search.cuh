@@ -99,12 +99,19 @@ __device__ __forceinline__ bool should_stop(const G& g, const SearchCtl& C) {
 // EPS decomposition per parent, as decompose() checks should_stop
 // (solver.cpp:189).
 template <class G>
-__device__ __forceinline__ bool time_stop(const G& g, const SearchCtl& C) {
+__device__ __forceinline__ bool time_stop(const G& g, const SearchCtl& C, unsigned reserve = 0) {
   int stop = 0;
   if (g.rank() == 0) {
     Globals* Gl = C.G;
     stop = *(volatile int*)&Gl->stop;
     if (!stop && Gl->timeout_ns && globaltimer() - Gl->t0 >= Gl->timeout_ns) {
+      atomicCAS(&Gl->stop, 0, 1);
+      stop = 1;
+    }
+    // the materialisations about to happen count against the node limit, as
+    // every materialisation does in the reference (solver.cpp:68-76, 100)
+    if (!stop && reserve && Gl->node_limit != ~0ull &&
+        atomicAdd(&Gl->nodes_reserved, (unsigned long long)reserve) + reserve > Gl->node_limit) {
       atomicCAS(&Gl->stop, 0, 1);
       stop = 1;
     }
@@ -343,6 +350,7 @@ __global__ void __launch_bounds__(MaxThreads<G, F>::value, MaxThreads<G, F>::min
   apply_fold(g, S, f.T, M.L);
   g.sync();
   join_objective(g, S, M.L, C);
+  if (g.rank() == 0 && C.G->node_limit != ~0ull) atomicAdd(&C.G->nodes_reserved, 1ull);  // the root's materialisation
   g.sync();
   int r = 0;
   const bool failed = propagate<G, TS, F>(g, S, sb, tab, M.L, r);
@@ -408,7 +416,7 @@ __device__ void expand_level(const G& g, volatile int* S, unsigned sb, const Tab
   const int gid = blockIdx.x * GroupOf<G>::per_cta() + GroupOf<G>::in_cta();
   const int ng = gridDim.x * GroupOf<G>::per_cta();
   for (int p = gid; p < n_par; p += ng) {
-    if (time_stop(g, C)) {  // abandoned parent: its subtree is unexplored
+    if (time_stop(g, C, 2)) {  // abandoned parent: its subtree is unexplored
       if (g.rank() == 0) {
         C.G->incomplete = 1;
         flags[2 * p] = flags[2 * p + 1] = 0;

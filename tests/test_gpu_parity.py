@@ -380,3 +380,26 @@ def test_enumerate_csp_depth12_without_fast_paths(golden):
         del os.environ["PCCP_NO_FAST"]
     for k in ("nodes", "failures", "solutions", "open_leaves", "hash_sum"):
         assert res[k] == g[k], k
+
+
+@pytest.mark.parametrize("limit", [1, 7, 500, 5000])
+def test_node_limit_bounds_materialisations(limit, golden):
+    """SharedControl's node limit (solver.cpp:68-76) counts every materialisation,
+    the root and the decomposition's included: the search stops after about
+    `limit` nodes (groups overshoot by at most one node each) and reports a
+    non-exhausted run; a limit above the tree size changes nothing."""
+    from paper_2207_12116_b200 import Engine
+    with Engine(0) as e:
+        e.load(build("nqueens10"))
+        r = e.enumerate(node_limit=limit)
+        assert not r["exhausted"]
+        assert r["nodes"] <= limit + 2 * 4736, (limit, r["nodes"])
+        full = e.enumerate(node_limit=10**9)
+        assert full["exhausted"] and full["nodes"] == golden["nqueens10"]["enumerate"]["nodes"]
+        m = build("rcpsp30_s1")
+        e.load(m)
+        s = e.solve(node_limit=limit)
+        assert s.status in ("SAT", "UNKNOWN")
+        assert s.stats["nodes"] <= limit + 2 * 4736
+        if s.objective is not None:
+            assert m.check_solution(s.best_words)
