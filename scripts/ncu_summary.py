@@ -24,6 +24,7 @@ METRICS = {
     "l1tex__data_pipe_lsu_wavefronts_mem_shared_op_atom.sum": "smem_atomic_wavefronts",
     "l1tex__data_bank_conflicts_pipe_lsu_mem_shared.sum": "smem_bank_conflicts",
     "lts__t_bytes.sum": "l2_bytes",
+    "lts__t_sectors.sum": "l2_sectors",
     "smsp__issue_active.avg.pct_of_peak_sustained_active": "issue_active_pct",
     "sm__warps_active.avg.pct_of_peak_sustained_active": "warps_active_pct",
     "launch__registers_per_thread": "registers_per_thread",
@@ -70,6 +71,13 @@ def main():
                 else:
                     d[short] = v
         d["dram_bytes_per_launch"] = d.get("dram_read_bytes", 0) + d.get("dram_write_bytes", 0)
+        if "l2_sectors" in d:
+            d["l2_bytes_per_launch"] = d["l2_sectors"] * 32
+        t = d.get("duration_ms", 0) / 1e3
+        if t > 0:  # achieved bandwidths of the launch (cold-cache, serialised replay)
+            d["achieved_gbs"] = {"smem": d.get("smem_wavefronts", 0) * 128 / t / 1e9,
+                                 "l2": d.get("l2_bytes_per_launch", 0) / t / 1e9,
+                                 "dram": d["dram_bytes_per_launch"] / t / 1e9}
         summ.setdefault(a.workload, {})[name] = d
         det = subprocess.run(["ncu", "-i", a.rep, "--page", "details"], capture_output=True, text=True).stdout
         with open(os.path.join(PROF, f"{a.tag}_{name}_details.txt"), "w") as f:
