@@ -117,11 +117,15 @@ typedef struct pccp_gpu_cfg {
                             the reference (BranchStrategy, solver.hpp:89-91, has candidates only):
                             a different tree, so node counts differ; optima and UNSAT do not. */
   int32_t primal_ms;     /* pccp_gpu_solve only, > 0: a primal phase of at most this many ms with
-                            var_order 1 runs first, restarted from the root under obj <= best-1
+                            var_order 2 runs first, restarted from the root under obj <= best-1
                             whenever it improved and then stalled (env PCCP_PRIMAL_STALL_MS,
                             default max(100, primal_ms/20)); its incumbent (and, if one segment
                             exhausts its tree, its proof) carries into the exact phase, which
                             searches the cfg's var_order tree under obj <= best-1.  0 = off. */
+  int32_t audit_nodes;   /* > 0: the persistent search records the store before and after the
+                            fixed point of up to this many nodes (every 2^audit_shift-th
+                            materialisation), for pccp_gpu_audit.  0 = off. */
+  int32_t audit_shift;
 } pccp_gpu_cfg;
 
 typedef struct pccp_limits {
@@ -228,6 +232,14 @@ int pccp_gpu_attach_peers(pccp_gpu_ctx* ctx, const uint8_t* handles64, int32_t n
  * and each context pushes improvements into every other context's cell.
  * Contexts on the same device are linked directly. */
 int pccp_gpu_link_peers(pccp_gpu_ctx* const* ctxs, int32_t n);
+
+/* The node audit of the last enumerate/solve call (cfg.audit_nodes > 0):
+ * pre[k] is a node's store as materialised (parent fixed point + decision +
+ * objective bound), post[k] the engine's result for it and failed[k] its
+ * status, so a caller can recompute run_sequential(pre[k]) (engine.cpp:13-32)
+ * and compare.  pre/post hold cfg.audit_nodes x n_words int32; *n_out gets
+ * the number of samples taken. */
+int pccp_gpu_audit(pccp_gpu_ctx* ctx, int32_t* pre, int32_t* post, uint8_t* failed, uint32_t* n_out);
 
 /* Information about the lowered model (device tables), for roofline accounting. */
 typedef struct pccp_lowering_info {

@@ -51,6 +51,8 @@ class PccpGpuCfg(C.Structure):
         ("value_order", C.c_int32),
         ("var_order", C.c_int32),
         ("primal_ms", C.c_int32),
+        ("audit_nodes", C.c_int32),
+        ("audit_shift", C.c_int32),
     ]
 
 
@@ -152,6 +154,7 @@ def lib():
         "pccp_gpu_solve": (C.c_int, [vp, vp, P(PccpLimits), P(PccpSolveResult), vp]),
         "pccp_gpu_incumbent_handle": (C.c_int, [vp, vp]),
         "pccp_gpu_attach_peers": (C.c_int, [vp, vp, i32, i32]),
+        "pccp_gpu_audit": (C.c_int, [vp, vp, vp, vp, vp]),
         # host model builder
         "pccp_host_last_error": (C.c_char_p, []),
         "pccp_host_new": (vp, []),

@@ -113,8 +113,9 @@ struct pccp_gpu_ctx {
   int table_in_smem = 0;
   int ne_only = 0;  // lowered to NE records (and fold tells) only: the kNeOnly kernels
   int dec_ctas = 0;  // grid of the persistent decomposition kernel
+  std::uint32_t audit_taken = 0;  // node-audit samples of the last search
 
-  DBuf<int> fa, fb, ia, ib, stack, best, io, mailbox, waitq, dec, chunk;
+  DBuf<int> fa, fb, ia, ib, stack, best, io, mailbox, waitq, dec, chunk, audit;
   DBuf<unsigned char> flags, st;
   DBuf<unsigned> rnd;
   dev::Globals* G = nullptr;
@@ -309,6 +310,15 @@ void run_search(pccp_gpu_ctx* c, int mode, const int32_t* root_words, int depth_
   C.count = shard_index == 0 ? 1 : 0;  // the decomposition runs on every GPU, counted once
   c->best.ensure((size_t)std::max(nw, 1));
   C.best_store = c->best.p;
+  if (c->cfg.audit_nodes > 0) {
+    const size_t k = (size_t)c->cfg.audit_nodes;
+    c->audit.ensure(2 * k * (size_t)std::max(nw, 1) + (k + 3) / 4);
+    C.audit_pre = c->audit.p;
+    C.audit_post = c->audit.p + k * (size_t)std::max(nw, 1);
+    C.audit_failed = reinterpret_cast<unsigned char*>(c->audit.p + 2 * k * (size_t)std::max(nw, 1));
+    C.audit_n = c->cfg.audit_nodes;
+    C.audit_shift = std::clamp(c->cfg.audit_shift, 0, 40);
+  }
 
   reset_globals(c, lim, keep_incumbent, stall_ns);
   // the root store is frontier buffer 0 of the decomposition (capacity 2*target)
@@ -506,6 +516,12 @@ void run_search(pccp_gpu_ctx* c, int mode, const int32_t* root_words, int depth_
     out.kernel_ms = ms;
   }
   out.elapsed_ms = now_ms() - t_start;
+  c->audit_taken = c->cfg.audit_nodes > 0
+                       ? (std::uint32_t)std::min<unsigned long long>(
+                             (out.g.audit_seen + (1ull << std::clamp(c->cfg.audit_shift, 0, 40)) - 1) >>
+                                 std::clamp(c->cfg.audit_shift, 0, 40),
+                             (unsigned long long)c->cfg.audit_nodes)
+                       : 0u;
   if (out.g.stop == 2) {
     if (out.g.error_code == 1) throw std::runtime_error("branch: a candidate variable is unbounded");
     throw LimitError("DFS stack capacity exceeded");
@@ -637,6 +653,7 @@ void pccp_gpu_close(pccp_gpu_ctx* c) {
   c->waitq.release();
   c->dec.release();
   c->chunk.release();
+  c->audit.release();
   c->best.release();
   c->io.release();
   c->flags.release();
@@ -926,6 +943,24 @@ int pccp_gpu_attach_peers(pccp_gpu_ctx* c, const uint8_t* handles, int32_t n, in
       c->d_peers.ensure(ptrs.size());
       CK(cudaMemcpy(c->d_peers.p, ptrs.data(), ptrs.size() * sizeof(int*), cudaMemcpyHostToDevice));
     }
+    return PCCP_OK;
+  });
+}
+
+int pccp_gpu_audit(pccp_gpu_ctx* c, int32_t* pre, int32_t* post, uint8_t* failed, uint32_t* n_out) {
+  return api([&] {
+    check_loaded(c);
+    if (!n_out) throw ArgError("null argument");
+    *n_out = 0;
+    if (c->cfg.audit_nodes <= 0 || !c->audit.p) return PCCP_OK;
+    const size_t nw = std::max<size_t>(c->low.L.n_words, 1), k = (size_t)c->cfg.audit_nodes, n = c->audit_taken;
+    if (n && (!pre || !post || !failed)) throw ArgError("null buffer");
+    if (n) {
+      CK(cudaMemcpy(pre, c->audit.p, n * nw * 4, cudaMemcpyDeviceToHost));
+      CK(cudaMemcpy(post, c->audit.p + k * nw, n * nw * 4, cudaMemcpyDeviceToHost));
+      CK(cudaMemcpy(failed, c->audit.p + 2 * k * nw, n, cudaMemcpyDeviceToHost));
+    }
+    *n_out = (uint32_t)n;
     return PCCP_OK;
   });
 }

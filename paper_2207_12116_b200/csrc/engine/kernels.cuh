@@ -62,6 +62,7 @@ struct Globals {
   unsigned long long stall_ns;     // 0: off
   unsigned long long last_impr_ns; // since t0
   int stalled;
+  unsigned long long audit_seen;   // materialisations offered to the node audit
 };
 
 __device__ __forceinline__ unsigned long long globaltimer() {

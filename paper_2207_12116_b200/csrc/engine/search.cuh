@@ -23,6 +23,12 @@ struct SearchCtl {
   int hash;              // accumulate the fixed-point hash-sum
   int depth_cap;         // < 0: none
   int count;             // accumulate counters (EPS on shard 0 only)
+  // node audit (pccp_gpu_audit): every 2^audit_shift-th materialisation of the
+  // persistent search, up to audit_n samples of (pre, post, failed)
+  int* audit_pre;
+  int* audit_post;
+  unsigned char* audit_failed;
+  int audit_n, audit_shift;
 };
 
 // Per-group counters, kept in shared memory (Frame::cnt) and updated by the
@@ -762,8 +768,23 @@ __global__ void __launch_bounds__(MaxThreads<G, F>::value, MaxThreads<G, F>::min
           abandoned = true;
           break;
         }
+        int slot = -1;
+        if (C.audit_n > 0) {  // claim an audit slot for this materialisation
+          int k = -1;
+          if (g.rank() == 0) {
+            const unsigned long long t = atomicAdd(&Gl->audit_seen, 1ull);
+            if ((t & ((1ull << C.audit_shift) - 1ull)) == 0ull && (t >> C.audit_shift) < (unsigned long long)C.audit_n)
+              k = (int)(t >> C.audit_shift);
+          }
+          slot = g.bcast0(k);
+          if (slot >= 0) copy_out(g, C.audit_pre + (size_t)slot * nw, S, nw);
+        }
         int r = 0;
         const bool failed = propagate<G, TS, F>(g, S, sb, tab, L, r, dirty);
+        if (slot >= 0) {
+          copy_out(g, C.audit_post + (size_t)slot * nw, S, nw);
+          if (g.rank() == 0) C.audit_failed[slot] = failed ? 1 : 0;
+        }
         if (g.rank() == 0) {
           ++cnt.nodes;
           cnt.rounds += (unsigned long long)r;

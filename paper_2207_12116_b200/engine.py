@@ -48,10 +48,12 @@ class Engine:
 
     def __init__(self, device: int = 0, *, group_threads: int = 0, groups_per_cta: int = 0, ctas_per_sm: int = 0,
                  eps_factor: int = 0, shard_index: int = 0, shard_count: int = 1, hash: bool = False,
-                 value_order: int = -1, var_order: int = 0, primal_ms: int = 0):
+                 value_order: int = -1, var_order: int = 0, primal_ms: int = 0, audit_nodes: int = 0,
+                 audit_shift: int = 0):
         L = N.lib()
         self.cfg = N.PccpGpuCfg(device, group_threads, groups_per_cta, ctas_per_sm, eps_factor, shard_index,
-                                shard_count, int(hash), 0, value_order, var_order, primal_ms)
+                                shard_count, int(hash), 0, value_order, var_order, primal_ms, audit_nodes,
+                                audit_shift)
         h = C.c_void_p()
         N.check(L.pccp_gpu_open(C.byref(self.cfg), C.byref(h)))
         self._h = h
@@ -144,6 +146,16 @@ class Engine:
         return SolveResult(N.STATUS_NAMES[res.status], res.objective if has else None, _stats(res.stats),
                            best[: self.tables.n_words] if has == 1 else None, imp, best_on_peer=has == 2,
                            primal=primal)
+
+    def audit(self):
+        """(pre, post, failed) of the nodes the last search sampled (cfg audit_nodes)."""
+        k, nw = max(self.cfg.audit_nodes, 1), self.tables.n_words
+        pre = np.zeros((k, nw), np.int32)
+        post = np.zeros((k, nw), np.int32)
+        fl = np.zeros(k, np.uint8)
+        n = C.c_uint32(0)
+        N.check(N.lib().pccp_gpu_audit(self._h, _vp(pre), _vp(post), _vp(fl), C.byref(n)))
+        return pre[: n.value], post[: n.value], fl[: n.value].astype(bool)
 
     # ---- multi-GPU incumbent sharing
     def incumbent_handle(self) -> bytes:
