@@ -157,6 +157,7 @@ void set_smem_attrs(size_t smem) {
   CK(cudaFuncSetAttribute(dev::k_root<Gp, TS, F>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   CK(cudaFuncSetAttribute(dev::k_decompose<Gp, TS, F>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   CK(cudaFuncSetAttribute(dev::k_search<Gp, TS, F>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  CK(cudaFuncSetAttribute(dev::k_search<Gp, TS, F, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
 }
 
 template <class Gp, bool TS, int F>
@@ -495,7 +496,8 @@ void run_search(pccp_gpu_ctx* c, int mode, const int32_t* root_words, int depth_
     if (const char* vo = std::getenv("PCCP_VALUE_ORDER")) P.value_order = std::atoi(vo);
     P.waitq = c->waitq.p;
     C.count = 1;
-    dev::k_search<Gp, TS, F><<<c->ctas, c->block, c->smem, c->stream>>>(M, C, P);
+    if (C.audit_n > 0) dev::k_search<Gp, TS, F, true><<<c->ctas, c->block, c->smem, c->stream>>>(M, C, P);
+    else dev::k_search<Gp, TS, F><<<c->ctas, c->block, c->smem, c->stream>>>(M, C, P);
     CK(cudaGetLastError());
     ++c->launches;
     searched = true;

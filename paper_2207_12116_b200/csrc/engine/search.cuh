@@ -678,7 +678,9 @@ __device__ __forceinline__ void hand_over(const G& g, const SearchParams& P, Glo
 // solver.cpp:122-146).  A branching node pushes (its fixed point, right
 // decision) and descends left in place; a leaf pops.  When the queue is
 // empty, idle groups are fed by donations (claim_donation_rank0, hand_over).
-template <class G, bool TS, int F>
+// Audit: the node-audit instantiation (pccp_gpu_audit), launched only when
+// samples are requested, so the production kernel carries no audit code.
+template <class G, bool TS, int F, bool Audit = false>
 __global__ void __launch_bounds__(MaxThreads<G, F>::value, MaxThreads<G, F>::min_blocks) k_search(Model M, SearchCtl C, SearchParams P) {
   const Frame f = frame(M);
   const G g = GroupOf<G>::make(f);
@@ -769,7 +771,7 @@ __global__ void __launch_bounds__(MaxThreads<G, F>::value, MaxThreads<G, F>::min
           break;
         }
         int slot = -1;
-        if (C.audit_n > 0) {  // claim an audit slot for this materialisation
+        if constexpr (Audit) {  // claim an audit slot for this materialisation
           int k = -1;
           if (g.rank() == 0) {
             const unsigned long long t = atomicAdd(&Gl->audit_seen, 1ull);
@@ -781,9 +783,11 @@ __global__ void __launch_bounds__(MaxThreads<G, F>::value, MaxThreads<G, F>::min
         }
         int r = 0;
         const bool failed = propagate<G, TS, F>(g, S, sb, tab, L, r, dirty);
-        if (slot >= 0) {
-          copy_out(g, C.audit_post + (size_t)slot * nw, S, nw);
-          if (g.rank() == 0) C.audit_failed[slot] = failed ? 1 : 0;
+        if constexpr (Audit) {
+          if (slot >= 0) {
+            copy_out(g, C.audit_post + (size_t)slot * nw, S, nw);
+            if (g.rank() == 0) C.audit_failed[slot] = failed ? 1 : 0;
+          }
         }
         if (g.rank() == 0) {
           ++cnt.nodes;
