@@ -10,6 +10,7 @@ import csv
 import io
 import json
 import os
+import shutil
 import subprocess
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
@@ -101,8 +102,7 @@ def main():
                     "cold-cache, serialised launches: compare shares, not absolutes\n\n")
             for k, (n, t) in sorted(agg.items(), key=lambda x: -x[1][1]):
                 f.write(f"{k:70s} {n:5d} launches {t / 1e6:10.3f} ms {100 * t / tot:6.2f}%\n")
-        os.replace(a.launches, os.path.join(PROF, f"{a.tag}_launches.csv")) if not os.path.exists(
-            os.path.join(PROF, f"{a.tag}_launches.csv")) else None
+        shutil.copyfile(a.launches, os.path.join(PROF, f"{a.tag}_launches.csv"))
 
 
 if __name__ == "__main__":
