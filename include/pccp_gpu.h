@@ -270,6 +270,12 @@ int pccp_gpu_lowering_info(pccp_gpu_ctx* ctx, pccp_lowering_info* out);
  * constraints, filtered-rounds flag, fused reifications. */
 int pccp_lower_only(const pccp_model* model, pccp_lowering_info* out, uint32_t* shape_counts);
 
+/* Host-only: the value-range analysis (lower.cpp fast_paths) for `n` input
+ * stores of the lowered model: *mask gets bit 0 NE, bit 1 sum rows, bit 2
+ * reifications, bit 3 unit records = the families whose 32-bit path the
+ * engine would take for these inputs (diagnostics and tests). */
+int pccp_lower_fast_paths(const pccp_model* model, const int32_t* stores, uint32_t n, uint32_t* mask);
+
 #ifdef __cplusplus
 }
 #endif

@@ -751,6 +751,17 @@ int pccp_lower_only(const pccp_model* m, pccp_lowering_info* o, uint32_t* shape_
   });
 }
 
+int pccp_lower_fast_paths(const pccp_model* m, const int32_t* stores, uint32_t n, uint32_t* mask) {
+  return api([&] {
+    if (!m || !mask || (n && !stores)) throw ArgError("null argument");
+    const Lowered low = lower_model(*m);
+    bool ne = false, rows = false, reif = false, unit = false;
+    fast_paths(low, stores, n, low.L.n_words, ne, rows, reif, unit);
+    *mask = (ne ? 1u : 0u) | (rows ? 2u : 0u) | (reif ? 4u : 0u) | (unit ? 8u : 0u);
+    return PCCP_OK;
+  });
+}
+
 int pccp_gpu_propagate_batch(pccp_gpu_ctx* c, const int32_t* in, uint32_t n, int32_t* out, uint8_t* status,
                              uint32_t* rounds) {
   return api([&] {

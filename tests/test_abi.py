@@ -73,3 +73,34 @@ def test_lowering_rejects_malformed_tables():
         L = N.lib()
         s, keep = bad.as_struct()
         N.check(L.pccp_lower_only(C.byref(s), C.byref(N.PccpLoweringInfo()), None))
+
+
+def fast_mask(m, stores):
+    L = N.lib()
+    L.pccp_lower_fast_paths.argtypes = [C.POINTER(N.PccpModel), C.c_void_p, C.c_uint32, C.c_void_p]
+    s, keep = m.tables().as_struct()
+    a = np.ascontiguousarray(stores, np.int32).reshape(-1, m.tables().n_words)
+    out = np.zeros(1, np.uint32)
+    N.check(L.pccp_lower_fast_paths(C.byref(s), a.ctypes.data_as(C.c_void_p), a.shape[0],
+                                    out.ctypes.data_as(C.c_void_p)))
+    return int(out[0])
+
+
+def test_value_range_analysis_decisions():
+    """lower.cpp fast_paths: the benchmark models take the 32-bit paths from their
+    bottom stores; unbounded or huge inputs, and domains whose sums could pass
+    2^30, fall back to the widened int64 arithmetic (command.cpp:11-27)."""
+    NE, ROWS, REIF, UNIT = 1, 2, 4, 8
+    q = Model.nqueens(14)
+    assert fast_mask(q, q.bottom()) == NE
+    r = Model.rcpsp_random(1, 30, 4)
+    assert fast_mask(r, r.bottom()) == ROWS | REIF | UNIT
+    c = Model.random_csp(1)
+    assert fast_mask(c, c.bottom()) == ROWS | UNIT
+    # a store whose words sit near the sentinels: everything widened
+    b = q.bottom().copy()
+    b[:] = 2**30
+    assert fast_mask(q, b) == 0
+    # domains large enough that a row sum could pass 2^30: rows widened, units not
+    big = Model.random_csp(1, dom_hi=10**8)
+    assert fast_mask(big, big.bottom()) & ROWS == 0
