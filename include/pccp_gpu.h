@@ -156,6 +156,10 @@ typedef struct pccp_stats {
   double device_ms;     /* device time of the whole call (CUDA events on the engine stream) */
   uint64_t bfs_levels;  /* EPS decomposition levels */
   uint64_t donations;   /* subtrees handed from busy to idle groups (dynamic load balancing) */
+  uint64_t rematerialised; /* nodes materialised a second time: EPS frontier nodes re-propagated under
+                              the current bound, as solve_parallel's workers re-materialise their
+                              subproblem roots (solver.cpp:266-268); distinct tree nodes = nodes -
+                              rematerialised */
 } pccp_stats;
 
 typedef struct pccp_enum_result {

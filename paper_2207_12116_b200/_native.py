@@ -81,6 +81,7 @@ class PccpStats(C.Structure):
         ("device_ms", C.c_double),
         ("bfs_levels", C.c_uint64),
         ("donations", C.c_uint64),
+        ("rematerialised", C.c_uint64),
     ]
 
 

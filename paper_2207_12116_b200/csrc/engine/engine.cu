@@ -556,6 +556,7 @@ void fill_stats(const pccp_gpu_ctx* c, const RunOut& r, pccp_stats& s) {
   s.device_ms = r.device_ms;
   s.bfs_levels = r.levels;
   s.donations = r.g.donations;
+  s.rematerialised = r.g.rematerialised;
 }
 
 // Counters of consecutive searches of one call (primal segments, exact
@@ -572,6 +573,7 @@ void merge_run(RunOut& acc, const RunOut& r, bool first) {
   g.rounds += acc.g.rounds;
   g.max_depth = std::max(g.max_depth, acc.g.max_depth);
   g.donations += acc.g.donations;
+  g.rematerialised += acc.g.rematerialised;
   acc.g = g;
   acc.bfs_rounds += r.bfs_rounds;
   acc.decompose_ms += r.decompose_ms;

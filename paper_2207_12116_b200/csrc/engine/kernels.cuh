@@ -63,6 +63,7 @@ struct Globals {
   unsigned long long last_impr_ns; // since t0
   int stalled;
   unsigned long long audit_seen;   // materialisations offered to the node audit
+  unsigned long long rematerialised;  // frontier nodes materialised again by the search (mode 1)
 };
 
 __device__ __forceinline__ unsigned long long globaltimer() {

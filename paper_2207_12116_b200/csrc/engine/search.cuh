@@ -748,6 +748,7 @@ __global__ void __launch_bounds__(MaxThreads<G, F>::value, MaxThreads<G, F>::min
     }
     int sp = 0, bot = 0;
     bool abandoned = false;
+    bool remat = need_prop && dirty != kAllDirty;  // a frontier node re-materialised under the bound (mode 1)
     // Enumeration: a frontier node was counted and classified during the
     // decomposition.  Minimisation: re-materialise it with the current bound,
     // as dfs() does for its subproblem root.  A donated node is unpropagated.
@@ -793,7 +794,9 @@ __global__ void __launch_bounds__(MaxThreads<G, F>::value, MaxThreads<G, F>::min
           ++cnt.nodes;
           cnt.rounds += (unsigned long long)r;
           if ((unsigned long long)depth > cnt.maxd) cnt.maxd = (unsigned long long)depth;
+          if (remat) atomicAdd(&Gl->rematerialised, 1ull);
         }
+        remat = false;
         e = classify(g, S, f.T, L, C, cnt, failed, depth, lbw, mid);
       } else {
         e = branch(g, S, f.T, L, lbw, mid);
