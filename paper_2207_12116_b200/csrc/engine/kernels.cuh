@@ -844,9 +844,16 @@ __device__ bool propagate(const G& g, volatile int* S, unsigned sb, const Tab<TS
     // after it changed a word, so the next round scans again (H8).
     if (L.iv_dense) {
       const int n_iv = (int)L.n_iv;
-      for (int i = g.rank(); i < n_iv; i += g.size()) {
-        const int2 v = sld2(sb + 8u * (unsigned)i);
-        fl |= v.x > v.y;
+      if (n_iv <= g.size()) {  // one interval per rank at most: no loop
+        if (g.rank() < n_iv) {
+          const int2 v = sld2(sb + 8u * (unsigned)g.rank());
+          fl = v.x > v.y;
+        }
+      } else {
+        for (int i = g.rank(); i < n_iv; i += g.size()) {
+          const int2 v = sld2(sb + 8u * (unsigned)i);
+          fl |= v.x > v.y;
+        }
       }
     } else {
       for (int i = g.rank(); i < (int)L.n_iv; i += g.size()) {
