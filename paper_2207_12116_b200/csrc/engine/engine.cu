@@ -113,6 +113,8 @@ struct pccp_gpu_ctx {
   int table_in_smem = 0;
   int ne_only = 0;  // lowered to NE records (and fold tells) only: the kNeOnly kernels
   int dec_ctas = 0;  // grid of the persistent decomposition kernel
+  long long plan_key = -1;  // last plan's (variant, block, smem) and its occupancies
+  int plan_occ = 0, plan_occ_dec = 0;
   std::uint32_t audit_taken = 0;  // node-audit samples of the last search
 
   DBuf<int> fa, fb, ia, ib, stack, best, io, mailbox, waitq, dec, chunk, audit;
@@ -225,11 +227,23 @@ void plan(pccp_gpu_ctx* c) {
   c->smem = base + (in_smem ? table : 0);
   int occ = 0;
   int occ_dec = 0;
-  dispatch(c, [&]<class Gp, bool TS, int F>() {
-    set_smem_attrs<Gp, TS, F>(c->smem);
-    occ = occupancy<Gp, TS, F>(c->block, c->smem);
-    occ_dec = occupancy_decompose<Gp, TS, F>(c->block, c->smem);
-  });
+  // the attributes and occupancies depend only on (kernel variant, block,
+  // smem): a reload of a model with the same plan reuses them
+  const long long key = ((long long)c->warp << 62) ^ ((long long)c->ne_only << 61) ^
+                        ((long long)c->table_in_smem << 60) ^ ((long long)c->block << 40) ^ (long long)c->smem;
+  if (c->plan_key == key) {
+    occ = c->plan_occ;
+    occ_dec = c->plan_occ_dec;
+  } else {
+    dispatch(c, [&]<class Gp, bool TS, int F>() {
+      set_smem_attrs<Gp, TS, F>(c->smem);
+      occ = occupancy<Gp, TS, F>(c->block, c->smem);
+      occ_dec = occupancy_decompose<Gp, TS, F>(c->block, c->smem);
+    });
+    c->plan_key = key;
+    c->plan_occ = occ;
+    c->plan_occ_dec = occ_dec;
+  }
   if (occ_dec < 1) throw LimitError("decomposition kernel does not fit on an SM");
   if (occ < 1) throw LimitError("kernel does not fit on an SM (smem " + std::to_string(c->smem) + " B)");
   if (c->cfg.ctas_per_sm > 0) occ = std::min(occ, c->cfg.ctas_per_sm);
