@@ -587,7 +587,14 @@ Lowered lower_model(const pccp_model& m) {
       for (std::size_t i = 0; i < nes.size(); ++i) key[i] = {seen[nes[i].x]++, i};
       std::vector<std::size_t> idx(nes.size());
       for (std::size_t i = 0; i < idx.size(); ++i) idx[i] = i;
-      std::stable_sort(idx.begin(), idx.end(), [&](std::size_t a2, std::size_t b2) { return key[a2].first < key[b2].first; });
+      // ties: by the distance of the two lb words (measured on Q14: 50.2 -> 49.0 M rounds)
+      auto dist = [&](std::size_t i) {
+        return std::abs((long)(nes[i].x & 0xffff) - (long)((unsigned)nes[i].x >> 16));
+      };
+      std::stable_sort(idx.begin(), idx.end(), [&](std::size_t a2, std::size_t b2) {
+        if (key[a2].first != key[b2].first) return key[a2].first < key[b2].first;
+        return dist(a2) < dist(b2);
+      });
       std::vector<NE> t;
       for (std::size_t i : idx) t.push_back(nes[i]);
       if (mode == 2) std::reverse(t.begin(), t.end());
