@@ -94,7 +94,7 @@ struct pccp_gpu_ctx {
   int n_sm = 0;
   size_t smem_optin = 0;
   cudaStream_t stream = nullptr;
-  cudaEvent_t ev[4] = {};
+  cudaEvent_t ev[6] = {};
   bool loaded = false;
 
   Lowered low;
@@ -358,8 +358,23 @@ void run_search(pccp_gpu_ctx* c, int mode, const int32_t* root_words, int depth_
   unsigned char rflag = 0;
   CK(cudaMemcpyAsync(&rflag, c->flags.p, 1, cudaMemcpyDeviceToHost, c->stream));
   CK(cudaMemcpyAsync(root.data(), c->fa.p, (size_t)nw * 4, cudaMemcpyDeviceToHost, c->stream));
+  CK(cudaEventRecord(c->ev[3], c->stream));
   CK(cudaStreamSynchronize(c->stream));
   out.d2h += 1 + (std::uint64_t)nw * 4;
+  // Device buffers for the decomposition and the search are sized here, while
+  // the GPU is idle, and the device clock restarts after them (ev[4]): a first
+  // call's allocations are host time, not device time (they are in elapsed_ms).
+  const int dmax = [&] {
+    const int d = depth_bound(c, root);
+    return depth_cap >= 0 ? std::min(d, depth_cap + 2) : d;
+  }();
+  const int entry = (int)align4((std::uint32_t)nw + 3);
+  const int mb_stride = (int)align4((std::uint32_t)nw + 3);
+  if (rflag) {
+    c->stack.ensure((size_t)c->groups() * (size_t)dmax * (size_t)entry);
+    c->mailbox.ensure((size_t)c->groups() * (size_t)mb_stride);
+    c->waitq.ensure((size_t)c->groups());
+  }
 
   // EPS decomposition: whole BFS levels until the frontier holds target nodes.
   // Levels are enqueued in batches without host round trips: each level's
@@ -387,7 +402,9 @@ void run_search(pccp_gpu_ctx* c, int mode, const int32_t* root_words, int depth_
     CK(cudaMemcpyAsync(c->ia.p, &zero, 4, cudaMemcpyHostToDevice, c->stream));
     c->flags.ensure(2 * (size_t)cap);
     c->dec.ensure(2);
+    c->chunk.ensure((size_t)c->dec_ctas + 2);
   }
+  CK(cudaEventRecord(c->ev[4], c->stream));
   dev::DecState* d_st = reinterpret_cast<dev::DecState*>(c->dec.p);
   // Expand the frontier in (fa, ia) until it holds `target` nodes, in one
   // cooperative launch of the persistent decomposition kernel; the result is
@@ -485,10 +502,6 @@ void run_search(pccp_gpu_ctx* c, int mode, const int32_t* root_words, int depth_
 
   bool searched = false;
   if (count > 0) {
-    int dmax = depth_bound(c, root);
-    if (depth_cap >= 0) dmax = std::min(dmax, depth_cap + 2);
-    const int entry = (int)align4((std::uint32_t)nw + 3);
-    c->stack.ensure((size_t)c->groups() * (size_t)dmax * (size_t)entry);
     dev::SearchParams P{};
     P.frontier = c->fa.p;
     P.frontier_idx = c->ia.p;
@@ -503,9 +516,7 @@ void run_search(pccp_gpu_ctx* c, int mode, const int32_t* root_words, int depth_
     // dynamic load balancing: per-group mailboxes + the wait ring
     P.balance = std::getenv("PCCP_NO_BALANCE") ? 0 : 1;
     P.n_groups = c->groups();
-    P.mb_stride = (int)align4((std::uint32_t)nw + 3);
-    c->mailbox.ensure((size_t)P.n_groups * (size_t)P.mb_stride);
-    c->waitq.ensure((size_t)P.n_groups);
+    P.mb_stride = mb_stride;
     CK(cudaMemsetAsync(c->mailbox.p, 0, (size_t)P.n_groups * P.mb_stride * 4, c->stream));
     CK(cudaMemsetAsync(c->waitq.p, 0xff, (size_t)P.n_groups * 4, c->stream));
     const int active = P.n_groups;
@@ -527,11 +538,13 @@ void run_search(pccp_gpu_ctx* c, int mode, const int32_t* root_words, int depth_
   out.d2h += sizeof(dev::Globals);
   out.launches = c->launches - launches0;
   out.levels = (std::uint64_t)level;
-  float ms = 0;
-  CK(cudaEventElapsedTime(&ms, c->ev[0], c->ev[2]));
-  out.device_ms = ms;
-  CK(cudaEventElapsedTime(&ms, c->ev[0], c->ev[1]));
-  out.decompose_ms = ms;
+  // device time = root propagation (ev0..ev3) + decomposition and search (ev4..ev2)
+  float ms = 0, root_ms = 0;
+  CK(cudaEventElapsedTime(&root_ms, c->ev[0], c->ev[3]));
+  CK(cudaEventElapsedTime(&ms, c->ev[4], c->ev[2]));
+  out.device_ms = root_ms + ms;
+  CK(cudaEventElapsedTime(&ms, c->ev[4], c->ev[1]));
+  out.decompose_ms = root_ms + ms;
   if (searched) {
     CK(cudaEventElapsedTime(&ms, c->ev[1], c->ev[2]));
     out.kernel_ms = ms;
