@@ -305,6 +305,7 @@ struct RunOut {
   std::uint64_t subproblems = 0;
   std::uint64_t bfs_rounds = 0, launches = 0, h2d = 0, d2h = 0, levels = 0;
   double device_ms = 0;
+  double root_ms = 0, gap_ms = 0;  // root propagation; host gap (buffer sizing) before the decomposition
 };
 
 template <class Gp, bool TS, int F>
@@ -545,6 +546,9 @@ void run_search(pccp_gpu_ctx* c, int mode, const int32_t* root_words, int depth_
   out.device_ms = root_ms + ms;
   CK(cudaEventElapsedTime(&ms, c->ev[4], c->ev[1]));
   out.decompose_ms = root_ms + ms;
+  CK(cudaEventElapsedTime(&ms, c->ev[3], c->ev[4]));
+  out.root_ms = root_ms;
+  out.gap_ms = ms;
   if (searched) {
     CK(cudaEventElapsedTime(&ms, c->ev[1], c->ev[2]));
     out.kernel_ms = ms;
@@ -615,9 +619,16 @@ void merge_run(RunOut& acc, const RunOut& r, bool first) {
 }
 
 // The device keeps the last 64 improvements in a ring (record_solution).
-void append_log(const dev::Globals& g, double offset_ms, std::vector<std::pair<int, double>>& log) {
+// Improvement times are device-clock offsets from the run's start; those after
+// the root fixed point exclude the host gap in which the search buffers were sized.
+void append_log(const RunOut& r, double offset_ms, std::vector<std::pair<int, double>>& log) {
+  const dev::Globals& g = r.g;
   const int n = g.n_impr, first = std::max(0, n - 64);
-  for (int k = first; k < n; ++k) log.emplace_back(g.impr_val[k & 63], offset_ms + (double)g.impr_ns[k & 63] * 1e-6);
+  for (int k = first; k < n; ++k) {
+    double t = (double)g.impr_ns[k & 63] * 1e-6;
+    if (t >= r.root_ms + r.gap_ms) t -= r.gap_ms;
+    log.emplace_back(g.impr_val[k & 63], offset_ms + t);
+  }
 }
 
 void check_loaded(const pccp_gpu_ctx* c) {
@@ -911,7 +922,7 @@ int pccp_gpu_solve(pccp_gpu_ctx* c, const int32_t* root, const pccp_limits* lim,
           run_search<Gp, TS, F>(c, 1, root, -1, &l1, r1, seg_order(seg), seg > 0,
                                 (unsigned long long)(stall_ms * 1e6), (unsigned)seg);
         });
-        append_log(r1.g, acc.device_ms, log);
+        append_log(r1, acc.device_ms, log);
         merge_run(acc, r1, seg == 0);
         if (r1.g.incomplete == 0) {
           proved = true;
@@ -929,11 +940,11 @@ int pccp_gpu_solve(pccp_gpu_ctx* c, const int32_t* root, const pccp_limits* lim,
     pccp_limits l2;
     if (c->cfg.primal_ms <= 0) {
       dispatch(c, [&]<class Gp, bool TS, int F>() { run_search<Gp, TS, F>(c, 1, root, -1, lim, r, var_order); });
-      append_log(r.g, 0.0, log);
+      append_log(r, 0.0, log);
     } else if (!proved && left(l2, r)) {
       RunOut r2;
       dispatch(c, [&]<class Gp, bool TS, int F>() { run_search<Gp, TS, F>(c, 1, root, -1, &l2, r2, var_order, true); });
-      append_log(r2.g, r.device_ms, log);
+      append_log(r2, r.device_ms, log);
       merge_run(r, r2, false);
       out->phases = 2;
     }

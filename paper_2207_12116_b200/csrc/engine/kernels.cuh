@@ -588,8 +588,14 @@ __device__ __forceinline__ bool eval_small(volatile int* S, const int* __restric
 // the values summed.  That is sound (the summed values are lower bounds of
 // the current ones, so a guard that holds on them holds now) and it is the
 // fixed point's: at the quiet round every read is of the final store.
+//
+// Pair (L.row_even: every term's lb word is even): each term is read as one
+// 8-byte (lb, ub) load, so the zeroing join b <- (0, 0) needs no second read:
+// it is due only when the snapshot has lb < 0 or ub > 0 (bounds only
+// tighten, so a snapshot already at 0 stays there), and a due join proves a
+// change this round, issued return-free like eval_ne_fast's.
 constexpr int kRowTerms = 8;
-template <class G, bool TS>
+template <class G, bool TS, bool Pair>
 __device__ bool eval_rows_fast(const G& g, unsigned sb, const Tab<TS>& tab, const DeviceLayout& L) {
   const int R = (int)L.row_lanes;
   const int sub = g.rank() & (R - 1);
@@ -602,7 +608,7 @@ __device__ bool eval_rows_fast(const G& g, unsigned sb, const Tab<TS>& tab, cons
     const int row = base + my;
     const bool act = row < n_rows;
     int s = 0;
-    int x[kRowTerms], v[kRowTerms];
+    int x[kRowTerms], v[kRowTerms], u[kRowTerms];
     const int4 meta = act ? tab.ld4(off_meta, row) : make_int4(0, 0, INT_MAX, 0);  // {beg, end, c, lsum}
     const int j0 = meta.x + sub, end = meta.y, c = meta.z;
     const unsigned alsum = sb + ((unsigned)meta.w << 2);
@@ -611,7 +617,15 @@ __device__ bool eval_rows_fast(const G& g, unsigned sb, const Tab<TS>& tab, cons
     for (int t = 0; t < kRowTerms; ++t) x[t] = t < n_my ? tab.ld1(off_terms, j0 + t * R) : 0;
     const int lsum_now = act && sub == 0 ? sld(alsum) : INT_MAX;  // snapshot for the lsum join
 #pragma unroll
-    for (int t = 0; t < kRowTerms; ++t) v[t] = t < n_my ? sld(sb + ((unsigned)tword(x[t]) << 2)) : 0;
+    for (int t = 0; t < kRowTerms; ++t) {
+      if constexpr (Pair) {
+        const int2 p = t < n_my ? sld2(sb + ((unsigned)tword(x[t]) << 2)) : make_int2(0, 0);
+        v[t] = p.x;
+        u[t] = p.y;
+      } else {
+        v[t] = t < n_my ? sld(sb + ((unsigned)tword(x[t]) << 2)) : 0;
+      }
+    }
 #pragma unroll
     for (int t = 0; t < kRowTerms; ++t) s += tcoef(x[t]) * v[t];
     for (int o = R >> 1; o > 0; o >>= 1) s += __shfl_xor_sync(kFull, s, o, R);
@@ -628,8 +642,19 @@ __device__ bool eval_rows_fast(const G& g, unsigned sb, const Tab<TS>& tab, cons
           const int coef = tcoef(x[t]);
           if (t < n_my && (over || coef + s - coef * v[t] > c)) {
             const unsigned a = sb + ((unsigned)tword(x[t]) << 2);
-            ch |= sjoin_max(a, 0);
-            ch |= sjoin_min(a + 4, 0);
+            if constexpr (Pair) {
+              if (v[t] < 0) {
+                sred_max(a, 0);
+                ch = 1u;
+              }
+              if (u[t] > 0) {
+                sred_min(a + 4, 0);
+                ch = 1u;
+              }
+            } else {
+              ch |= sjoin_max(a, 0);
+              ch |= sjoin_min(a + 4, 0);
+            }
           }
         }
       }
@@ -640,7 +665,7 @@ __device__ bool eval_rows_fast(const G& g, unsigned sb, const Tab<TS>& tab, cons
 
 template <class G, bool TS>
 __device__ bool eval_rows(const G& g, unsigned sb, const Tab<TS>& tab, const DeviceLayout& L) {
-  if (L.rows_fast) return eval_rows_fast(g, sb, tab, L);
+  if (L.rows_fast) return L.row_even ? eval_rows_fast<G, TS, true>(g, sb, tab, L) : eval_rows_fast<G, TS, false>(g, sb, tab, L);
   const int R = (int)L.row_lanes;
   const int sub = g.rank() & (R - 1);
   const int per_pass = g.size() / R;

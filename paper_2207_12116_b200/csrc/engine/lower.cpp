@@ -745,6 +745,23 @@ Lowered lower_model(const pccp_model& m) {
       for (std::int32_t x : rows[r].terms) B[L.row_terms + t++] = x;
     }
     B[L.row_off + L.n_rows] = static_cast<std::int32_t>(t);
+    // Paired (lb, ub) loads pay when neighbouring lanes read neighbouring
+    // intervals (RCPSP: term k of rows t and t+1 is b_{i,t}, b_{i,t+1}); on
+    // scattered terms (random CSP) the 8-byte loads only add bank conflicts.
+    L.row_even = 1;
+    std::uint64_t contig = 0;
+    auto tw = [](std::int32_t x) { return static_cast<std::uint32_t>(x) & kTermWordMask; };
+    for (std::size_t r = 0; r < rows.size(); ++r) {
+      const auto& ts = rows[r].terms;
+      for (std::size_t k = 0; k < ts.size(); ++k) {
+        if ((tw(ts[k]) & 1u) || tw(ts[k]) + 1 >= m.n_words) L.row_even = 0;
+        if (k + 1 < ts.size() && tw(ts[k + 1]) == tw(ts[k]) + 2) ++contig;
+        if (r + 1 < rows.size() && rows[r + 1].terms.size() == ts.size() && tw(rows[r + 1].terms[k]) == tw(ts[k]) + 2)
+          ++contig;
+      }
+    }
+    if (2 * contig < t) L.row_even = 0;
+    if (std::getenv("PCCP_ROW_PAIR") && std::atoi(std::getenv("PCCP_ROW_PAIR")) == 0) L.row_even = 0;
     // the same per row as one int4 {first term, end, c, lsum word} (eval_rows_fast)
     L.row_meta = reserve_arr(4 * L.n_rows);
     for (std::uint32_t r = 0; r < L.n_rows; ++r) {
