@@ -341,12 +341,13 @@ void run_search(pccp_gpu_ctx* c, int mode, const int32_t* root_words, int depth_
     C.audit_shift = std::clamp(c->cfg.audit_shift, 0, 40);
   }
 
-  reset_globals(c, lim, keep_incumbent, stall_ns);
-  // the root store is frontier buffer 0 of the decomposition (capacity 2*target)
+  // the root store is frontier buffer 0 of the decomposition (capacity 2*target),
+  // allocated before the device clock starts (reset_globals)
   const long long target_cap = (long long)eps_factor(c) * c->groups() * shard_count;
   c->fa.ensure((size_t)stride * (size_t)std::max<long long>(1, std::min<long long>(2 * target_cap, 1ll << 29)));
   c->ia.ensure(1);
   c->flags.ensure(2);
+  reset_globals(c, lim, keep_incumbent, stall_ns);
   std::vector<std::int32_t> root(root_words, root_words + nw);
   CK(cudaMemcpyAsync(c->fa.p, root.data(), (size_t)nw * 4, cudaMemcpyHostToDevice, c->stream));
   const int zero = 0;
