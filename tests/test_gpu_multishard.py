@@ -73,3 +73,24 @@ def test_two_process_solve_with_ipc_incumbent(seed, optimum):
         assert p.exitcode == 0
     for rank, status, obj, checked, nodes in out:
         assert status == "OPTIMAL" and obj == optimum and checked
+
+
+def test_bench_two_ranks_on_one_device():
+    """bench.py under torch.distributed.run with 2 ranks (the driver's N > 1
+    launch), both on cuda:0 over gloo (PCCP_BENCH_SHARE_DEVICE): one JSON line
+    from rank 0, with the whole-job Q14 counts exact (parity over the ranks)."""
+    import json
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    env = dict(os.environ, PCCP_BENCH_SHARE_DEVICE="1")
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", "2",
+           "--master-addr", "127.0.0.1", "--master-port", str(_free_port()), "bench.py", "--gpus", "2",
+           "--steps", "2", "--warmup", "3", "--no-tto", "--no-cpu-baseline"]
+    p = subprocess.run(cmd, cwd=root, env=env, capture_output=True, text=True, timeout=600)
+    assert p.returncode == 0, p.stderr[-2000:]
+    lines = [ln for ln in p.stdout.splitlines() if ln.startswith("{")]
+    assert len(lines) == 1, p.stdout[-2000:]
+    d = json.loads(lines[0])
+    assert d["n_gpus"] == 2 and d["parity"]["exact"], d["parity"]
+    assert d["value"] > 0 and d["e2e"]["value"] > 0 and d["gpu_launches"] > 0
