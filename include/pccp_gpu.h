@@ -153,7 +153,9 @@ typedef struct pccp_stats {
   uint64_t search_evals;/* evals inside the persistent search kernel only */
   uint64_t h2d_bytes;   /* host->device bytes moved by this call */
   uint64_t d2h_bytes;   /* device->host bytes moved by this call */
-  double device_ms;     /* device time of the whole call (CUDA events on the engine stream) */
+  double device_ms;     /* device time of the whole call (CUDA events on the engine stream): root
+                           propagation + decomposition + search; host-side buffer sizing between
+                           them (first calls) is in elapsed_ms only */
   uint64_t bfs_levels;  /* EPS decomposition levels */
   uint64_t donations;   /* subtrees handed from busy to idle groups (dynamic load balancing) */
   uint64_t rematerialised; /* nodes materialised a second time: EPS frontier nodes re-propagated under
