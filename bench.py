@@ -199,7 +199,8 @@ def time_to_optimum(local, rank, world, dist):
         ev_s = st["search_evals"] / (st["kernel_ms"] / 1e3) if st["kernel_ms"] > 0 else 0.0
         out[str(seed)] = {"status": status, "objective": obj, "valid": bool(ok),
                           "matches_reference": obj == TTO_OPTIMA[seed], "t_first_optimal_ms": t_first,
-                          "t_proof_ms": t_proof, "nodes": local_r.stats["nodes"],
+                          "t_proof_ms": t_proof, "t_wall_ms": local_r.stats["elapsed_ms"],
+                          "nodes": local_r.stats["nodes"],
                           "tree_nodes": local_r.stats["nodes"] - local_r.stats["rematerialised"],
                           "k_search": {"ms": st["kernel_ms"], "evals_per_s": ev_s,
                                        "smem_frac_alg": ev_s * b_alg / (148 * 128 * sm_mhz * 1e6)},

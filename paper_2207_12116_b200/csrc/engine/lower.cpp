@@ -874,9 +874,10 @@ Lowered lower_model(const pccp_model& m) {
   std::copy(iv.begin(), iv.end(), B.begin() + L.iv_lb);
   // Dense interval stores (every word belongs to an interval, lb words 0, 2,
   // 4, ...): the failure scan reads (lb, ub) pairs by index, no table.
-  L.iv_dense = L.n_iv * 2 == m.n_words ? 1 : 0;
-  for (std::uint32_t i = 0; i < L.n_iv && L.iv_dense; ++i)
-    if (iv[i] != static_cast<std::int32_t>(2 * i)) L.iv_dense = 0;
+  L.iv_prefix = 1;
+  for (std::uint32_t i = 0; i < L.n_iv && L.iv_prefix; ++i)
+    if (iv[i] != static_cast<std::int32_t>(2 * i)) L.iv_prefix = 0;
+  L.iv_dense = L.iv_prefix && L.n_iv * 2 == m.n_words ? 1 : 0;
   L.n_sc = static_cast<std::uint32_t>(scw.size());
   L.sc_w = reserve_arr(L.n_sc);
   L.sc_top = reserve_arr(L.n_sc);

@@ -61,6 +61,7 @@ struct DeviceLayout {
   std::uint32_t n_gen;
   std::uint32_t iv_lb;  // lb words of interval slots (failure scan)
   std::uint32_t iv_dense;  // the store is intervals only, lb words 0, 2, 4, ... (scan by index)
+  std::uint32_t iv_prefix;  // the intervals are words [0, 2 n_iv), scalars after (RCPSP: the sums)
   std::uint32_t n_iv;
   std::uint32_t sc_w, sc_top;  // scalar slots: word, top value
   std::uint32_t n_sc;
