@@ -867,7 +867,9 @@ __device__ bool propagate(const G& g, volatile int* S, unsigned sb, const Tab<TS
     if constexpr (F == kAllFamilies) ch |= eval_other_families(g, S, sb, tab, L);
     // The scan may see an intermediate state: failure is monotone, and a join
     // after it changed a word, so the next round scans again (H8).
-    if (L.iv_prefix) {  // intervals by index; scalars (if any) from their list
+    // NE-only kernels keep the plain test (iv_dense): the extra scalar branch
+    // costs Q14 3% in code generation.
+    if (F == kAllFamilies ? L.iv_prefix : L.iv_dense) {  // intervals by index; scalars (if any) from their list
       const int n_iv = (int)L.n_iv;
       if (n_iv <= g.size()) {  // one interval per rank at most: no loop
         if (g.rank() < n_iv) {
@@ -880,7 +882,7 @@ __device__ bool propagate(const G& g, volatile int* S, unsigned sb, const Tab<TS
           fl |= v.x > v.y;
         }
       }
-      if (!L.iv_dense)
+      if (F == kAllFamilies && !L.iv_dense)
         for (int i = g.rank(); i < (int)L.n_sc; i += g.size())
           fl |= sld(sb + 4u * (unsigned)tab.ld1(L.sc_w, i)) == tab.ld1(L.sc_top, i);
     } else {
