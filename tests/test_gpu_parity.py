@@ -403,3 +403,37 @@ def test_node_limit_bounds_materialisations(limit, golden):
         assert s.stats["nodes"] <= limit + 2 * 4736
         if s.objective is not None:
             assert m.check_solution(s.best_words)
+
+
+@pytest.mark.parametrize("seed", [1, 2])
+def test_interleaved_scalar_cells(seed, hengine):
+    """A store whose scalar cells (sum accumulators) sit between interval
+    cells: the failure scan cannot walk the intervals by index (lower.cpp
+    iv_prefix) and reads the interval and scalar lists.  Enumeration counts and
+    hash-sum, GPU == C oracle."""
+    from paper_2207_12116_b200 import Model
+    from paper_2207_12116_b200.model import Kind, leq_offset, linear_leq
+    rng = np.random.default_rng(seed)
+    m = Model()
+    xs = []
+    for blk in range(4):
+        for _ in range(4):
+            x = m.add_cell()
+            m.tell(x, 0, 6)
+            xs.append(x)
+        # sums over the cells so far: their accumulators follow this block
+        for _ in range(2):
+            idx = rng.choice(len(xs), size=3, replace=False)
+            terms = [(int(rng.integers(1, 4)), xs[i]) for i in idx]
+            m.post(linear_leq(terms, int(rng.integers(6, 14))))
+        i, j = sorted(rng.choice(len(xs), size=2, replace=False))
+        m.post(leq_offset(xs[i], 1, xs[j]))
+    t = m.tables()
+    scal = [w for k, w in zip(t.slot_kind, t.slot_word) if k != Kind.Interval]
+    assert scal and min(scal) < max(t.slot_word), "scalars must be interleaved"
+    o = Oracle(t)
+    g = o.enumerate(o.bottom(), depth_cap=24)
+    assert g["nodes"] > 1000 and g["exhausted"]
+    res = hengine.load(m).enumerate(depth_cap=24)
+    for k in ("nodes", "failures", "solutions", "open_leaves", "hash_sum"):
+        assert res[k] == g[k], k
