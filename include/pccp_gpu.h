@@ -103,7 +103,8 @@ typedef struct pccp_gpu_cfg {
   int32_t group_threads; /* threads owning one subproblem: 32 (warp) .. 1024; 0 = auto */
   int32_t groups_per_cta;/* warp-groups sharing one CTA (and its smem command table); 0 = auto */
   int32_t ctas_per_sm;   /* 0 = auto (occupancy) */
-  int32_t eps_factor;    /* EPS subproblems per resident group; 0 = auto */
+  int32_t eps_factor;    /* EPS subproblems per resident group; 0 = auto (warp groups 8; CTA groups
+                            start from the root alone and spread by donations) */
   int32_t shard_index;   /* this GPU's share of the EPS frontier: i mod shard_count == shard_index */
   int32_t shard_count;   /* 0/1 = unsharded */
   int32_t hash;          /* 1: accumulate the order-independent fixed-point hash-sum */
