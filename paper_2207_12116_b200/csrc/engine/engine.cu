@@ -523,7 +523,8 @@ void run_search(pccp_gpu_ctx* c, int mode, const int32_t* root_words, int depth_
     P.stack_depth = dmax;
     P.entry_stride = entry;
     // dynamic load balancing: per-group mailboxes + the wait ring
-    P.balance = std::getenv("PCCP_NO_BALANCE") ? 0 : 1;
+    P.balance = std::getenv("PCCP_NO_BALANCE") ? 0 : 2;
+    if (const char* dm = std::getenv("PCCP_DONATE_MIN")) P.balance = std::max(1, std::atoi(dm));
     P.n_groups = c->groups();
     P.mb_stride = mb_stride;
     CK(cudaMemsetAsync(c->mailbox.p, 0, (size_t)P.n_groups * P.mb_stride * 4, c->stream));

@@ -611,7 +611,7 @@ struct SearchParams {
   int stack_depth;   // entries per group
   int entry_stride;  // words per entry: store + (lbw, mid, depth)
   // dynamic load balancing (donation of the shallowest pending right branch)
-  int balance;
+  int balance;       // 0: off; else the pending branches a group needs before it donates one
   int* mailbox;      // per group: store (n_words) + (unused, depth, state)
   int mb_stride;
   int* waitq;        // ring of idle group ids (-1: empty)
@@ -760,7 +760,7 @@ __global__ void __launch_bounds__(MaxThreads<G, F>::value, MaxThreads<G, F>::min
       // one broadcast per node for the donation claim and the limit checks
       int ctl = 0;
       if (g.rank() == 0) {
-        if (P.balance && sp - bot >= 2) ctl |= claim_donation_rank0(Gl) << 1;
+        if (P.balance && sp - bot >= P.balance) ctl |= claim_donation_rank0(Gl) << 1;
         if (need_prop) ctl |= stop_rank0(C);
       }
       ctl = g.bcast0(ctl);
