@@ -741,6 +741,34 @@ int pccp_gpu_load(pccp_gpu_ctx* c, const pccp_model* m) {
     c->blob.ensure(c->low.blob.size() + 4);
     CK(cudaMemcpyAsync(c->blob.p, c->low.blob.data(), c->low.blob.size() * 4, cudaMemcpyHostToDevice, c->stream));
     plan(c);
+    // Size the DFS stacks here rather than in the first solve: the depth bound
+    // of the bottom store under the folded constant tells bounds the one of any
+    // root reached from it by propagation (bounds only tighten).  Skipped when
+    // a candidate is unbounded there (the solve sizes them from its root).
+    {
+      const DeviceLayout& L = c->low.L;
+      std::vector<std::int32_t> r0(L.n_words);
+      for (std::uint32_t w = 0; w < L.n_words; ++w) r0[w] = c->low.word_up[w] ? INT32_MIN : INT32_MAX;
+      for (std::uint32_t k = 0; k < L.n_fold; ++k) {
+        const std::uint32_t fw = static_cast<std::uint32_t>(c->low.blob[L.fold_w + k]);
+        const std::int32_t v = c->low.blob[L.fold_v + k];
+        const std::uint32_t w = fw & 0x7fffffffu;
+        if (w >= L.n_words) continue;
+        r0[w] = (fw >> 31) ? std::max(r0[w], v) : std::min(r0[w], v);
+      }
+      bool bounded = true;
+      for (std::uint32_t i = 0; i < L.n_cand; ++i) {
+        const int w = c->low.blob[L.cand_lbw + i];
+        if (r0[w] == INT32_MIN || r0[w + 1] == INT32_MAX) bounded = false;
+      }
+      const size_t entry = align4(L.n_words + 3);
+      const size_t bytes = bounded ? (size_t)c->groups() * (size_t)depth_bound(c, r0) * entry * 4 : 0;
+      if (bounded && bytes <= (size_t(8) << 30)) {
+        c->stack.ensure(bytes / 4);
+        c->mailbox.ensure((size_t)c->groups() * entry);
+        c->waitq.ensure((size_t)c->groups());
+      }
+    }
     CK(cudaStreamSynchronize(c->stream));
     c->loaded = true;
     return PCCP_OK;
