@@ -763,6 +763,9 @@ int pccp_gpu_load(pccp_gpu_ctx* c, const pccp_model* m) {
       }
       const size_t entry = align4(L.n_words + 3);
       const size_t bytes = bounded ? (size_t)c->groups() * (size_t)depth_bound(c, r0) * entry * 4 : 0;
+      // the root frontier buffer of run_search (its first ensure), sized here too
+      const long long tcap = (long long)eps_factor(c) * c->groups() * std::max(1, c->cfg.shard_count);
+      c->fa.ensure((size_t)c->store_stride * (size_t)std::max<long long>(1, std::min<long long>(2 * tcap, 1ll << 29)));
       if (bounded && bytes <= (size_t(8) << 30)) {
         c->stack.ensure(bytes / 4);
         c->mailbox.ensure((size_t)c->groups() * entry);
