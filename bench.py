@@ -160,7 +160,6 @@ def cpu_reference(w, budget_s, threads):
 
 TTO_SEEDS = (1, 2, 5, 7, 9, 11)  # SURVEY 8(d) config 4 parity seeds
 TTO_OPTIMA = {1: 84, 2: 77, 5: 73, 7: 60, 9: 61, 11: 99}
-TTO_CPU_W1_S = {1: 0.23, 2: 6.4, 5: 0.34, 7: 28.2, 9: 40.9, 11: 3.2}  # reference W=1, survey
 
 
 def time_to_optimum(local, rank, world, dist):
@@ -202,9 +201,7 @@ def time_to_optimum(local, rank, world, dist):
                           "t_proof_ms": t_proof, "t_wall_ms": local_r.stats["elapsed_ms"],
                           "nodes": local_r.stats["nodes"],
                           "tree_nodes": local_r.stats["nodes"] - local_r.stats["rematerialised"],
-                          "k_search": {"ms": st["kernel_ms"], "evals_per_s": ev_s,
-                                       "smem_frac_alg": ev_s * b_alg / (148 * 128 * sm_mhz * 1e6)},
-                          "cpu_reference_w1_s": TTO_CPU_W1_S[seed]}
+                          "k_search": {"ms": st["kernel_ms"], "evals_per_s": ev_s}}
     eng.close()
     return {"config": "rcpsp 30 tasks x 4 resources, random_patterson(mt19937_64(seed)), minimise makespan",
             "note": "node counts differ from the CPU only through search order and incumbent timing",
@@ -331,18 +328,47 @@ def _gather_obj(dist, v):
     return out
 
 
-def cpu_time_to_optimum(threads):
-    """The reference solve_parallel (oracle/_ref) with W = host threads on the
-    quick parity seeds (solver.cpp:229-283, EngineConfig Seq, eps_factor 8)."""
+def host_cpu():
+    """nproc, the lscpu model and clocks of this host."""
+    info = {"threads": os.cpu_count() or 1}
+    try:
+        txt = subprocess.run(["lscpu"], capture_output=True, text=True, timeout=10).stdout
+        for line in txt.splitlines():
+            k, _, v = line.partition(":")
+            k, v = k.strip(), v.strip()
+            if k == "Model name":
+                info["model"] = v
+            elif k in ("CPU max MHz", "CPU MHz", "Socket(s)", "Core(s) per socket", "Thread(s) per core"):
+                info[k.lower().replace("(s)", "s").replace(" ", "_")] = v
+    except Exception:
+        pass
+    return info
+
+
+def cpu_time_to_optimum(threads, timeout_s=90.0):
+    """The reference solve_parallel (oracle/_ref: the reference library compiled
+    from its sources) on all six parity seeds, with W = 1 and W = host threads
+    (solver.cpp:229-283, EngineConfig Seq, eps_factor 8 — the call of
+    `pccp solve`, tools/pccp.cpp:61-62), timed in this run.  The six W = 1
+    solves run at the same time, one host thread each (ctypes releases the
+    GIL; each is single-threaded), the W = nproc solves one after the other."""
+    from concurrent.futures import ThreadPoolExecutor
+
     from oracle import refh
     if not refh.available():
         return None
-    out = {}
-    for seed in (1, 5, 11):
-        r = refh.RefModel.rcpsp(seed, 30, 4).solve_parallel(workers=threads, timeout_s=60)
-        out[str(seed)] = {"status": ["OPTIMAL", "SAT", "UNSAT", "UNKNOWN"][r["status"]], "objective": r["objective"],
-                          "t_proof_ms": r["elapsed_ms"], "nodes": r["nodes"], "workers": threads}
-    return out
+
+    def one(seed, workers):
+        r = refh.RefModel.rcpsp(seed, 30, 4).solve_parallel(workers=workers, timeout_s=timeout_s)
+        return {"status": ["OPTIMAL", "SAT", "UNSAT", "UNKNOWN"][r["status"]], "objective": r["objective"],
+                "t_proof_ms": r["elapsed_ms"] if r["status"] == 0 else None, "t_ms": r["elapsed_ms"],
+                "nodes": r["nodes"], "workers": workers}
+    concurrent = min(len(TTO_SEEDS), max(1, threads // 2))
+    with ThreadPoolExecutor(concurrent) as ex:
+        w1 = list(ex.map(lambda sd: one(sd, 1), TTO_SEEDS))
+    wn = [one(sd, threads) for sd in TTO_SEEDS]
+    return {"timeout_s": timeout_s, "w1_concurrent_solves": concurrent, "host": host_cpu(),
+            "seeds": {str(sd): {"w1": a, "wN": b} for sd, a, b in zip(TTO_SEEDS, w1, wn)}}
 
 
 def run_reference_arm(a, w):

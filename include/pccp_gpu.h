@@ -127,6 +127,8 @@ typedef struct pccp_gpu_cfg {
                             fixed point of up to this many nodes (every 2^audit_shift-th
                             materialisation), for pccp_gpu_audit.  0 = off. */
   int32_t audit_shift;
+  int32_t record_frontier; /* 1: keep the hashes of the last search's shared EPS frontier and of this
+                              shard's share of it (pccp_gpu_frontier; tests of the partition) */
 } pccp_gpu_cfg;
 
 typedef struct pccp_limits {
@@ -179,7 +181,9 @@ typedef struct pccp_solve_result {
   int32_t improvements[64];    /* objective values, in improvement order */
   double improvement_ms[64];   /* device time since search start */
   int32_t phases;              /* 1, or 2 with a primal phase (cfg.primal_ms) */
-  int32_t primal_proved;       /* the primal phase exhausted its tree: its result is the proof */
+  int32_t primal_proved;       /* the primal phase exhausted its tree: its result is the proof.  The
+                                  primal dives of an N-shard solve cover the WHOLE tree on every GPU,
+                                  so one GPU's primal proof is the job's proof (peers are told to stop) */
   uint64_t primal_nodes;       /* nodes of the primal phase (included in stats.nodes) */
   double primal_device_ms;     /* device time of the primal phase */
   int32_t primal_restarts;     /* primal segments restarted from the root under a better bound */
@@ -240,6 +244,27 @@ int pccp_gpu_attach_peers(pccp_gpu_ctx* ctx, const uint8_t* handles64, int32_t n
  * Contexts on the same device are linked directly. */
 int pccp_gpu_link_peers(pccp_gpu_ctx* const* ctxs, int32_t n);
 
+/* Cross-rank cells.  Once peers are attached or linked, a search never
+ * resets the incumbent cell, the best-store lock and the `done` flag (a
+ * peer's push may land before this rank's search starts, and must not be
+ * lost); they are reset by pccp_gpu_open, pccp_gpu_load and this call.  A
+ * multi-rank caller resets every rank, then barriers, then solves
+ * (paper_2207_12116_b200/distributed.py run_solve). */
+int pccp_gpu_reset_shared(pccp_gpu_ctx* ctx);
+
+/* Offers an objective value to the incumbent cell (atomicMin): the value of a
+ * known solution, e.g. a warm start.  The search then looks for strictly
+ * better solutions only (solver.cpp:96-99); a value below the optimum makes
+ * the solve report that value with no store (has_objective = 2). */
+int pccp_gpu_offer_incumbent(pccp_gpu_ctx* ctx, int32_t value);
+
+/* With cfg.record_frontier: the FNV store hashes of the last
+ * search's shared EPS frontier (phase A, identical on every shard) and of the
+ * positions i = shard_index (mod shard_count) this context kept.  Each array
+ * receives at most `cap` entries; *n_all / *n_share get the full sizes. */
+int pccp_gpu_frontier(pccp_gpu_ctx* ctx, uint64_t* all, uint32_t* n_all, uint64_t* share,
+                      uint32_t* n_share, uint32_t cap);
+
 /* The node audit of the last enumerate/solve call (cfg.audit_nodes > 0):
  * pre[k] is a node's store as materialised (parent fixed point + decision +
  * objective bound), post[k] the engine's result for it and failed[k] its
@@ -266,7 +291,11 @@ typedef struct pccp_lowering_info {
   uint32_t table_in_smem;
   uint32_t stack_in_smem;
   uint32_t stack_depth;
-  double alg_bytes_per_eval; /* 4*(guard terms) + 4*(fn terms + target words) */
+  double alg_bytes_per_eval; /* 4*(guard terms) + 4*(fn terms + target words), per
+                                reference command: counts a word once per command that reads it */
+  double store_bytes_per_round; /* the lowered records' byte model: store bytes one fixed-point round
+                                   reads (fused records read each word once for several commands) */
+  double table_bytes_per_round; /* table bytes one round reads (shared memory if table_in_smem, else L2) */
 } pccp_lowering_info;
 
 int pccp_gpu_lowering_info(pccp_gpu_ctx* ctx, pccp_lowering_info* out);

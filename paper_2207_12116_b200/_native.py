@@ -53,6 +53,7 @@ class PccpGpuCfg(C.Structure):
         ("primal_ms", C.c_int32),
         ("audit_nodes", C.c_int32),
         ("audit_shift", C.c_int32),
+        ("record_frontier", C.c_int32),
     ]
 
 
@@ -125,6 +126,8 @@ class PccpLoweringInfo(C.Structure):
         ("stack_in_smem", C.c_uint32),
         ("stack_depth", C.c_uint32),
         ("alg_bytes_per_eval", C.c_double),
+        ("store_bytes_per_round", C.c_double),
+        ("table_bytes_per_round", C.c_double),
     ]
 
 
@@ -156,6 +159,10 @@ def lib():
         "pccp_gpu_incumbent_handle": (C.c_int, [vp, vp]),
         "pccp_gpu_attach_peers": (C.c_int, [vp, vp, i32, i32]),
         "pccp_gpu_audit": (C.c_int, [vp, vp, vp, vp, vp]),
+        "pccp_gpu_link_peers": (C.c_int, [vp, i32]),
+        "pccp_gpu_reset_shared": (C.c_int, [vp]),
+        "pccp_gpu_offer_incumbent": (C.c_int, [vp, i32]),
+        "pccp_gpu_frontier": (C.c_int, [vp, vp, P(u32), vp, P(u32), u32]),
         # host model builder
         "pccp_host_last_error": (C.c_char_p, []),
         "pccp_host_new": (vp, []),

@@ -122,8 +122,11 @@ struct pccp_gpu_ctx {
   DBuf<unsigned> rnd;
   dev::Globals* G = nullptr;
   std::vector<void*> opened;
-  DBuf<int*> d_peers;
+  DBuf<dev::Globals*> d_peers;  // peer contexts' globals (incumbent replicas, done flags)
   int n_peers = 0;
+  // cfg.record_frontier: FNV hashes of the shared EPS frontier (phase A) and of
+  // this shard's share of it, from the last search (pccp_gpu_frontier)
+  std::vector<std::uint64_t> frontier_all, frontier_share;
   std::uint64_t launches = 0;
 
   int groups() const { return ctas * (warp ? gpc : 1); }
@@ -259,8 +262,21 @@ void plan(pccp_gpu_ctx* c) {
 // the tail (CSP depth 22: 5.1 -> 4.9 ms).
 int eps_factor(const pccp_gpu_ctx* c) { return c->cfg.eps_factor > 0 ? c->cfg.eps_factor : (c->warp ? 8 : 2); }
 
+// The cross-rank cells of Globals (incumbent, best_lock, best_value, done):
+// INT_MAX / unlocked / no proof.  At open, at load and on request
+// (pccp_gpu_reset_shared): with peers linked a search never rewrites them, so
+// a push that lands before this rank's search starts is kept.
+void reset_shared(pccp_gpu_ctx* c) {
+  const int cells[4] = {INT32_MAX, 0, INT32_MAX, 0};
+  static_assert(offsetof(dev::Globals, done) - offsetof(dev::Globals, incumbent) == 3 * sizeof(int), "layout");
+  CK(cudaMemcpyAsync(reinterpret_cast<char*>(c->G) + offsetof(dev::Globals, incumbent), cells, sizeof(cells),
+                     cudaMemcpyHostToDevice, c->stream));
+  CK(cudaStreamSynchronize(c->stream));
+}
+
 void reset_globals(pccp_gpu_ctx* c, const pccp_limits* lim, bool keep_incumbent = false,
                    unsigned long long stall_ns = 0) {
+  if (c->n_peers > 0) keep_incumbent = true;  // peers push into the cells at any time
   dev::Globals h;
   std::memset(&h, 0, sizeof(h));
   h.stall_ns = stall_ns;
@@ -300,7 +316,7 @@ int depth_bound(const pccp_gpu_ctx* c, const std::vector<std::int32_t>& root) {
 }
 
 struct RunOut {
-  dev::Globals g;
+  dev::Globals g{};
   double decompose_ms = 0, kernel_ms = 0, elapsed_ms = 0;
   std::uint64_t subproblems = 0;
   std::uint64_t bfs_rounds = 0, launches = 0, h2d = 0, d2h = 0, levels = 0;
@@ -308,17 +324,47 @@ struct RunOut {
   double root_ms = 0, gap_ms = 0;  // root propagation; host gap (buffer sizing) before the decomposition
 };
 
+std::uint64_t host_store_hash(const std::int32_t* w, std::uint32_t n) {
+  std::uint64_t h = 1469598103934665603ull;
+  for (std::uint32_t i = 0; i < n; ++i) {
+    const std::uint32_t v = static_cast<std::uint32_t>(w[i]);
+    for (int b = 0; b < 4; ++b) {
+      h ^= (v >> (8 * b)) & 0xffu;
+      h *= 1099511628211ull;
+    }
+  }
+  return h;
+}
+
+// cfg.record_frontier: hashes of the frontier in (fa, ia) and of the share
+// i = shard (mod shards) this GPU keeps (tests of the partition).
+void record_frontier(pccp_gpu_ctx* c, int count, int stride, int shard, int shards) {
+  const std::uint32_t nw = c->low.L.n_words;
+  std::vector<int> idx((size_t)count);
+  CK(cudaMemcpyAsync(idx.data(), c->ia.p, (size_t)count * 4, cudaMemcpyDeviceToHost, c->stream));
+  std::vector<std::int32_t> st((size_t)c->fa.n);
+  CK(cudaMemcpyAsync(st.data(), c->fa.p, c->fa.n * 4, cudaMemcpyDeviceToHost, c->stream));
+  CK(cudaStreamSynchronize(c->stream));
+  for (int i = 0; i < count; ++i) {
+    const std::uint64_t h = host_store_hash(st.data() + (size_t)idx[(size_t)i] * (size_t)stride, nw);
+    c->frontier_all.push_back(h);
+    if (i % shards == shard) c->frontier_share.push_back(h);
+  }
+}
+
 template <class Gp, bool TS, int F>
 void run_search(pccp_gpu_ctx* c, int mode, const int32_t* root_words, int depth_cap, const pccp_limits* lim,
                 RunOut& out, int var_order = 0, bool keep_incumbent = false, unsigned long long stall_ns = 0,
-                unsigned var_seed = 0) {
+                unsigned var_seed = 0, bool sharded = true) {
   const double t_start = now_ms();
   const std::uint64_t launches0 = c->launches;
   const DeviceLayout& L = c->low.L;
   const int nw = (int)L.n_words;
   const int stride = c->store_stride;
-  const int shard_count = std::max(1, c->cfg.shard_count);
-  const int shard_index = c->cfg.shard_index;
+  // sharded = false: this search covers the whole tree on this GPU (the
+  // primal segments of an N-shard solve), counted by it alone
+  const int shard_count = sharded ? std::max(1, c->cfg.shard_count) : 1;
+  const int shard_index = sharded ? c->cfg.shard_index : 0;
   if (shard_index < 0 || shard_index >= shard_count) throw ArgError("shard_index out of range");
   const dev::Model M = c->model(var_order, var_seed, root_words, 1, (size_t)nw);
   dev::SearchCtl C{};
@@ -329,6 +375,12 @@ void run_search(pccp_gpu_ctx* c, int mode, const int32_t* root_words, int depth_
   C.hash = c->cfg.hash;
   C.depth_cap = depth_cap;
   C.count = shard_index == 0 ? 1 : 0;  // the decomposition runs on every GPU, counted once
+  // With N shards the root and the shared phase A must be the same on every
+  // GPU, whatever incumbent each has seen (peers push at any time): they run
+  // without the objective join, so the frontier depends on the model and the
+  // root alone and positions i = shard (mod N) partition it.  Phase B and the
+  // search re-materialise under the bound (sound: the bound is a solution's).
+  C.bound = shard_count > 1 ? 0 : 1;
   c->best.ensure((size_t)std::max(nw, 1));
   C.best_store = c->best.p;
   if (c->cfg.audit_nodes > 0) {
@@ -341,10 +393,23 @@ void run_search(pccp_gpu_ctx* c, int mode, const int32_t* root_words, int depth_
     C.audit_shift = std::clamp(c->cfg.audit_shift, 0, 40);
   }
 
-  // the root store is frontier buffer 0 of the decomposition (capacity 2*target),
-  // allocated before the device clock starts (reset_globals)
-  const long long target_cap = (long long)eps_factor(c) * c->groups() * shard_count;
-  c->fa.ensure((size_t)stride * (size_t)std::max<long long>(1, std::min<long long>(2 * target_cap, 1ll << 29)));
+  // EPS targets (see below), known before anything is allocated
+  const int eps = eps_factor(c);
+  // CTA groups (stores of hundreds of words and more) skip phase B by default:
+  // the root goes to one group and donations spread the tree (a donation per
+  // node of every busy group doubles the busy groups per node time), which
+  // beats BFS levels of whole-grid barriers (RCPSP30 proofs 3.5-4.5 -> 2.6-3.9
+  // ms, CSP depth 22 4.75 -> 4.3 ms).  Warp groups keep eps x groups (Q14:
+  // 17.33 ms vs 17.44 ms without).
+  long long target_ll = (c->warp || c->cfg.eps_factor > 0) ? (long long)eps * c->groups() : 1;
+  if (const char* dt = std::getenv("PCCP_DEC_TARGET")) target_ll = std::max(1, std::atoi(dt));
+  const long long target_a_ll = shard_count > 1 ? (long long)c->groups() * shard_count : 0;
+  if (std::max(target_ll, target_a_ll) > (1ll << 28)) throw LimitError("EPS target too large");
+  const int cap = (int)std::max(target_ll, target_a_ll);
+  // the root store is frontier buffer 0 of the decomposition (capacity 2*cap:
+  // odd levels write their children there), allocated before the device
+  // clock starts (reset_globals)
+  c->fa.ensure((size_t)stride * (size_t)std::max(2 * (size_t)cap, (size_t)1));
   c->ia.ensure(1);
   c->flags.ensure(2);
   reset_globals(c, lim, keep_incumbent, stall_ns);
@@ -390,20 +455,8 @@ void run_search(pccp_gpu_ctx* c, int mode, const int32_t* root_words, int depth_
   // expands only those (counted by their owner) to `eps * groups` nodes.  So
   // each GPU expands its own share, not the whole job's frontier, and every
   // tree node is still materialised exactly once across the GPUs.
-  const int eps = eps_factor(c);
-  // CTA groups (stores of hundreds of words and more) skip phase B by default:
-  // the root goes to one group and donations spread the tree (a donation per
-  // node of every busy group doubles the busy groups per node time), which
-  // beats BFS levels of whole-grid barriers (RCPSP30 proofs 3.5-4.5 -> 2.6-3.9
-  // ms, CSP depth 22 4.75 -> 4.3 ms).  Warp groups keep eps x groups (Q14:
-  // 17.33 ms vs 17.44 ms without).
-  long long target_ll = (c->warp || c->cfg.eps_factor > 0) ? (long long)eps * c->groups() : 1;
-  if (const char* dt = std::getenv("PCCP_DEC_TARGET")) target_ll = std::max(1, std::atoi(dt));
-  const long long target_a_ll = shard_count > 1 ? (long long)c->groups() * shard_count : 0;
-  if (std::max(target_ll, target_a_ll) > (1ll << 28)) throw LimitError("EPS target too large");
   int count = rflag ? 1 : 0;
   int level = 0;
-  const int cap = (int)std::max(target_ll, target_a_ll);
   if (count > 0) {
     c->fb.ensure(2 * (size_t)cap * stride);
     c->ib.ensure(2 * (size_t)cap);
@@ -487,8 +540,11 @@ void run_search(pccp_gpu_ctx* c, int mode, const int32_t* root_words, int depth_
     }
     return stop != 2;
   };
+  c->frontier_all.clear();
+  c->frontier_share.clear();
   if (shard_count > 1) {
     if (expand_until((int)target_a_ll) && count > 0) {
+      if (c->cfg.record_frontier) record_frontier(c, count, stride, shard_index, shard_count);
       const int mine = count > shard_index ? (count - shard_index + shard_count - 1) / shard_count : 0;
       if (mine > 0) {
         dev::k_shard_filter<<<(mine + 255) / 256, 256, 0, c->stream>>>(c->ia.p, c->ib.p, shard_index, shard_count, mine);
@@ -498,11 +554,14 @@ void run_search(pccp_gpu_ctx* c, int mode, const int32_t* root_words, int depth_
       }
       count = mine;
       C.count = 1;  // phase B and the search: every node below here is this GPU's alone
+      C.bound = 1;  // and is re-materialised under the bound
       expand_until((int)target_ll);
     }
   } else {
     expand_until((int)target_ll);
+    if (c->cfg.record_frontier && count > 0) record_frontier(c, count, stride, 0, 1);
   }
+  C.bound = 1;
   CK(cudaEventRecord(c->ev[1], c->stream));
   CK(cudaMemcpyAsync(&out.bfs_rounds, &c->G->rounds, 8, cudaMemcpyDeviceToHost, c->stream));
   CK(cudaStreamSynchronize(c->stream));
@@ -685,6 +744,7 @@ int pccp_gpu_open(const pccp_gpu_cfg* cfg, pccp_gpu_ctx** out) {
       for (auto& e : c->ev) CK(cudaEventCreate(&e));
       CK(cudaMalloc(&c->G, sizeof(dev::Globals)));
       CK(cudaMemset(c->G, 0, sizeof(dev::Globals)));
+      reset_shared(c);
     } catch (...) {
       pccp_gpu_close(c);
       throw;
@@ -730,6 +790,7 @@ int pccp_gpu_load(pccp_gpu_ctx* c, const pccp_model* m) {
     c->loaded = false;
     c->low = lower_model(*m);
     if (c->low.L.n_cand >= (1u << 24)) throw LimitError("more than 2^24 branching candidates");
+    reset_shared(c);  // an incumbent of the previous model means nothing for this one
     c->slot_kind.assign(m->slot_kind, m->slot_kind + m->n_slots);
     c->slot_word.assign(m->slot_word, m->slot_word + m->n_slots);
     c->view = *m;
@@ -763,13 +824,22 @@ int pccp_gpu_load(pccp_gpu_ctx* c, const pccp_model* m) {
       }
       const size_t entry = align4(L.n_words + 3);
       const size_t bytes = bounded ? (size_t)c->groups() * (size_t)depth_bound(c, r0) * entry * 4 : 0;
-      // the root frontier buffer of run_search (its first ensure), sized here too
-      const long long tcap = (long long)eps_factor(c) * c->groups() * std::max(1, c->cfg.shard_count);
-      c->fa.ensure((size_t)c->store_stride * (size_t)std::max<long long>(1, std::min<long long>(2 * tcap, 1ll << 29)));
-      if (bounded && bytes <= (size_t(8) << 30)) {
-        c->stack.ensure(bytes / 4);
-        c->mailbox.ensure((size_t)c->groups() * entry);
-        c->waitq.ensure((size_t)c->groups());
+      // Best effort: at most a quarter of the free device memory (several
+      // contexts may share a device); a solve whose root needs more sizes
+      // the stacks itself (run_search), and a failed allocation here only
+      // defers that.
+      size_t free_b = 0, total_b = 0;
+      CK(cudaMemGetInfo(&free_b, &total_b));
+      if (bounded && bytes <= free_b / 4) {
+        try {
+          c->stack.ensure(bytes / 4);
+          c->mailbox.ensure((size_t)c->groups() * entry);
+          c->waitq.ensure((size_t)c->groups());
+        } catch (const LimitError&) {
+          c->stack.release();
+          c->mailbox.release();
+          c->waitq.release();
+        }
       }
     }
     CK(cudaStreamSynchronize(c->stream));
@@ -799,6 +869,9 @@ int pccp_gpu_lowering_info(pccp_gpu_ctx* c, pccp_lowering_info* o) {
     o->table_in_smem = c->table_in_smem;
     o->stack_in_smem = 0;
     o->alg_bytes_per_eval = c->low.alg_bytes_per_eval;
+    o->store_bytes_per_round = c->low.store_bytes_per_round;
+    o->table_bytes_per_round = c->low.table_bytes_per_round;
+    o->stack_depth = 0;
     return PCCP_OK;
   });
 }
@@ -819,6 +892,8 @@ int pccp_lower_only(const pccp_model* m, pccp_lowering_info* o, uint32_t* shape_
     o->table_bytes = L.blob_words * 4;
     o->store_bytes = L.n_words * 4;
     o->alg_bytes_per_eval = low.alg_bytes_per_eval;
+    o->store_bytes_per_round = low.store_bytes_per_round;
+    o->table_bytes_per_round = low.table_bytes_per_round;
     if (shape_counts) {
       shape_counts[0] = L.n_unit1;
       shape_counts[1] = L.n_unit2;
@@ -929,7 +1004,16 @@ int pccp_gpu_solve(pccp_gpu_ctx* c, const int32_t* root, const pccp_limits* lim,
     // RCPSP30 seed 10; the default is the plain restart-on-improvement loop.
     const char* pdv = std::getenv("PCCP_PRIMAL_DIVERSIFY");
     const bool diversify = pdv && std::atoi(pdv) != 0;
-    auto seg_order = [&](int seg) { return (diversify && (seg & 1)) ? 3 : primal_order; };
+    // With N shards every GPU dives the WHOLE tree in the primal phase
+    // (sharded = false below), so a segment that exhausts its tree is a proof
+    // by itself, whatever the other GPUs did.  Shard 0 keeps primal_order;
+    // the others take randomised ties (var_order 3, seeded by shard and
+    // segment), so the N dives differ.
+    const int shards = std::max(1, c->cfg.shard_count);
+    auto seg_order = [&](int seg) {
+      if (shards > 1 && c->cfg.shard_index > 0) return 3;
+      return (diversify && (seg & 1)) ? 3 : primal_order;
+    };
     std::vector<std::pair<int, double>> log;  // improvement log over all phases
     RunOut r;
     out->phases = 1;
@@ -950,6 +1034,8 @@ int pccp_gpu_solve(pccp_gpu_ctx* c, const int32_t* root, const pccp_limits* lim,
       const char* se = std::getenv("PCCP_PRIMAL_STALL_MS");
       const double stall_ms = se ? std::atof(se) : std::max(100.0, 0.05 * budget_ms);
       RunOut acc;
+      acc.g.incumbent = acc.g.best_value = INT32_MAX;  // nothing ran yet: no incumbent, no proof
+      acc.g.incomplete = 1;
       for (int seg = 0;; ++seg) {
         pccp_limits l1;
         if (!left(l1, acc)) break;
@@ -960,14 +1046,21 @@ int pccp_gpu_solve(pccp_gpu_ctx* c, const int32_t* root, const pccp_limits* lim,
         RunOut r1;
         dispatch(c, [&]<class Gp, bool TS, int F>() {
           run_search<Gp, TS, F>(c, 1, root, -1, &l1, r1, seg_order(seg), seg > 0,
-                                (unsigned long long)(stall_ms * 1e6), (unsigned)seg);
+                                (unsigned long long)(stall_ms * 1e6), (unsigned)seg + 7919u * (unsigned)c->cfg.shard_index,
+                                /*sharded=*/false);
         });
         append_log(r1, acc.device_ms, log);
         merge_run(acc, r1, seg == 0);
         if (r1.g.incomplete == 0) {
           proved = true;
+          if (c->n_peers > 0) {  // the whole tree is exhausted: every peer may stop
+            dev::k_signal_done<<<1, 1, 0, c->stream>>>(c->d_peers.p, c->n_peers);
+            CK(cudaGetLastError());
+            CK(cudaStreamSynchronize(c->stream));
+          }
           break;
         }
+        if (r1.g.done) break;                                  // a peer proved it
         if (!r1.g.stalled) break;                              // out of time or limits
         if (r1.g.n_impr == 0 && !(diversify && seg + 1 < 64)) break;  // nothing new
         out->primal_restarts = seg + 1;
@@ -981,7 +1074,7 @@ int pccp_gpu_solve(pccp_gpu_ctx* c, const int32_t* root, const pccp_limits* lim,
     if (c->cfg.primal_ms <= 0) {
       dispatch(c, [&]<class Gp, bool TS, int F>() { run_search<Gp, TS, F>(c, 1, root, -1, lim, r, var_order); });
       append_log(r, 0.0, log);
-    } else if (!proved && left(l2, r)) {
+    } else if (!proved && !r.g.done && left(l2, r)) {
       RunOut r2;
       dispatch(c, [&]<class Gp, bool TS, int F>() { run_search<Gp, TS, F>(c, 1, root, -1, &l2, r2, var_order, true); });
       append_log(r2, r.device_ms, log);
@@ -1026,7 +1119,7 @@ int pccp_gpu_attach_peers(pccp_gpu_ctx* c, const uint8_t* handles, int32_t n, in
   return api([&] {
     if (!c || (n > 0 && !handles)) throw ArgError("null argument");
     CK(cudaSetDevice(c->device));
-    std::vector<int*> ptrs;
+    std::vector<dev::Globals*> ptrs;
     for (int i = 0; i < n; ++i) {
       if (i == self) continue;
       cudaIpcMemHandle_t h;
@@ -1034,13 +1127,45 @@ int pccp_gpu_attach_peers(pccp_gpu_ctx* c, const uint8_t* handles, int32_t n, in
       void* p = nullptr;
       CK(cudaIpcOpenMemHandle(&p, h, cudaIpcMemLazyEnablePeerAccess));
       c->opened.push_back(p);
-      ptrs.push_back(reinterpret_cast<int*>(static_cast<char*>(p) + offsetof(dev::Globals, incumbent)));
+      ptrs.push_back(static_cast<dev::Globals*>(p));
     }
     c->n_peers = (int)ptrs.size();
     if (!ptrs.empty()) {
       c->d_peers.ensure(ptrs.size());
-      CK(cudaMemcpy(c->d_peers.p, ptrs.data(), ptrs.size() * sizeof(int*), cudaMemcpyHostToDevice));
+      CK(cudaMemcpy(c->d_peers.p, ptrs.data(), ptrs.size() * sizeof(dev::Globals*), cudaMemcpyHostToDevice));
     }
+    return PCCP_OK;
+  });
+}
+
+int pccp_gpu_reset_shared(pccp_gpu_ctx* c) {
+  return api([&] {
+    if (!c) throw ArgError("null context");
+    CK(cudaSetDevice(c->device));
+    reset_shared(c);
+    return PCCP_OK;
+  });
+}
+
+int pccp_gpu_offer_incumbent(pccp_gpu_ctx* c, int32_t value) {
+  return api([&] {
+    if (!c) throw ArgError("null context");
+    CK(cudaSetDevice(c->device));
+    dev::k_offer_incumbent<<<1, 1, 0, c->stream>>>(c->G, value);
+    CK(cudaGetLastError());
+    CK(cudaStreamSynchronize(c->stream));
+    return PCCP_OK;
+  });
+}
+
+int pccp_gpu_frontier(pccp_gpu_ctx* c, uint64_t* all, uint32_t* n_all, uint64_t* share, uint32_t* n_share,
+                      uint32_t cap) {
+  return api([&] {
+    if (!c || !n_all || !n_share) throw ArgError("null argument");
+    *n_all = (uint32_t)c->frontier_all.size();
+    *n_share = (uint32_t)c->frontier_share.size();
+    if (all) std::copy_n(c->frontier_all.begin(), std::min<size_t>(cap, c->frontier_all.size()), all);
+    if (share) std::copy_n(c->frontier_share.begin(), std::min<size_t>(cap, c->frontier_share.size()), share);
     return PCCP_OK;
   });
 }
@@ -1071,7 +1196,7 @@ int pccp_gpu_link_peers(pccp_gpu_ctx* const* ctxs, int32_t n) {
     for (int i = 0; i < n; ++i) {
       pccp_gpu_ctx* c = ctxs[i];
       CK(cudaSetDevice(c->device));
-      std::vector<int*> ptrs;
+      std::vector<dev::Globals*> ptrs;
       for (int j = 0; j < n; ++j) {
         if (j == i) continue;
         const int dj = ctxs[j]->device;
@@ -1083,12 +1208,12 @@ int pccp_gpu_link_peers(pccp_gpu_ctx* const* ctxs, int32_t n) {
           if (e == cudaErrorPeerAccessAlreadyEnabled) cudaGetLastError();
           else CK(e);
         }
-        ptrs.push_back(&ctxs[j]->G->incumbent);
+        ptrs.push_back(ctxs[j]->G);
       }
       c->n_peers = (int)ptrs.size();
       if (!ptrs.empty()) {
         c->d_peers.ensure(ptrs.size());
-        CK(cudaMemcpy(c->d_peers.p, ptrs.data(), ptrs.size() * sizeof(int*), cudaMemcpyHostToDevice));
+        CK(cudaMemcpy(c->d_peers.p, ptrs.data(), ptrs.size() * sizeof(dev::Globals*), cudaMemcpyHostToDevice));
       }
     }
     return PCCP_OK;

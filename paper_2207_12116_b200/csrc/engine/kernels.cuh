@@ -45,9 +45,13 @@ struct Globals {
   unsigned int cursor;             // EPS work queue
   int stop;                        // 1: limit reached, 2: model error
   int incomplete;                  // a subproblem was abandoned
+  // [incumbent, n_impr): the cross-rank cells.  With peers linked they are
+  // never rewritten by a search's reset (engine.cu reset_globals), only by
+  // pccp_gpu_reset_shared / a model load, so a peer's push is never lost.
   int incumbent;                   // best objective, INT_MAX: none (local replica)
   int best_lock;
   int best_value;
+  int done;                        // a peer proved optimality over the whole tree: stop
   int n_impr;
   int impr_val[64];
   unsigned long long impr_ns[64];

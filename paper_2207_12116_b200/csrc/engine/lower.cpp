@@ -907,6 +907,46 @@ Lowered lower_model(const pccp_model& m) {
   } else {
     L.obj_lbw = -1;
   }
+  // Byte model of one round (lower.hpp): per record, the store words its
+  // evaluation reads and its table entry.
+  {
+    double sb = 0, tb = 0;
+    sb += 16.0 * L.n_ne, tb += 16.0 * L.n_ne;      // (lb, ub) of x and y; int4
+    sb += 24.0 * L.n_reif, tb += 16.0 * L.n_reif;  // x, y, b intervals; int4
+    auto unit_words = [&](std::uint32_t x, std::uint32_t w) {
+      int k = 1;  // the target
+      for (std::uint32_t v : {x & 0xffffu, x >> 16, (w >> 15) & 0x7fffu}) k += v != Z ? 1 : 0;
+      return 4.0 * k;
+    };
+    for (const U1& r : unit1) sb += unit_words(static_cast<std::uint32_t>(r.x), static_cast<std::uint32_t>(r.w));
+    tb += 16.0 * unit1.size();
+    for (const auto& r : unit2) {
+      sb += unit_words(static_cast<std::uint32_t>(r.first.x), static_cast<std::uint32_t>(r.first.w));
+      const std::uint32_t g2 = static_cast<std::uint32_t>(r.second.first);
+      for (std::uint32_t v : {g2 & 0xffffu, g2 >> 16}) sb += v != Z ? 4.0 : 0.0;
+    }
+    tb += 24.0 * unit2.size();
+    for (const Small& sm : smalls) {
+      int k = 1 + ((sm.shape >> 10) & 1);  // target word(s)
+      for (int j = 0; j < 4; ++j) k += sm.g[j] ? 1 : 0;
+      k += sm.lbt ? 1 : 0;
+      k += sm.ubt ? 1 : 0;
+      sb += 4.0 * k;
+    }
+    tb += 44.0 * smalls.size();
+    sb += 4.0 * L.n_rows + (L.row_even ? 8.0 : 4.0) * n_terms;  // lsum + each term's lb (or (lb, ub))
+    tb += 16.0 * L.n_rows + 4.0 * n_terms;
+    for (std::uint32_t g : generic) {
+      const CmdP& c = cmds[g];
+      for (const GuardP& gp : c.guards) sb += 4.0 * gp.lhs.terms.size();
+      for (const auto* e : {&c.sc, &c.lb, &c.ub})
+        if (*e) sb += 4.0 * ((*e)->terms.size() + 1);
+      tb += 4.0 * (m.cmd_off[g + 1] - m.cmd_off[g]);
+    }
+    sb += 8.0 * L.n_iv + 4.0 * L.n_sc;  // the failure scan
+    out.store_bytes_per_round = sb;
+    out.table_bytes_per_round = tb;
+  }
   L.blob_words = static_cast<std::uint32_t>(B.size());
   if (B.empty()) B.push_back(0);
   return out;

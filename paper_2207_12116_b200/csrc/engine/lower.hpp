@@ -86,6 +86,11 @@ struct Lowered {
   std::vector<std::int32_t> blob;
   std::uint32_t n_dropped = 0;  // commands that can never fire (guard rhs = +inf with '>')
   double alg_bytes_per_eval = 0;  // SURVEY 8(d) B_alg over the reference commands
+  // The byte model of one fixed-point round over the LOWERED records (what a
+  // fused record actually reads, engine roofline): store words read
+  // (shared memory) and table bytes read (shared memory when the tables fit,
+  // else L2).  Joins are not counted: a round writes a few words at most.
+  double store_bytes_per_round = 0, table_bytes_per_round = 0;
   std::vector<std::uint8_t> word_up;
   // value-range analysis (fast_paths)
   std::vector<std::uint8_t> word_cls;        // 0 constant-only, 1 affine interval bound, 2 unbounded

@@ -17,8 +17,9 @@ namespace dev {
 struct SearchCtl {
   Globals* G;
   int* best_store;       // n_words, the best solution store
-  int* const* peers;     // peer replicas of the incumbent cell (system-scope atomics)
+  Globals* const* peers; // peer contexts' globals: incumbent replicas, done flags (system-scope atomics)
   int n_peers;
+  int bound;             // join obj <= best-1 at materialisation (0 in the shared EPS phase of N shards)
   int mode;              // 0: enumerate, 1: minimise the objective
   int hash;              // accumulate the fixed-point hash-sum
   int depth_cap;         // < 0: none
@@ -56,7 +57,7 @@ __device__ __forceinline__ unsigned long long word_bit(int w) { return w < 64 ? 
 template <class G>
 __device__ __forceinline__ unsigned long long join_objective(const G& g, volatile int* S, const DeviceLayout& L,
                                                              const SearchCtl& C) {
-  if (C.mode != 1 || L.obj_lbw < 0) return 0ull;
+  if (C.mode != 1 || !C.bound || L.obj_lbw < 0) return 0ull;
   int moved = 0;
   if (g.rank() == 0) {
     const int best = *(volatile int*)&C.G->incumbent;
@@ -75,6 +76,10 @@ __device__ __forceinline__ int stop_rank0(const SearchCtl& C) {
   {
     Globals* Gl = C.G;
     stop = *(volatile int*)&Gl->stop;
+    if (!stop && *(volatile int*)&Gl->done) {  // a peer's proof covers this tree too
+      atomicCAS(&Gl->stop, 0, 1);
+      stop = 1;
+    }
     if (!stop && Gl->timeout_ns && globaltimer() - Gl->t0 >= Gl->timeout_ns) {
       atomicCAS(&Gl->stop, 0, 1);
       stop = 1;
@@ -110,6 +115,10 @@ __device__ __forceinline__ bool time_stop(const G& g, const SearchCtl& C, unsign
   if (g.rank() == 0) {
     Globals* Gl = C.G;
     stop = *(volatile int*)&Gl->stop;
+    if (!stop && *(volatile int*)&Gl->done) {
+      atomicCAS(&Gl->stop, 0, 1);
+      stop = 1;
+    }
     if (!stop && Gl->timeout_ns && globaltimer() - Gl->t0 >= Gl->timeout_ns) {
       atomicCAS(&Gl->stop, 0, 1);
       stop = 1;
@@ -139,7 +148,7 @@ __device__ void record_solution(const G& g, volatile int* S, const DeviceLayout&
     const int old = atomicMin(&Gl->incumbent, value);
     improved = value < old;
     if (improved) {
-      for (int p = 0; p < C.n_peers; ++p) atomicMin_system(C.peers[p], value);
+      for (int p = 0; p < C.n_peers; ++p) atomicMin_system(&C.peers[p]->incumbent, value);
       while (atomicCAS(&Gl->best_lock, 0, 1) != 0) {
       }
     }
@@ -599,6 +608,15 @@ __global__ void k_shard_filter(const int* idx, int* out, int shard, int shards, 
 }
 
 __global__ void k_init_clock(Globals* G) { G->t0 = globaltimer(); }
+
+// A proof over the whole tree (an unsharded primal segment exhausted): every
+// peer may stop (stop_rank0 reads `done`).
+__global__ void k_signal_done(Globals* const* peers, int n) {
+  for (int p = 0; p < n; ++p) atomicExch_system(&peers[p]->done, 1);
+}
+
+// Offer a bound to the incumbent cell (an objective value some solution has).
+__global__ void k_offer_incumbent(Globals* G, int v) { atomicMin(&G->incumbent, v); }
 
 struct SearchParams {
   const int* frontier;

@@ -167,14 +167,17 @@ int cmd_solve(const Config& cfg) {
     }
   }
 
-  // finish() (solver.cpp:148-162) over the union of the shards.
-  bool exhausted = true, has = false;
+  // finish() (solver.cpp:148-162) over the union of the shards: every shard
+  // exhausted (they partition one bound-free EPS frontier), or one GPU's
+  // primal dive exhausted the whole tree.
+  bool exhausted = true, has = false, whole_tree = false;
   std::int32_t obj = 0;
   int owner = -1;
   std::uint64_t nodes = 0, primal_nodes = 0, restarts = 0;
   for (int i = 0; i < n; ++i) {
     const pccp_solve_result& r = res[static_cast<std::size_t>(i)];
     exhausted = exhausted && (r.status == PCCP_OPTIMAL || r.status == PCCP_UNSAT);
+    whole_tree = whole_tree || r.primal_proved;
     nodes += r.stats.nodes;
     primal_nodes += r.primal_nodes;
     restarts += static_cast<std::uint64_t>(r.primal_restarts);
@@ -183,6 +186,7 @@ int cmd_solve(const Config& cfg) {
       obj = r.objective;
     }
   }
+  exhausted = exhausted || whole_tree;
   for (int i = 0; i < n && has; ++i) {
     const pccp_solve_result& r = res[static_cast<std::size_t>(i)];
     if (r.has_objective == 1 && r.objective == obj) {

@@ -45,8 +45,10 @@ def combine_enum(results: list[dict]) -> dict:
 
 def combine_solve(results: list[dict]) -> dict:
     """finish() (solver.cpp:148-162) over the union of the shards: a proof needs
-    every shard exhausted; the objective is the minimum over ranks."""
-    exhausted = all(r["exhausted"] for r in results)
+    every shard exhausted — the shards partition one bound-free EPS frontier
+    (engine.cu run_search) — or one rank's primal dive exhausted the WHOLE tree
+    (`proved`); the objective is the minimum over ranks."""
+    exhausted = all(r["exhausted"] for r in results) or any(r.get("proved", False) for r in results)
     objs = [r["objective"] for r in results if r["objective"] is not None]
     obj = min(objs) if objs else None
     if obj is not None:
@@ -87,8 +89,14 @@ def run_solve(engine, timeout_s: float = 0.0, root=None, group=None,
               check: Callable[[np.ndarray], bool] | None = None) -> dict:
     """Branch and bound over this rank's shard with the shared incumbent; returns
     the combined result (and the best store, gathered from its owner) on every rank."""
+    import torch.distributed as dist
+    # every rank resets its cross-rank cells before any rank starts: a peer's
+    # push must not be wiped by a late reset (include/pccp_gpu.h)
+    engine.reset_shared()
+    dist.barrier(group)
     r = engine.solve(root=root, timeout_s=timeout_s)
     local = {"objective": r.objective, "exhausted": r.status in ("OPTIMAL", "UNSAT"),
+             "proved": bool(getattr(r, "primal_proved", False)),
              "nodes": r.stats["nodes"], "solutions": r.stats["solutions"], "has_store": r.best_words is not None}
     res = combine_solve(_gather(local, group))
     stores = _gather(r.best_words.tolist() if r.best_words is not None else None, group)

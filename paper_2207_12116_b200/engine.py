@@ -35,6 +35,7 @@ class SolveResult:
     improvements: list = field(default_factory=list)  # (objective, ms since search start)
     best_on_peer: bool = False
     primal: dict | None = None  # {nodes, device_ms, proved} when a primal phase ran (cfg primal_ms)
+    primal_proved: bool = False  # a primal dive exhausted the whole tree: a proof for every shard
 
 
 def device_count() -> int:
@@ -49,11 +50,11 @@ class Engine:
     def __init__(self, device: int = 0, *, group_threads: int = 0, groups_per_cta: int = 0, ctas_per_sm: int = 0,
                  eps_factor: int = 0, shard_index: int = 0, shard_count: int = 1, hash: bool = False,
                  value_order: int = -1, var_order: int = 0, primal_ms: int = 0, audit_nodes: int = 0,
-                 audit_shift: int = 0):
+                 audit_shift: int = 0, record_frontier: bool = False):
         L = N.lib()
         self.cfg = N.PccpGpuCfg(device, group_threads, groups_per_cta, ctas_per_sm, eps_factor, shard_index,
                                 shard_count, int(hash), 0, value_order, var_order, primal_ms, audit_nodes,
-                                audit_shift)
+                                audit_shift, int(record_frontier))
         h = C.c_void_p()
         N.check(L.pccp_gpu_open(C.byref(self.cfg), C.byref(h)))
         self._h = h
@@ -145,7 +146,7 @@ class Engine:
                       "restarts": res.primal_restarts}
         return SolveResult(N.STATUS_NAMES[res.status], res.objective if has else None, _stats(res.stats),
                            best[: self.tables.n_words] if has == 1 else None, imp, best_on_peer=has == 2,
-                           primal=primal)
+                           primal=primal, primal_proved=bool(res.primal_proved))
 
     def audit(self):
         """(pre, post, failed) of the nodes the last search sampled (cfg audit_nodes)."""
@@ -167,3 +168,29 @@ class Engine:
         raw = b"".join(h.ljust(64, b"\0")[:64] for h in handles)
         buf = (C.c_uint8 * max(len(raw), 1)).from_buffer_copy(raw or b"\0")
         N.check(N.lib().pccp_gpu_attach_peers(self._h, buf, len(handles), self_index))
+
+    def reset_shared(self) -> None:
+        """Reset the cross-rank cells (incumbent, best lock, done flag); with peers
+        attached a solve never does it itself (include/pccp_gpu.h)."""
+        N.check(N.lib().pccp_gpu_reset_shared(self._h))
+
+    def offer_incumbent(self, value: int) -> None:
+        """atomicMin a known objective value into the incumbent cell."""
+        N.check(N.lib().pccp_gpu_offer_incumbent(self._h, int(value)))
+
+    def frontier(self):
+        """(all, share): store hashes of the last search's shared EPS frontier and of
+        this shard's positions (cfg record_frontier)."""
+        na, ns = C.c_uint32(0), C.c_uint32(0)
+        N.check(N.lib().pccp_gpu_frontier(self._h, None, C.byref(na), None, C.byref(ns), 0))
+        a = np.zeros(max(na.value, 1), np.uint64)
+        b = np.zeros(max(ns.value, 1), np.uint64)
+        N.check(N.lib().pccp_gpu_frontier(self._h, _vp(a), C.byref(na), _vp(b), C.byref(ns), max(a.size, b.size)))
+        return a[: na.value], b[: ns.value]
+
+
+def link_peers(engines: list) -> None:
+    """pccp_gpu_link_peers: contexts of one process share the incumbent (and the
+    done flag) through peer memory; contexts on one device are linked directly."""
+    arr = (C.c_void_p * len(engines))(*[e._h.value for e in engines])
+    N.check(N.lib().pccp_gpu_link_peers(arr, len(engines)))

@@ -25,8 +25,12 @@ class FakeEnumEngine:
 
 
 class FakeSolveEngine:
-    def __init__(self, rank, objective, exhausted):
-        self.rank, self.objective, self.exhausted = rank, objective, exhausted
+    def __init__(self, rank, objective, exhausted, proved=False):
+        self.rank, self.objective, self.exhausted, self.proved = rank, objective, exhausted, proved
+        self.resets = 0
+
+    def reset_shared(self):
+        self.resets += 1
 
     def solve(self, root=None, timeout_s=0.0):
         import numpy as np
@@ -39,6 +43,7 @@ class FakeSolveEngine:
             "SAT" if self.objective is not None else "UNKNOWN")
         r.stats = {"nodes": 1000, "solutions": 1 if self.objective is not None else 0}
         r.best_words = None if self.objective is None else np.full(4, self.objective, np.int32)
+        r.primal_proved = self.proved
         return r
 
 
@@ -58,8 +63,11 @@ def _worker(rank, world, port, q):
         s1 = run_solve(FakeSolveEngine(rank, [57, 55][rank], True))
         s2 = run_solve(FakeSolveEngine(rank, [None, 61][rank], [True, False][rank]))
         s3 = run_solve(FakeSolveEngine(rank, None, True))
+        # rank 1's primal dive exhausted the whole tree; rank 0 was told to stop (unfinished)
+        f4 = FakeSolveEngine(rank, [70, 64][rank], False, proved=rank == 1)
+        s4 = run_solve(f4)
         q.put((rank, e, s1["status"], s1["objective"], int(s1["best_words"][0]), s2["status"], s2["objective"],
-               s3["status"]))
+               s3["status"], s4["status"], s4["objective"], f4.resets))
     finally:
         dist.destroy_process_group()
 
@@ -75,13 +83,14 @@ def test_two_rank_combination_over_gloo():
     for p in procs:
         p.join(timeout=60)
         assert p.exitcode == 0
-    for rank, e, st1, ob1, bw, st2, ob2, st3 in out:
+    for rank, e, st1, ob1, bw, st2, ob2, st3, st4, ob4, resets in out:
         assert e["nodes"] == 201 and e["solutions"] == 7 and e["failures"] == 20
         assert e["hash_sum"] == (2 * 2**64 - 9) % 2**64
         assert e["exhausted"] and e["device_ms"] == 2.0
         assert (st1, ob1, bw) == ("OPTIMAL", 55, 55)   # min over ranks, store from the owner
         assert (st2, ob2) == ("SAT", 61)               # one shard unfinished: no proof
         assert st3 == "UNSAT"
+        assert (st4, ob4, resets) == ("OPTIMAL", 64, 1)  # a whole-tree primal proof is the job's proof
 
 
 def test_shards_partition_the_frontier():
@@ -97,6 +106,11 @@ def test_shards_partition_the_frontier():
 
 def test_combine_rules():
     assert combine_solve([{"objective": None, "exhausted": False, "nodes": 1, "solutions": 0}])["status"] == "UNKNOWN"
+    two = [{"objective": 9, "exhausted": True, "nodes": 1, "solutions": 1},
+           {"objective": 8, "exhausted": False, "nodes": 1, "solutions": 1}]
+    assert combine_solve(two)["status"] == "SAT"
+    two[0]["proved"] = True
+    assert combine_solve(two)["status"] == "OPTIMAL" and combine_solve(two)["objective"] == 8
     r = combine_enum([{"nodes": 5, "hash_sum": 2**64 - 1, "exhausted": True},
                       {"nodes": 6, "hash_sum": 2, "exhausted": False}])
     assert r["nodes"] == 11 and r["hash_sum"] == 1 and not r["exhausted"]

@@ -94,3 +94,99 @@ def test_bench_two_ranks_on_one_device():
     d = json.loads(lines[0])
     assert d["n_gpus"] == 2 and d["parity"]["exact"], d["parity"]
     assert d["value"] > 0 and d["e2e"]["value"] > 0 and d["gpu_launches"] > 0
+
+
+# ---- soundness of sharded minimisation -------------------------------------------
+# The shards partition ONE frontier: phase A of the EPS decomposition runs
+# without the objective join while shard_count > 1 (engine.cu run_search), so
+# it is the same on every shard whatever incumbent each has seen.  The shards
+# run one after the other in one process with linked incumbents, so shard k
+# starts its phase A after shards < k pushed their solutions into its cell
+# (plus a pre-seeded bound on shard 1): the situation in which a
+# bound-dependent frontier would shift positions and lose subtrees.
+RCPSP30_OPTIMA = {1: 84, 2: 77, 5: 73, 7: 60, 9: 61, 11: 99}
+
+
+def _sharded_solve(model, n, seed_bound=None, primal_ms=0, timeout_s=120):
+    import numpy as np
+
+    from paper_2207_12116_b200 import Engine
+    from paper_2207_12116_b200.distributed import combine_solve
+    from paper_2207_12116_b200.engine import link_peers
+    engs = [Engine(0, shard_index=k, shard_count=n, record_frontier=True, primal_ms=primal_ms) for k in range(n)]
+    try:
+        for e in engs:
+            e.load(model)
+        link_peers(engs)
+        if seed_bound is not None:
+            engs[1].offer_incumbent(seed_bound)
+        res, fronts = [], []
+        for e in engs:
+            r = e.solve(timeout_s=timeout_s)
+            res.append(r)
+            fronts.append(e.frontier())
+        local = [{"objective": r.objective, "exhausted": r.status in ("OPTIMAL", "UNSAT"), "proved": r.primal_proved,
+                  "nodes": r.stats["nodes"], "solutions": r.stats["solutions"], "has_store": r.best_words is not None}
+                 for r in res]
+        comb = combine_solve(local)
+        best = None
+        if comb["owner"] is not None:
+            best = res[comb["owner"]].best_words
+        return comb, res, fronts, best
+    finally:
+        for e in engs:
+            e.close()
+
+
+def _check_partition(fronts):
+    import numpy as np
+    searched = [(a, s) for a, s in fronts if a.size]  # a shard stopped by a peer's proof has none
+    if not searched:
+        return
+    all0 = np.sort(searched[0][0])
+    assert len(np.unique(all0)) == all0.size
+    for a, _ in searched:  # the shared phase A is identical on every shard
+        assert np.array_equal(np.sort(a), all0)
+    if len(searched) == len(fronts):  # the shares partition it
+        shares = np.sort(np.concatenate([s for _, s in fronts]))
+        assert np.array_equal(shares, all0)
+
+
+@pytest.mark.parametrize("n_shards", [2, 4, 8])
+@pytest.mark.parametrize("seed", sorted(RCPSP30_OPTIMA))
+def test_sharded_minimisation_is_sound(seed, n_shards):
+    from paper_2207_12116_b200 import Model
+    m = Model.rcpsp_random(seed, 30, 4)
+    opt = RCPSP30_OPTIMA[seed]
+    comb, res, fronts, best = _sharded_solve(m, n_shards, seed_bound=opt + 3)
+    _check_partition(fronts)
+    assert all(f[0].size for f in fronts)  # no primal phase: every shard ran the exact search
+    assert comb["status"] == "OPTIMAL" and comb["objective"] == opt, (comb, [r.status for r in res])
+    assert best is not None and m.check_solution(best)
+
+
+@pytest.mark.parametrize("n_shards", [2, 4])
+@pytest.mark.parametrize("seed", [1, 7, 9])
+def test_sharded_minimisation_with_primal_phase(seed, n_shards):
+    from paper_2207_12116_b200 import Model
+    m = Model.rcpsp_random(seed, 30, 4)
+    opt = RCPSP30_OPTIMA[seed]
+    comb, res, fronts, best = _sharded_solve(m, n_shards, primal_ms=2000)
+    _check_partition(fronts)
+    assert comb["status"] == "OPTIMAL" and comb["objective"] == opt, (comb, [r.status for r in res])
+    assert best is not None and m.check_solution(best)
+
+
+@pytest.mark.parametrize("n_shards", [2, 4, 8])
+def test_sharded_micro_rcpsp_optima(n_shards):
+    """The 200 micro RCPSPs of the optimality criterion (acceptance_main.cpp:243-287)
+    solved as n linked shards, shard 1 pre-seeded with brute force + 1."""
+    from conftest import load_micro_rcpsps
+    for t, rec in load_micro_rcpsps():
+        bf = rec["brute_force"]
+        comb, res, fronts, _ = _sharded_solve(t, n_shards, seed_bound=None if bf is None else bf + 1)
+        _check_partition(fronts)
+        if bf is None:
+            assert comb["status"] == "UNSAT"
+        else:
+            assert comb["status"] == "OPTIMAL" and comb["objective"] == bf, (rec, comb)
