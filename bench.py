@@ -125,6 +125,42 @@ def load_peaks():
         return {}
 
 
+def smem_peak_gbs(sm_mhz):
+    """Shared-memory bandwidth: 148 SMs x 128 B/clk at the given SM clock."""
+    return 148 * 128 * sm_mhz * 1e6 / 1e9
+
+
+def roofline(st, info, sm_mhz, world=1):
+    """Roofline of the persistent search kernel (k_search) from one search's
+    stats, on the LOWERED records' byte model (pccp_lowering_info): a round
+    reads store_bytes_per_round of the store (shared memory) and
+    table_bytes_per_round of the tables (shared memory when table_in_smem,
+    else L2).  achieved = search rounds x bytes per round / k_search time.
+
+    Also reported, not used for `frac`: the per-reference-command model of
+    SURVEY 8(d) (alg_bytes_per_eval x evals), which counts a word once per
+    reference command reading it — a fused record reads it once for several
+    commands, so that ratio can pass 1 (`per_command_model_ratio`)."""
+    ks = st["kernel_ms"] / 1e3
+    if ks <= 0:
+        return None
+    rounds = st["search_evals"] / max(info["n_cmds"], 1)
+    tis = bool(info["table_in_smem"])
+    bpr = info["store_bytes_per_round"] + (info["table_bytes_per_round"] if tis else 0.0)
+    achieved = rounds * bpr / ks / 1e9 / world
+    peak = smem_peak_gbs(sm_mhz)
+    d = {"bound": "smem", "kernel": "k_search", "achieved": achieved, "peak": peak, "unit": "GB/s",
+         "frac": achieved / peak, "bytes_per_round": bpr, "store_bytes_per_round": info["store_bytes_per_round"],
+         "table_bytes_per_round": info["table_bytes_per_round"], "table_in_smem": tis,
+         "search_rounds": rounds, "kernel_ms": st["kernel_ms"],
+         "evals_per_s": st["search_evals"] / ks / world,
+         "per_command_model_ratio": st["search_evals"] * info["alg_bytes_per_eval"] / ks / 1e9 / world / peak,
+         "peak_source": f"148 SMs x 128 B/clk x {sm_mhz:.0f} MHz"}
+    if not tis:
+        d["l2_table_gbs"] = rounds * info["table_bytes_per_round"] / ks / 1e9 / world
+    return d
+
+
 def ncu_kernel(workload):
     """The committed ncu --set full summary of k_search for a workload (profiles/)."""
     p = os.path.join(ROOT, "profiles", "ncu_summary.json")
@@ -193,15 +229,13 @@ def time_to_optimum(local, rank, world, dist):
             t_first = min(x for x in _gather_obj(dist, t_first))
             t_proof = max(_gather_obj(dist, t_proof))
         st = local_r.stats
-        b_alg = eng.lowering_info()["alg_bytes_per_eval"]
         sm_mhz = load_peaks().get("sm_max_mhz", 1965.0)
-        ev_s = st["search_evals"] / (st["kernel_ms"] / 1e3) if st["kernel_ms"] > 0 else 0.0
         out[str(seed)] = {"status": status, "objective": obj, "valid": bool(ok),
                           "matches_reference": obj == TTO_OPTIMA[seed], "t_first_optimal_ms": t_first,
                           "t_proof_ms": t_proof, "t_wall_ms": local_r.stats["elapsed_ms"],
                           "nodes": local_r.stats["nodes"],
                           "tree_nodes": local_r.stats["nodes"] - local_r.stats["rematerialised"],
-                          "k_search": {"ms": st["kernel_ms"], "evals_per_s": ev_s}}
+                          "roofline": roofline(st, eng.lowering_info(), sm_mhz)}
     eng.close()
     return {"config": "rcpsp 30 tasks x 4 resources, random_patterson(mt19937_64(seed)), minimise makespan",
             "note": "node counts differ from the CPU only through search order and incumbent timing",
@@ -245,27 +279,70 @@ def stretch_and_large(local, rank, world, dist, timeout_s, large_timeout_s):
     stretch = {"config": "rcpsp 30x4 stretch seeds (unproven by the reference CPU solver)",
                "timeout_s": timeout_s, "gpu": out}
 
+    large = rcpsp120(local, rank, world, dist, large_timeout_s)
+    return stretch, large
+
+
+def destructive_lower_bound(eng, m, lo, hi):
+    """The smallest makespan T in [lo, hi) whose root fixed point under
+    `makespan <= T` does not fail: every T below it is refuted by propagation
+    alone, so it is a lower bound on the optimum (the classic destructive
+    bound).  All candidate T go through one pccp_gpu_propagate_batch."""
+    import numpy as np
+    if hi <= lo:
+        return lo
+    t = m.tables()
+    ub_word = int(t.slot_word[m.starts()[-1]]) + 1
+    ts = np.arange(lo, hi, dtype=np.int64)
+    stores = np.repeat(m.bottom()[None, :], len(ts), axis=0)
+    stores[:, ub_word] = np.minimum(stores[:, ub_word], ts)
+    _, failed, _ = eng.propagate_batch(stores)
+    ok = np.nonzero(~failed)[0]
+    return int(ts[ok[0]]) if ok.size else int(hi)
+
+
+def rcpsp120(local, rank, world, dist, budget_s):
+    """Config 5: RCPSP 120x4 seed 1.  (1) The reference's branching order alone
+    (branch(), solver.cpp:19-47; no incumbent is found in that order) for a few
+    seconds: nodes/s and the k_search roofline.  (2) The solve with the primal
+    phase for `budget_s`: the incumbent over time (every improvement) and the
+    gap to the best lower bound (root critical path; destructive bound)."""
+    from paper_2207_12116_b200 import Engine, Model
+    from paper_2207_12116_b200.distributed import attach_incumbents
     m = Model.rcpsp_random(1, 120, 4)
-    eng = Engine(local, shard_index=rank, shard_count=world, primal_ms=int(large_timeout_s * 1e3))
+    sm = load_peaks().get("sm_max_mhz", 1965.0)
+    with Engine(local, shard_index=rank, shard_count=world) as e0:  # unlinked: nothing to share
+        e0.load(m)
+        r0 = e0.solve(timeout_s=3.0)
+        ref_order = {"status": r0.status, "nodes": r0.stats["nodes"], "device_ms": r0.stats["device_ms"],
+                     "nodes_per_s": r0.stats["nodes"] / (r0.stats["device_ms"] / 1e3),
+                     "roofline": roofline(r0.stats, e0.lowering_info(), sm)}
+        if world > 1:
+            ref_order["nodes_per_s_all_ranks"] = sum(_gather_obj(dist, ref_order["nodes_per_s"]))
+    eng = Engine(local, shard_index=rank, shard_count=world, primal_ms=int(budget_s * 1e3))
     eng.load(m)
     if world > 1:
         attach_incumbents(eng)
     failed, root, _ = eng.run_sequential()
     sink = int(m.tables().slot_word[m.starts()[-1]])
-    status, obj, ok, r = _solve_on_ranks(eng, m, world, dist, large_timeout_s)
+    status, obj, ok, r = _solve_on_ranks(eng, m, world, dist, budget_s)
     first = r.improvements[0] if r.improvements else (None, None)
     t_best = min((ms for v, ms in r.improvements if v == obj), default=None)
     if world > 1:
         t_best = min(x for x in _gather_obj(dist, t_best if t_best is not None else float("inf")))
+    lb_root = int(root[sink])
+    lb = destructive_lower_bound(eng, m, lb_root, obj if obj is not None else lb_root + 64)
     eng.close()
-    large = {"config": "rcpsp 120x4 seed 1 (random_patterson(mt19937_64(1), 120, 4)), minimise makespan",
-             "timeout_s": large_timeout_s, "status": status, "objective": obj, "valid": bool(ok),
-             "root_lower_bound": int(root[sink]), "first": {"objective": first[0], "t_ms": first[1]},
-             "t_best_ms": t_best, "nodes": r.stats["nodes"], "nodes_per_s": r.stats["nodes"] / (r.stats["device_ms"] / 1e3),
-             "primal": r.primal,
-             "note": "the reference's branching order reaches no leaf (SURVEY 8d); the primal phase's incumbents "
-                     "are ordinary solutions of the same model, checked by check_solution"}
-    return stretch, large
+    return {"config": "rcpsp 120x4 seed 1 (random_patterson(mt19937_64(1), 120, 4)), minimise makespan",
+            "timeout_s": budget_s, "status": status, "objective": obj, "valid": bool(ok),
+            "lower_bound": {"root_critical_path": lb_root, "destructive": lb},
+            "gap": None if obj is None else (obj - lb) / obj,
+            "first": {"objective": first[0], "t_ms": first[1]}, "t_best_ms": t_best,
+            "incumbent_over_time": [[v, ms] for v, ms in r.improvements],
+            "nodes": r.stats["nodes"], "nodes_per_s": r.stats["nodes"] / (r.stats["device_ms"] / 1e3),
+            "primal": r.primal, "reference_order": ref_order,
+            "note": "the reference's branching order reaches no leaf (SURVEY 8d); the primal phase's incumbents "
+                    "are ordinary solutions of the same model, checked by check_solution"}
 
 
 def cpu_large(threads, budget_s):
@@ -293,6 +370,7 @@ def enumeration_configs(local, rank, world, dist, cpu, threads):
         m = build_model(w)
         with Engine(local, shard_index=rank, shard_count=world) as eng:
             eng.load(m)
+            info = eng.lowering_info()
             for _ in range(3):
                 r = eng.enumerate(depth_cap=w["depth"])
             runs = []
@@ -311,9 +389,8 @@ def enumeration_configs(local, rank, world, dist, cpu, threads):
              "parity": all(int(hr[k]) == v for k, v in exp.items())}
         if world == 1:
             r = runs[-1]
-            if r["kernel_ms"] > 0:
-                ev_s = r["search_evals"] / (r["kernel_ms"] / 1e3)
-                d["k_search"] = {"ms": r["kernel_ms"], "decompose_ms": r["decompose_ms"], "evals_per_s": ev_s}
+            d["decompose_ms"] = r["decompose_ms"]
+            d["roofline"] = roofline(r, info, load_peaks().get("sm_max_mhz", 1965.0))
         if cpu:
             c = cpu_reference(dict(w, workload=name), 3.0, threads)
             d["cpu_reference"] = {"nodes_per_s": c["value"], "threads": c["cores"], "kind": c["kind"],
@@ -418,7 +495,9 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-tto", action="store_true", help="skip the RCPSP time-to-optimum sections")
     ap.add_argument("--stretch-timeout", type=float, default=10.0)
-    ap.add_argument("--large-timeout", type=float, default=10.0)
+    ap.add_argument("--large-timeout", type=float, default=20.0)
+    ap.add_argument("--cpu-tto-timeout", type=float, default=60.0,
+                    help="budget of each reference solve_parallel in the time-to-optimum comparison")
     a = ap.parse_args()
     w = WORKLOADS[a.config]
     if a.impl == "reference":
@@ -544,25 +623,29 @@ def main():
     e2e_value = total_nodes / sum(e2e_max)
     peaks = load_peaks()
     sm_mhz = (clocks or {}).get("sm_mhz") or peaks.get("sm_max_mhz", 1965.0)
-    smem_peak = 148 * 128 * sm_mhz * 1e6 / 1e9  # GB/s: 148 SMs x 128 B/clk
-    b_alg = info["alg_bytes_per_eval"]
-    achieved = statistics.mean(se * b_alg / (km / 1e3) / 1e9 / world for se, km in zip(sevals_all, kern_max))
+    # roofline of k_search over the timed steps (lowered-record byte model)
+    rl_steps = [roofline({"kernel_ms": km, "search_evals": se, "n_cmds": info["n_cmds"]}, info, sm_mhz, world)
+                for se, km in zip(sevals_all, kern_max)]
+    rl = dict(rl_steps[-1])
+    for k in ("achieved", "frac", "evals_per_s", "per_command_model_ratio", "kernel_ms", "search_rounds"):
+        rl[k] = statistics.mean(x[k] for x in rl_steps)
     nk = ncu_kernel(w["workload"])
-    traffic = nk["dram_bytes_per_launch"] if nk else None
-    kern_s = statistics.mean(kern_max) / 1e3
-    physical = None
-    if nk:  # per-launch ncu counts over this run's live kernel time
-        clk = sm_mhz * 1e6
-        physical = {
-            "smem_gbs": nk["smem_wavefronts"] * 128 / kern_s / 1e9,
-            "smem_frac": nk["smem_wavefronts"] * 128 / kern_s / 1e9 / smem_peak,
-            "issue_frac": nk["warp_instructions"] / kern_s / (148 * 4 * clk),
-            "source": nk["source"],
-            "note": "fused records read each store word once for several reference commands, so the per-command "
-                    "byte model of SURVEY 8(d) (alg_bytes_per_eval) exceeds the physical shared-memory traffic and "
-                    "frac can pass 1; the physical figures are ncu's shared-memory wavefronts (x 128 B) and warp "
-                    "instructions per launch over this run's kernel time: the kernel is instruction-issue bound",
-        }
+    ncu = None
+    if nk:  # the committed capture of this build, on its own (cold-cache, serialised) launch time
+        t = nk["duration_ms"] / 1e3
+        clk = nk.get("sm_clock_mhz", sm_mhz)
+        ncu = {"source": nk["source"], "duration_ms": nk["duration_ms"], "sm_clock_mhz": clk,
+               "smem_wavefront_frac": nk["smem_wavefronts"] * 128 / t / 1e9 / smem_peak_gbs(clk),
+               "issue_frac": nk["warp_instructions"] / t / (148 * 4 * clk * 1e6),
+               "issue_active_pct": nk.get("issue_active_pct"),
+               "bank_conflict_share": nk.get("smem_bank_conflicts", 0) / max(nk.get("smem_wavefronts", 1), 1),
+               "l2_bytes_per_launch": nk.get("l2_bytes_per_launch"),
+               "note": "measured by ncu on the same command line and build, not in this run: wavefronts include "
+                       "bank conflicts and partial-warp accesses, so the physical fraction exceeds the byte model's"}
+    rl["traffic"] = nk["dram_bytes_per_launch"] if nk else None
+    rl["traffic_source"] = nk["source"] if nk else None
+    rl["hbm_peak_gbs"] = peaks.get("hbm_gbs")
+    rl["ncu"] = ncu
     line = {
         "metric": "search nodes/sec", "value": value, "unit": "nodes/s", "n_gpus": world, "steps": a.steps,
         "warmup": a.warmup, "ms_per_step": 1e3 * total_dev_s / a.steps, "higher_is_better": True,
@@ -574,13 +657,7 @@ def main():
         "e2e": {"value": e2e_value, "unit": "nodes/s", "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h),
                 "note": "pccp_gpu_load (lowering + table upload) + pccp_gpu_enumerate from host buffers, host clock"},
         "gpu_launches": int(launches_all),
-        "roofline": {"bound": "smem", "achieved": achieved, "peak": smem_peak, "unit": "GB/s",
-                     "frac": achieved / smem_peak, "traffic": traffic, "kernel": "k_search",
-                     "alg_bytes_per_eval": b_alg,
-                     "evals_per_s": statistics.mean(se / (km / 1e3) for se, km in zip(sevals_all, kern_max)),
-                     "peak_source": f"148 SMs x 128 B/clk x {sm_mhz:.0f} MHz (SM clock sampled during the run); "
-                                    "the path is shared-memory bound (SURVEY 8(d)), HBM/tensor peaks do not apply",
-                     "hbm_peak_gbs": peaks.get("hbm_gbs"), "physical": physical},
+        "roofline": rl,
         "parity": {"exact": all(parity.values()), **parity},
         "region_ms": region_ms, "region_wall_s": region_wall,
         "kernel_ms_per_step": statistics.mean(kern_max),
@@ -593,14 +670,14 @@ def main():
                                 "sample": cb["sample"]}
     if tto is not None:
         if world == 1 and not a.no_cpu_baseline:
-            tto["cpu_reference"] = cpu_time_to_optimum(os.cpu_count() or 1)
+            tto["cpu_reference"] = cpu_time_to_optimum(os.cpu_count() or 1, a.cpu_tto_timeout)
         line["time_to_optimum"] = tto
     if others is not None:
         line["other_configs"] = others
     if stretch is not None:
         line["stretch"] = stretch
         if world == 1 and not a.no_cpu_baseline:
-            large["cpu_reference"] = cpu_large(os.cpu_count() or 1, a.large_timeout)
+            large["cpu_reference"] = cpu_large(os.cpu_count() or 1, min(a.large_timeout, 30.0))
         line["rcpsp120"] = large
     print(json.dumps(line))
     if world > 1:

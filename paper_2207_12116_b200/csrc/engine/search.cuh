@@ -75,11 +75,7 @@ __device__ __forceinline__ int stop_rank0(const SearchCtl& C) {
   int stop = 0;
   {
     Globals* Gl = C.G;
-    stop = *(volatile int*)&Gl->stop;
-    if (!stop && *(volatile int*)&Gl->done) {  // a peer's proof covers this tree too
-      atomicCAS(&Gl->stop, 0, 1);
-      stop = 1;
-    }
+    stop = *(volatile int*)&Gl->stop;  // also raised by a peer's proof (k_signal_done)
     if (!stop && Gl->timeout_ns && globaltimer() - Gl->t0 >= Gl->timeout_ns) {
       atomicCAS(&Gl->stop, 0, 1);
       stop = 1;
@@ -115,10 +111,6 @@ __device__ __forceinline__ bool time_stop(const G& g, const SearchCtl& C, unsign
   if (g.rank() == 0) {
     Globals* Gl = C.G;
     stop = *(volatile int*)&Gl->stop;
-    if (!stop && *(volatile int*)&Gl->done) {
-      atomicCAS(&Gl->stop, 0, 1);
-      stop = 1;
-    }
     if (!stop && Gl->timeout_ns && globaltimer() - Gl->t0 >= Gl->timeout_ns) {
       atomicCAS(&Gl->stop, 0, 1);
       stop = 1;
@@ -607,12 +599,21 @@ __global__ void k_shard_filter(const int* idx, int* out, int shard, int shards, 
   if (k < n_out) out[k] = idx[shard + k * shards];
 }
 
-__global__ void k_init_clock(Globals* G) { G->t0 = globaltimer(); }
+// Search start: the clock, and a peer's proof that landed before this
+// search's reset (`done` survives resets, `stop` does not).
+__global__ void k_init_clock(Globals* G) {
+  G->t0 = globaltimer();
+  if (*(volatile int*)&G->done) atomicCAS(&G->stop, 0, 1);
+}
 
 // A proof over the whole tree (an unsharded primal segment exhausted): every
-// peer may stop (stop_rank0 reads `done`).
+// peer may stop.  `done` persists across the peer's searches; `stop` ends the
+// running one without an extra per-node load (stop_rank0 reads it anyway).
 __global__ void k_signal_done(Globals* const* peers, int n) {
-  for (int p = 0; p < n; ++p) atomicExch_system(&peers[p]->done, 1);
+  for (int p = 0; p < n; ++p) {
+    atomicExch_system(&peers[p]->done, 1);
+    atomicCAS_system(&peers[p]->stop, 0, 1);
+  }
 }
 
 // Offer a bound to the incumbent cell (an objective value some solution has).
