@@ -296,6 +296,8 @@ typedef struct pccp_lowering_info {
   double store_bytes_per_round; /* the lowered records' byte model: store bytes one fixed-point round
                                    reads (fused records read each word once for several commands) */
   double table_bytes_per_round; /* table bytes one round reads (shared memory if table_in_smem, else L2) */
+  uint32_t packed_cells;  /* 0/1 interval cells held as bits of (lb, ub) bit planes (0: plain layout) */
+  uint32_t device_words;  /* words of one device store (= n_words in the plain layout) */
 } pccp_lowering_info;
 
 int pccp_gpu_lowering_info(pccp_gpu_ctx* ctx, pccp_lowering_info* out);
@@ -311,6 +313,15 @@ int pccp_lower_only(const pccp_model* model, pccp_lowering_info* out, uint32_t* 
  * reifications, bit 3 unit records = the families whose 32-bit path the
  * engine would take for these inputs (diagnostics and tests). */
 int pccp_lower_fast_paths(const pccp_model* model, const int32_t* stores, uint32_t n, uint32_t* mask);
+
+/* Host-only: the device store layout the engine picks for this model (bit
+ * planes for its 0/1 cells, lower.hpp lower_packed).  *dev_words gets the
+ * device store size; when dev / back are non-null the n reference stores in
+ * `stores` are converted to it (dev: n * dev_words) and back (back: n *
+ * n_words).  The conversion folds the packed cells' constant tells, as every
+ * entry point does, and keeps an empty 0/1 cell empty (tests, diagnostics). */
+int pccp_lower_layout(const pccp_model* model, const int32_t* stores, uint32_t n, int32_t* dev, int32_t* back,
+                      uint32_t* dev_words);
 
 #ifdef __cplusplus
 }

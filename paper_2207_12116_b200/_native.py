@@ -128,6 +128,8 @@ class PccpLoweringInfo(C.Structure):
         ("alg_bytes_per_eval", C.c_double),
         ("store_bytes_per_round", C.c_double),
         ("table_bytes_per_round", C.c_double),
+        ("packed_cells", C.c_uint32),
+        ("device_words", C.c_uint32),
     ]
 
 
@@ -163,6 +165,7 @@ def lib():
         "pccp_gpu_reset_shared": (C.c_int, [vp]),
         "pccp_gpu_offer_incumbent": (C.c_int, [vp, i32]),
         "pccp_gpu_frontier": (C.c_int, [vp, vp, P(u32), vp, P(u32), u32]),
+        "pccp_lower_layout": (C.c_int, [P(PccpModel), vp, u32, vp, vp, P(u32)]),
         # host model builder
         "pccp_host_last_error": (C.c_char_p, []),
         "pccp_host_new": (vp, []),

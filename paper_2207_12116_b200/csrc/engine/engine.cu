@@ -97,7 +97,8 @@ struct pccp_gpu_ctx {
   cudaEvent_t ev[6] = {};
   bool loaded = false;
 
-  Lowered low;
+  Lowered low;  // the plain lowering (reference words): value-range analysis, byte models
+  Lowered dl;   // the device layout: bit-plane 0/1 cells when the model has them (lower_packed), else = low
   std::vector<std::uint8_t> slot_kind;
   std::vector<std::uint32_t> slot_word;
   pccp_model view{};  // host copy of the slot tables (commands not kept)
@@ -137,7 +138,7 @@ struct pccp_gpu_ctx {
   dev::Model model(int var_order = 0, unsigned var_seed = 0, const std::int32_t* stores = nullptr,
                    std::size_t n_stores = 0, std::size_t stride = 0) const {
     dev::Model M;
-    M.L = low.L;
+    M.L = dl.L;
     M.L.var_order = (std::uint32_t)var_order;
     M.L.var_seed = var_seed;
     bool ne = false, rows = false, reif = false, unit = false;
@@ -199,7 +200,7 @@ void dispatch(const pccp_gpu_ctx* c, Fn&& f) {
 }
 
 void plan(pccp_gpu_ctx* c) {
-  const DeviceLayout& L = c->low.L;
+  const DeviceLayout& L = c->dl.L;
   c->store_stride = (int)align4(L.n_words + 1);  // + the constant-zero word
   const int gt = c->cfg.group_threads;
   c->warp = gt == 32 || (gt == 0 && L.n_words <= 256);
@@ -300,11 +301,12 @@ void reset_globals(pccp_gpu_ctx* c, const pccp_limits* lim, bool keep_incumbent 
 
 // Depth bound for the DFS stacks: a variable of width w can be bisected at
 // most ceil(log2 w) times along one path (solver.cpp:44-46).
+// `root` is in the device layout.
 int depth_bound(const pccp_gpu_ctx* c, const std::vector<std::int32_t>& root) {
-  const DeviceLayout& L = c->low.L;
+  const DeviceLayout& L = c->dl.L;
   long long d = 2;
   for (std::uint32_t i = 0; i < L.n_cand; ++i) {
-    const int w = c->low.blob[L.cand_lbw + i];
+    const int w = c->dl.blob[L.cand_lbw + i];
     const long long lo = root[w], hi = root[w + 1];
     if (lo == INT32_MIN || hi == INT32_MAX) {
       d += 33;
@@ -339,14 +341,16 @@ std::uint64_t host_store_hash(const std::int32_t* w, std::uint32_t n) {
 // cfg.record_frontier: hashes of the frontier in (fa, ia) and of the share
 // i = shard (mod shards) this GPU keeps (tests of the partition).
 void record_frontier(pccp_gpu_ctx* c, int count, int stride, int shard, int shards) {
-  const std::uint32_t nw = c->low.L.n_words;
+  const std::uint32_t nw = c->low.L.n_words;  // hashed in the reference layout
+  std::vector<std::int32_t> ref(nw);
   std::vector<int> idx((size_t)count);
   CK(cudaMemcpyAsync(idx.data(), c->ia.p, (size_t)count * 4, cudaMemcpyDeviceToHost, c->stream));
   std::vector<std::int32_t> st((size_t)c->fa.n);
   CK(cudaMemcpyAsync(st.data(), c->fa.p, c->fa.n * 4, cudaMemcpyDeviceToHost, c->stream));
   CK(cudaStreamSynchronize(c->stream));
   for (int i = 0; i < count; ++i) {
-    const std::uint64_t h = host_store_hash(st.data() + (size_t)idx[(size_t)i] * (size_t)stride, nw);
+    to_reference(c->dl, st.data() + (size_t)idx[(size_t)i] * (size_t)stride, ref.data());
+    const std::uint64_t h = host_store_hash(ref.data(), nw);
     c->frontier_all.push_back(h);
     if (i % shards == shard) c->frontier_share.push_back(h);
   }
@@ -358,15 +362,15 @@ void run_search(pccp_gpu_ctx* c, int mode, const int32_t* root_words, int depth_
                 unsigned var_seed = 0, bool sharded = true) {
   const double t_start = now_ms();
   const std::uint64_t launches0 = c->launches;
-  const DeviceLayout& L = c->low.L;
-  const int nw = (int)L.n_words;
+  const DeviceLayout& L = c->dl.L;
+  const int nw = (int)L.n_words;  // device store words
   const int stride = c->store_stride;
   // sharded = false: this search covers the whole tree on this GPU (the
   // primal segments of an N-shard solve), counted by it alone
   const int shard_count = sharded ? std::max(1, c->cfg.shard_count) : 1;
   const int shard_index = sharded ? c->cfg.shard_index : 0;
   if (shard_index < 0 || shard_index >= shard_count) throw ArgError("shard_index out of range");
-  const dev::Model M = c->model(var_order, var_seed, root_words, 1, (size_t)nw);
+  const dev::Model M = c->model(var_order, var_seed, root_words, 1, (size_t)c->low.L.n_words);
   dev::SearchCtl C{};
   C.G = c->G;
   C.n_peers = mode == 1 ? c->n_peers : 0;
@@ -413,7 +417,8 @@ void run_search(pccp_gpu_ctx* c, int mode, const int32_t* root_words, int depth_
   c->ia.ensure(1);
   c->flags.ensure(2);
   reset_globals(c, lim, keep_incumbent, stall_ns);
-  std::vector<std::int32_t> root(root_words, root_words + nw);
+  std::vector<std::int32_t> root((size_t)nw);
+  to_device(c->dl, root_words, root.data());
   CK(cudaMemcpyAsync(c->fa.p, root.data(), (size_t)nw * 4, cudaMemcpyHostToDevice, c->stream));
   const int zero = 0;
   CK(cudaMemcpyAsync(c->ia.p, &zero, 4, cudaMemcpyHostToDevice, c->stream));
@@ -790,6 +795,8 @@ int pccp_gpu_load(pccp_gpu_ctx* c, const pccp_model* m) {
     c->loaded = false;
     c->low = lower_model(*m);
     if (c->low.L.n_cand >= (1u << 24)) throw LimitError("more than 2^24 branching candidates");
+    // bit-plane cells only where the plain lowering found reifications or rows
+    c->dl = (c->low.L.n_reif || c->low.L.n_rows) ? lower_packed(*m) : c->low;
     reset_shared(c);  // an incumbent of the previous model means nothing for this one
     c->slot_kind.assign(m->slot_kind, m->slot_kind + m->n_slots);
     c->slot_word.assign(m->slot_word, m->slot_word + m->n_slots);
@@ -799,8 +806,8 @@ int pccp_gpu_load(pccp_gpu_ctx* c, const pccp_model* m) {
     c->view.cmd_off = nullptr;
     c->view.cmd_code = nullptr;
     c->view.cands = nullptr;
-    c->blob.ensure(c->low.blob.size() + 4);
-    CK(cudaMemcpyAsync(c->blob.p, c->low.blob.data(), c->low.blob.size() * 4, cudaMemcpyHostToDevice, c->stream));
+    c->blob.ensure(c->dl.blob.size() + 4);
+    CK(cudaMemcpyAsync(c->blob.p, c->dl.blob.data(), c->dl.blob.size() * 4, cudaMemcpyHostToDevice, c->stream));
     plan(c);
     // Size the DFS stacks here rather than in the first solve: the depth bound
     // of the bottom store under the folded constant tells bounds the one of any
@@ -822,8 +829,10 @@ int pccp_gpu_load(pccp_gpu_ctx* c, const pccp_model* m) {
         const int w = c->low.blob[L.cand_lbw + i];
         if (r0[w] == INT32_MIN || r0[w + 1] == INT32_MAX) bounded = false;
       }
-      const size_t entry = align4(L.n_words + 3);
-      const size_t bytes = bounded ? (size_t)c->groups() * (size_t)depth_bound(c, r0) * entry * 4 : 0;
+      std::vector<std::int32_t> d0(c->dl.L.n_words);
+      to_device(c->dl, r0.data(), d0.data());
+      const size_t entry = align4(c->dl.L.n_words + 3);
+      const size_t bytes = bounded ? (size_t)c->groups() * (size_t)depth_bound(c, d0) * entry * 4 : 0;
       // Best effort: at most a quarter of the free device memory (several
       // contexts may share a device); a solve whose root needs more sizes
       // the stacks itself (run_search), and a failed allocation here only
@@ -860,8 +869,10 @@ int pccp_gpu_lowering_info(pccp_gpu_ctx* c, pccp_lowering_info* o) {
     o->n_rows = L.n_rows;
     o->n_row_terms = L.n_row_terms;
     o->n_generic = L.n_gen;
-    o->table_bytes = L.blob_words * 4;
-    o->store_bytes = L.n_words * 4;
+    o->table_bytes = c->dl.L.blob_words * 4;
+    o->store_bytes = c->dl.L.n_words * 4;
+    o->packed_cells = (std::uint32_t)c->dl.bit_lbw.size();
+    o->device_words = c->dl.L.n_words;
     o->group_threads = c->warp ? 32 : c->block;
     o->groups_per_cta = c->warp ? c->gpc : 1;
     o->ctas = c->ctas;
@@ -869,8 +880,8 @@ int pccp_gpu_lowering_info(pccp_gpu_ctx* c, pccp_lowering_info* o) {
     o->table_in_smem = c->table_in_smem;
     o->stack_in_smem = 0;
     o->alg_bytes_per_eval = c->low.alg_bytes_per_eval;
-    o->store_bytes_per_round = c->low.store_bytes_per_round;
-    o->table_bytes_per_round = c->low.table_bytes_per_round;
+    o->store_bytes_per_round = c->dl.store_bytes_per_round;
+    o->table_bytes_per_round = c->dl.table_bytes_per_round;
     o->stack_depth = 0;
     return PCCP_OK;
   });
@@ -882,6 +893,11 @@ int pccp_lower_only(const pccp_model* m, pccp_lowering_info* o, uint32_t* shape_
     const Lowered low = lower_model(*m);
     const DeviceLayout& L = low.L;
     std::memset(o, 0, sizeof(*o));
+    {
+      const Lowered pk = lower_packed(*m);
+      o->packed_cells = (std::uint32_t)pk.bit_lbw.size();
+      o->device_words = pk.L.n_words;
+    }
     o->n_words = L.n_words;
     o->n_cmds = L.n_ref_cmds;
     o->n_folded = L.n_fold;
@@ -917,18 +933,42 @@ int pccp_lower_fast_paths(const pccp_model* m, const int32_t* stores, uint32_t n
   });
 }
 
+int pccp_lower_layout(const pccp_model* m, const int32_t* stores, uint32_t n, int32_t* dev, int32_t* back,
+                      uint32_t* dev_words) {
+  return api([&] {
+    if (!m || !dev_words || (n && !stores)) throw ArgError("null argument");
+    const Lowered d = lower_packed(*m);
+    *dev_words = d.L.n_words;
+    const size_t rw = m->n_words, dw = d.L.n_words;
+    for (uint32_t i = 0; i < n; ++i) {
+      std::vector<std::int32_t> t(dw);
+      to_device(d, stores + i * rw, t.data());
+      if (dev) std::copy(t.begin(), t.end(), dev + i * dw);
+      if (back) to_reference(d, t.data(), back + i * rw);
+    }
+    return PCCP_OK;
+  });
+}
+
 int pccp_gpu_propagate_batch(pccp_gpu_ctx* c, const int32_t* in, uint32_t n, int32_t* out, uint8_t* status,
                              uint32_t* rounds) {
   return api([&] {
     check_loaded(c);
     if (n == 0) return PCCP_OK;
     if (!in || !out || !status) throw ArgError("null buffer");
-    const size_t nw = c->low.L.n_words;
+    const size_t rw = c->low.L.n_words, nw = c->dl.L.n_words;  // reference / device words
     c->io.ensure((size_t)n * std::max<size_t>(nw, 1));
     c->st.ensure(n);
     c->rnd.ensure(n);
-    if (nw) CK(cudaMemcpyAsync(c->io.p, in, (size_t)n * nw * 4, cudaMemcpyHostToDevice, c->stream));
-    const dev::Model M = c->model(0, 0, in, n, nw);
+    std::vector<std::int32_t> dev_in;
+    const std::int32_t* src = in;
+    if (c->dl.L.packed) {
+      dev_in.resize((size_t)n * nw);
+      for (uint32_t i = 0; i < n; ++i) to_device(c->dl, in + (size_t)i * rw, dev_in.data() + (size_t)i * nw);
+      src = dev_in.data();
+    }
+    if (nw) CK(cudaMemcpyAsync(c->io.p, src, (size_t)n * nw * 4, cudaMemcpyHostToDevice, c->stream));
+    const dev::Model M = c->model(0, 0, in, n, rw);
     const int per = c->warp ? c->gpc : 1;
     const int grid = (int)std::min<long long>(c->ctas, ((long long)n + per - 1) / per);
     dispatch(c, [&]<class Gp, bool TS, int F>() {
@@ -937,10 +977,16 @@ int pccp_gpu_propagate_batch(pccp_gpu_ctx* c, const int32_t* in, uint32_t n, int
     });
     CK(cudaGetLastError());
     ++c->launches;
-    if (nw) CK(cudaMemcpyAsync(out, c->io.p, (size_t)n * nw * 4, cudaMemcpyDeviceToHost, c->stream));
+    if (c->dl.L.packed) {
+      CK(cudaMemcpyAsync(dev_in.data(), c->io.p, (size_t)n * nw * 4, cudaMemcpyDeviceToHost, c->stream));
+    } else if (nw) {
+      CK(cudaMemcpyAsync(out, c->io.p, (size_t)n * nw * 4, cudaMemcpyDeviceToHost, c->stream));
+    }
     CK(cudaMemcpyAsync(status, c->st.p, n, cudaMemcpyDeviceToHost, c->stream));
     if (rounds) CK(cudaMemcpyAsync(rounds, c->rnd.p, (size_t)n * 4, cudaMemcpyDeviceToHost, c->stream));
     CK(cudaStreamSynchronize(c->stream));
+    if (c->dl.L.packed)
+      for (uint32_t i = 0; i < n; ++i) to_reference(c->dl, dev_in.data() + (size_t)i * nw, out + (size_t)i * rw);
     return PCCP_OK;
   });
 }
@@ -1094,8 +1140,11 @@ int pccp_gpu_solve(pccp_gpu_ctx* c, const int32_t* root, const pccp_limits* lim,
       out->improvements[k] = log[k].first;
       out->improvement_ms[k] = log[k].second;
     }
-    if (best_words && has && r.g.best_value == r.g.incumbent)
-      CK(cudaMemcpy(best_words, c->best.p, (size_t)c->low.L.n_words * 4, cudaMemcpyDeviceToHost));
+    if (best_words && has && r.g.best_value == r.g.incumbent) {
+      std::vector<std::int32_t> dw(c->dl.L.n_words);
+      CK(cudaMemcpy(dw.data(), c->best.p, dw.size() * 4, cudaMemcpyDeviceToHost));
+      to_reference(c->dl, dw.data(), best_words);
+    }
     else if (best_words && has)
       out->has_objective = 2;  // incumbent found on a peer GPU: its store lives there
     return PCCP_OK;
@@ -1176,12 +1225,18 @@ int pccp_gpu_audit(pccp_gpu_ctx* c, int32_t* pre, int32_t* post, uint8_t* failed
     if (!n_out) throw ArgError("null argument");
     *n_out = 0;
     if (c->cfg.audit_nodes <= 0 || !c->audit.p) return PCCP_OK;
-    const size_t nw = std::max<size_t>(c->low.L.n_words, 1), k = (size_t)c->cfg.audit_nodes, n = c->audit_taken;
+    const size_t nw = std::max<size_t>(c->dl.L.n_words, 1), rw = c->low.L.n_words, k = (size_t)c->cfg.audit_nodes,
+                 n = c->audit_taken;
     if (n && (!pre || !post || !failed)) throw ArgError("null buffer");
     if (n) {
-      CK(cudaMemcpy(pre, c->audit.p, n * nw * 4, cudaMemcpyDeviceToHost));
-      CK(cudaMemcpy(post, c->audit.p + k * nw, n * nw * 4, cudaMemcpyDeviceToHost));
+      std::vector<std::int32_t> a(n * nw), b(n * nw);
+      CK(cudaMemcpy(a.data(), c->audit.p, n * nw * 4, cudaMemcpyDeviceToHost));
+      CK(cudaMemcpy(b.data(), c->audit.p + k * nw, n * nw * 4, cudaMemcpyDeviceToHost));
       CK(cudaMemcpy(failed, c->audit.p + 2 * k * nw, n, cudaMemcpyDeviceToHost));
+      for (size_t i = 0; i < n; ++i) {
+        to_reference(c->dl, a.data() + i * nw, pre + i * rw);
+        to_reference(c->dl, b.data() + i * nw, post + i * rw);
+      }
     }
     *n_out = (uint32_t)n;
     return PCCP_OK;

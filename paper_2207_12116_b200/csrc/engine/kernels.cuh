@@ -433,13 +433,10 @@ __device__ __forceinline__ bool ne_round(const G& g, unsigned sb, const Tab<TS>&
 // Fast: the host's value-range analysis (fast_paths) proved every x/y value
 // read stays inside (-2^30, 2^30), so the 32-bit branch is taken unchecked.
 template <bool Fast>
-__device__ __forceinline__ bool eval_reif(unsigned sb, int4 r) {
-  const unsigned ax = sb + (((unsigned)r.x & 0xffffu) << 2), ay = sb + (((unsigned)r.x >> 16) << 2);
-  const unsigned ab = sb + ((unsigned)r.y << 2);
-  const int lx = sld(ax), ux = sld(ax + 4), ly = sld(ay), uy = sld(ay + 4), lb = sld(ab), ub = sld(ab + 4);
-  const int p = r.z, q = r.w;
+__device__ __forceinline__ void reif_core(int lx, int ux, int ly, int uy, int lb, int ub, int p, int q, int& nlb,
+                                          int& nub, int& nux, int& nly, int& nuy, int& nlx) {
   const bool bt = lb > 0, bf = ub <= 0;  // [lb b > 0], [ub b <= 0]
-  int nlb = INT_MIN, nub = INT_MAX, nux = INT_MAX, nly = INT_MIN, nuy = INT_MAX, nlx = INT_MIN;
+  nlb = INT_MIN, nub = INT_MAX, nux = INT_MAX, nly = INT_MIN, nuy = INT_MAX, nlx = INT_MIN;
   if (Fast || (small30(lx) & small30(ux) & small30(ly) & small30(uy))) {
     const bool eA = ux - ly <= -p, eB = uy - lx <= -q;  // entailment of x + p <= y, y + q <= x
     const bool nA = lx - uy > -p, nB = ly - ux > -q;    // entailment of their negations
@@ -486,6 +483,15 @@ __device__ __forceinline__ bool eval_reif(unsigned sb, int4 r) {
       nlx = max(nlx, narrow(wly + 1 - p));
     }
   }
+}
+
+template <bool Fast>
+__device__ __forceinline__ bool eval_reif(unsigned sb, int4 r) {
+  const unsigned ax = sb + (((unsigned)r.x & 0xffffu) << 2), ay = sb + (((unsigned)r.x >> 16) << 2);
+  const unsigned ab = sb + ((unsigned)r.y << 2);
+  const int lx = sld(ax), ux = sld(ax + 4), ly = sld(ay), uy = sld(ay + 4), lb = sld(ab), ub = sld(ab + 4);
+  int nlb, nub, nux, nly, nuy, nlx;
+  reif_core<Fast>(lx, ux, ly, uy, lb, ub, r.z, r.w, nlb, nub, nux, nly, nuy, nlx);
   // Joins; the snapshot is the pre-check (bounds only move toward top).  As in
   // eval_ne_fast, a candidate that beats its snapshot proves a change this
   // round, so the joins need no return value: all six are issued under one
@@ -494,6 +500,36 @@ __device__ __forceinline__ bool eval_reif(unsigned sb, int4 r) {
   if (c1 | c2 | c3 | c4 | c5 | c6) {
     sred_max(ab, c1 ? nlb : INT_MIN);
     sred_min(ab + 4, c2 ? nub : INT_MAX);
+    sred_min(ax + 4, c3 ? nux : INT_MAX);
+    sred_max(ay, c4 ? nly : INT_MIN);
+    sred_min(ay + 4, c5 ? nuy : INT_MAX);
+    sred_max(ax, c6 ? nlx : INT_MIN);
+    return true;
+  }
+  return false;
+}
+
+__device__ __forceinline__ void sred_or(unsigned a, unsigned v) {
+  asm volatile("red.shared.or.b32 [%0], %1;" ::"r"(a), "r"(v) : "memory");
+}
+
+// eval_reif with b a bit-plane cell (L.packed, lower_packed): r.y is b's bit;
+// sp is the shared address of plane pair 0.  lb b = LB bit, ub b = 1 - UB bit;
+// the joins b <- 1 / b <- 0 set the LB / UB bit (red.or), the only moves a
+// 0/1 cell has (nlb > lb only for nlb = 1, lb = 0; nub < ub only for 0 < 1).
+template <bool Fast>
+__device__ __forceinline__ bool eval_reif_bits(unsigned sb, unsigned sp, int4 r) {
+  const unsigned ax = sb + (((unsigned)r.x & 0xffffu) << 2), ay = sb + (((unsigned)r.x >> 16) << 2);
+  const unsigned bit = (unsigned)r.y, ap = sp + ((bit >> 5) << 3), mk = 1u << (bit & 31u);
+  const int lx = sld(ax), ux = sld(ax + 4), ly = sld(ay), uy = sld(ay + 4);
+  const int2 P = sld2(ap);
+  const int lb = ((unsigned)P.x & mk) ? 1 : 0, ub = ((unsigned)P.y & mk) ? 0 : 1;
+  int nlb, nub, nux, nly, nuy, nlx;
+  reif_core<Fast>(lx, ux, ly, uy, lb, ub, r.z, r.w, nlb, nub, nux, nly, nuy, nlx);
+  const bool c1 = nlb > lb, c2 = nub < ub, c3 = nux < ux, c4 = nly > ly, c5 = nuy < uy, c6 = nlx > lx;
+  if (c1 | c2 | c3 | c4 | c5 | c6) {
+    if (c1) sred_or(ap, mk);
+    if (c2) sred_or(ap + 4, mk);
     sred_min(ax + 4, c3 ? nux : INT_MAX);
     sred_max(ay, c4 ? nly : INT_MIN);
     sred_min(ay + 4, c5 ? nuy : INT_MAX);
@@ -711,6 +747,71 @@ __device__ bool eval_rows(const G& g, unsigned sb, const Tab<TS>& tab, const Dev
   return ch;
 }
 
+// Sum rows over bit-plane cells (L.packed): the row of eval_rows_fast with
+// each term's lb read as its LB bit (lb in {0, 1}) and the zeroing join
+// b <- (0, 0) as setting its UB bit (lb >= 0 already holds).  A term's pair
+// (LB, UB) is one 8-byte load; the terms of a row are consecutive bits
+// (lower_packed orders them so), so a sub-warp's loads hit a few words.
+// Sums are exact in 32 bits: lower_packed bounds sum |coef| by 2^29.
+template <class G, bool TS>
+__device__ bool eval_brows(const G& g, unsigned sb, const Tab<TS>& tab, const DeviceLayout& L) {
+  const int R = (int)L.brow_lanes;
+  const int sub = g.rank() & (R - 1);
+  const int per_pass = g.size() / R;
+  const int my = g.rank() / R;
+  const int n_rows = (int)L.n_brows;
+  const unsigned sp = sb + 4u * L.plane;
+  unsigned ch = 0;
+  for (int base = 0; base < n_rows; base += per_pass) {
+    const int row = base + my;
+    const bool act = row < n_rows;
+    const int4 meta = act ? tab.ld4(L.brow_meta, row) : make_int4(0, 0, INT_MAX, 0);  // {beg, end, c, lsum}
+    const int b0 = act ? tab.ld1(L.brow_base, row) : 0;
+    const int j0 = meta.x + sub, end = meta.y, c = meta.z;
+    const unsigned alsum = sb + ((unsigned)meta.w << 2);
+    const int n_my = end > j0 ? (end - j0 + R - 1) / R : 0;
+    int x[kRowTerms];
+    unsigned v = 0, z = 0;  // this lane's terms: LB bits, UB bits
+#pragma unroll
+    for (int t = 0; t < kRowTerms; ++t) x[t] = t < n_my ? tab.ld1(L.bpat, j0 + t * R) : 0;
+    const int lsum_now = act && sub == 0 ? sld(alsum) : INT_MAX;
+    int s = 0;
+#pragma unroll
+    for (int t = 0; t < kRowTerms; ++t) {
+      if (t < n_my) {
+        const unsigned bit = (unsigned)(b0 + tword(x[t]));
+        const int2 P = sld2(sp + ((bit >> 5) << 3));
+        const unsigned lbb = ((unsigned)P.x >> (bit & 31u)) & 1u, ubb = ((unsigned)P.y >> (bit & 31u)) & 1u;
+        v |= lbb << t;
+        z |= ubb << t;
+        s += tcoef(x[t]) * (int)lbb;
+      }
+    }
+    for (int o = R >> 1; o > 0; o >>= 1) s += __shfl_xor_sync(kFull, s, o, R);
+    if (act) {
+      const bool over = s > c;
+      const int cell = over ? INT_MAX : s;  // [lsum > c] => lsum <- +inf
+      if (sub == 0 && cell > lsum_now) {
+        sred_max(alsum, cell);
+        ch = 1u;
+      }
+      if (c != INT_MAX) {
+#pragma unroll
+        for (int t = 0; t < kRowTerms; ++t) {
+          const int coef = tcoef(x[t]);
+          const int vb = (int)((v >> t) & 1u);
+          if (t < n_my && !((z >> t) & 1u) && (over || coef + s - coef * vb > c)) {
+            const unsigned bit = (unsigned)(b0 + tword(x[t]));
+            sred_or(sp + ((bit >> 5) << 3) + 4u, 1u << (bit & 31u));
+            ch = 1u;
+          }
+        }
+      }
+    }
+  }
+  return ch != 0;
+}
+
 // Unguarded constant tells, joined once at node entry.
 template <class G>
 __device__ __forceinline__ void apply_fold(const G& g, volatile int* S, const int* __restrict__ T,
@@ -815,7 +916,14 @@ __device__ __forceinline__ bool eval_other_families(const G& g, volatile int* S,
                                                     const DeviceLayout& L) {
     const int* __restrict__ T = tab.p;
     bool ch = false;
-    if (L.reif_fast) {
+    if (L.packed) {
+      const unsigned sp = sb + 4u * L.plane;
+      if (L.reif_fast) {
+        for (int i = g.rank(); i < (int)L.n_reif; i += g.size()) ch |= eval_reif_bits<true>(sb, sp, tab.ld4(L.reif, i));
+      } else {
+        for (int i = g.rank(); i < (int)L.n_reif; i += g.size()) ch |= eval_reif_bits<false>(sb, sp, tab.ld4(L.reif, i));
+      }
+    } else if (L.reif_fast) {
       for (int i = g.rank(); i < (int)L.n_reif; i += g.size()) ch |= eval_reif<true>(sb, tab.ld4(L.reif, i));
     } else {
       for (int i = g.rank(); i < (int)L.n_reif; i += g.size()) ch |= eval_reif<false>(sb, tab.ld4(L.reif, i));
@@ -845,6 +953,7 @@ __device__ __forceinline__ bool eval_other_families(const G& g, volatile int* S,
     for (int i = g.rank(); i < (int)L.n_small; i += g.size()) ch |= eval_small(S, T, L, i);
     dbg_r(2);
     if (L.n_rows) ch |= eval_rows(g, sb, tab, L);
+    if (L.n_brows) ch |= eval_brows(g, sb, tab, L);
     dbg_r(3);
     for (int i = g.rank(); i < (int)L.n_gen; i += g.size())
       ch |= eval_generic(S, T + L.gen_code + T[L.gen_off + i]);
@@ -889,6 +998,11 @@ __device__ bool propagate(const G& g, volatile int* S, unsigned sb, const Tab<TS
       if (F == kAllFamilies && !L.iv_dense)
         for (int i = g.rank(); i < (int)L.n_sc; i += g.size())
           fl |= sld(sb + 4u * (unsigned)tab.ld1(L.sc_w, i)) == tab.ld1(L.sc_top, i);
+      if (F == kAllFamilies && L.packed)  // bit cells: empty = both bits
+        for (int i = g.rank(); i < (int)L.n_pairs; i += g.size()) {
+          const int2 P = sld2(sb + 4u * (L.plane + 2u * (unsigned)i));
+          fl |= (P.x & P.y) != 0;
+        }
     } else {
       for (int i = g.rank(); i < (int)L.n_iv; i += g.size()) {
         const unsigned a = sb + 4u * (unsigned)tab.ld1(L.iv_lb, i);
@@ -896,6 +1010,11 @@ __device__ bool propagate(const G& g, volatile int* S, unsigned sb, const Tab<TS
       }
       for (int i = g.rank(); i < (int)L.n_sc; i += g.size())
         fl |= sld(sb + 4u * (unsigned)tab.ld1(L.sc_w, i)) == tab.ld1(L.sc_top, i);
+      if (F == kAllFamilies && L.packed)
+        for (int i = g.rank(); i < (int)L.n_pairs; i += g.size()) {
+          const int2 P = sld2(sb + 4u * (L.plane + 2u * (unsigned)i));
+          fl |= (P.x & P.y) != 0;
+        }
     }
     dbg_r(4);
     bool any_ch, any_fl;
@@ -979,6 +1098,31 @@ __device__ __forceinline__ unsigned long long store_hash(volatile int* S, int n)
   unsigned long long h = 1469598103934665603ull;
   for (int w = 0; w < n; ++w) {
     const unsigned v = (unsigned)S[w];
+#pragma unroll
+    for (int b = 0; b < 4; ++b) {
+      h ^= (v >> (8 * b)) & 0xffu;
+      h *= 1099511628211ull;
+    }
+  }
+  return h;
+}
+
+// The hash over the reference layout: a packed store decodes its bit cells
+// (lower.hpp L.dec) back to the reference's (lb, ub) words on the fly.
+__device__ __forceinline__ unsigned long long store_hash_ref(volatile int* S, const int* __restrict__ T,
+                                                             const DeviceLayout& L) {
+  if (!L.packed) return store_hash(S, (int)L.n_words);
+  unsigned long long h = 1469598103934665603ull;
+  for (unsigned w = 0; w < L.ref_words; ++w) {
+    const int e = T[L.dec + w];
+    unsigned v;
+    if (e >= 0) {
+      v = (unsigned)S[e];
+    } else {
+      const unsigned code = (unsigned)(-1 - e), b = code >> 1;
+      const unsigned set = ((unsigned)S[L.plane + 2u * (b >> 5) + (code & 1u)] >> (b & 31u)) & 1u;
+      v = (code & 1u) ? 1u - set : set;  // UB bit: ub = 0; LB bit: lb = 1
+    }
 #pragma unroll
     for (int b = 0; b < 4; ++b) {
       h ^= (v >> (8 * b)) & 0xffu;

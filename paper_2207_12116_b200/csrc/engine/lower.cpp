@@ -2,6 +2,7 @@
 #include "lower.hpp"
 
 #include <algorithm>
+#include <functional>
 #include <map>
 #include <cstdlib>
 #include <optional>
@@ -128,7 +129,16 @@ std::uint32_t align4(std::uint32_t x) { return (x + 3u) & ~3u; }
 
 }  // namespace
 
-Lowered lower_model(const pccp_model& m) {
+namespace {
+Lowered lower_impl(const pccp_model& m, bool want_bits);
+}
+
+Lowered lower_model(const pccp_model& m) { return lower_impl(m, false); }
+Lowered lower_packed(const pccp_model& m) { return lower_impl(m, true); }
+
+namespace {
+
+Lowered lower_impl(const pccp_model& m, bool want_bits) {
   if (m.n_slots && (!m.slot_kind || !m.slot_word)) bad("null slot tables");
   if (m.n_cmds && (!m.cmd_off || !m.cmd_code)) bad("null command tables");
   Lowered out;
@@ -565,6 +575,241 @@ Lowered lower_model(const pccp_model& m) {
   // Group shapes so a warp walks a homogeneous segment (fewer divergent paths).
   std::stable_sort(smalls.begin(), smalls.end(), [](const Small& a, const Small& b) { return a.shape < b.shape; });
 
+  // ---- bit-plane 0/1 cells (lower_packed, lower.hpp) -----------------------------
+  const std::uint32_t NW = m.n_words;
+  std::vector<std::int32_t> bitof(NW, -1);  // lb word of a packed slot -> its bit
+  std::vector<std::uint8_t> brow(rows.size(), 0);  // rows over packed cells only
+  std::uint32_t n_bits = 0;
+  std::vector<std::int32_t> flb(NW, INT32_MIN), fub(NW, INT32_MAX);  // folded constants per word
+  bool packed = false;
+  if (want_bits && !std::getenv("PCCP_NO_PACK")) {
+    std::vector<std::uint8_t> other(NW, 0), fold_bad(NW, 0);
+    auto touch = [&](std::uint32_t w) {
+      if (w < NW) other[w] = 1;
+    };
+    auto touch_iv = [&](std::uint32_t w) {
+      touch(w);
+      touch(w + 1);
+    };
+    for (const NE& e : nes) {
+      touch_iv(static_cast<std::uint32_t>(e.x) & 0xffffu);
+      touch_iv(static_cast<std::uint32_t>(e.x) >> 16);
+    }
+    for (const Reif& r : reifs) {
+      touch_iv(static_cast<std::uint32_t>(r.xy) & 0xffffu);
+      touch_iv(static_cast<std::uint32_t>(r.xy) >> 16);
+    }
+    auto touch_unit = [&](const U1& r) {
+      const std::uint32_t x = static_cast<std::uint32_t>(r.x), w = static_cast<std::uint32_t>(r.w);
+      touch(x & 0xffffu);
+      touch(x >> 16);
+      touch(w & 0x7fffu);
+      touch((w >> 15) & 0x7fffu);
+    };
+    for (const U1& r : unit1) touch_unit(r);
+    for (const auto& r : unit2) {
+      touch_unit(r.first);
+      touch(static_cast<std::uint32_t>(r.second.first) & 0xffffu);
+      touch(static_cast<std::uint32_t>(r.second.first) >> 16);
+    }
+    auto tw_of = [](std::int32_t t) { return static_cast<std::uint32_t>(t) & kTermWordMask; };
+    for (const Small& s : smalls) {
+      for (int k = 0; k < 4; ++k)
+        if (s.g[k]) touch(tw_of(s.g[k]));
+      if (s.lbt) touch(tw_of(s.lbt));
+      if (s.ubt) touch(tw_of(s.ubt));
+      touch_iv(static_cast<std::uint32_t>(s.tw));
+    }
+    for (std::uint32_t gi : generic) {
+      const CmdP& c = cmds[gi];
+      touch(c.tw);
+      if (c.kind == PCCP_INTERVAL) touch(c.tw + 1);
+      for (const GuardP& g : c.guards)
+        for (auto& t : g.lhs.terms) touch(t.second);
+      for (const auto* e : {&c.sc, &c.lb, &c.ub})
+        if (*e)
+          for (auto& t : (*e)->terms) touch(t.second);
+    }
+    for (const Row& r : rows) touch(r.lsum);
+    if (m.n_cands == 0) {  // every interval slot is a candidate: nothing packs
+      std::fill(other.begin(), other.end(), 1);
+    } else if (m.cands) {
+      for (std::uint32_t i = 0; i < m.n_cands; ++i) {
+        const std::int32_t s = m.cands[i];
+        if (s >= 0 && static_cast<std::uint32_t>(s) < m.n_slots) touch_iv(m.slot_word[s]);
+      }
+    }
+    if (m.obj_slot >= 0 && static_cast<std::uint32_t>(m.obj_slot) < m.n_slots) touch_iv(m.slot_word[m.obj_slot]);
+    for (std::size_t i = 0; i < fold_w.size(); ++i) {
+      const std::uint32_t w = static_cast<std::uint32_t>(fold_w[i]) & 0x7fffffffu;
+      const std::int32_t v = fold_v[i];
+      if (w >= NW) continue;
+      if (v != 0 && v != 1) fold_bad[w] = 1;
+      if (fold_w[i] < 0) {
+        if (is_lb[w]) flb[w] = std::max(flb[w], v);
+        else other[w] = 1;  // an up scalar
+      } else if (w > 0 && is_lb[w - 1]) {
+        fub[w] = std::min(fub[w], v);
+      } else {
+        other[w] = 1;
+      }
+    }
+    std::vector<std::uint8_t> pk(NW, 0);  // lb words of packable slots
+    for (std::uint32_t s = 0; s < m.n_slots; ++s) {
+      if (m.slot_kind[s] != PCCP_INTERVAL) continue;
+      const std::uint32_t w = m.slot_word[s];
+      pk[w] = !other[w] && !other[w + 1] && !fold_bad[w] && !fold_bad[w + 1] && flb[w] != INT32_MIN &&
+              fub[w + 1] != INT32_MAX;
+    }
+    // A row sums packed bits only if every term is packed (else it stays a
+    // word row and its terms stay words); its bit sum must fit 2^29.
+    for (bool ch = true; ch;) {
+      ch = false;
+      for (const Row& r : rows) {
+        std::size_t cnt = 0;
+        std::int64_t sum = 0;
+        for (std::int32_t x : r.terms) {
+          cnt += pk[tw_of(x)] ? 1 : 0;
+          sum += std::abs(std::int64_t{x >> kTermWordBits});
+        }
+        if (cnt && (cnt < r.terms.size() || sum >= (1 << 29) || r.c <= -(1 << 30) || (r.c >= (1 << 30) && r.c != INT32_MAX))) {
+          for (std::int32_t x : r.terms)
+            if (pk[tw_of(x)]) {
+              pk[tw_of(x)] = 0;
+              ch = true;
+            }
+        }
+      }
+    }
+    bool all_reif = true;
+    for (const Reif& r : reifs) all_reif &= pk[static_cast<std::uint32_t>(r.b)] != 0;
+    std::size_t n_pk = 0;
+    for (std::uint32_t w = 0; w < NW; ++w) n_pk += pk[w];
+    packed = all_reif && n_pk > 0 && n_pk < (1u << 20);
+    if (packed) {
+      // Bit order: cells summed by the same rows are neighbours (union-find
+      // over each row's terms; RCPSP: one column b_{., j} per component), so a
+      // row reads a few consecutive plane words.  Components in order of first
+      // appearance in the rows, cells by reference word inside a component.
+      std::vector<std::int32_t> par(NW, -1);
+      std::function<std::int32_t(std::int32_t)> find = [&](std::int32_t w) {
+        while (par[w] != w) w = par[w] = par[par[w]];
+        return w;
+      };
+      for (std::uint32_t w = 0; w < NW; ++w)
+        if (pk[w]) par[w] = static_cast<std::int32_t>(w);
+      for (std::size_t r = 0; r < rows.size(); ++r) {
+        if (rows[r].terms.empty() || !pk[tw_of(rows[r].terms[0])]) continue;
+        brow[r] = 1;
+        const std::int32_t a = find(static_cast<std::int32_t>(tw_of(rows[r].terms[0])));
+        for (std::int32_t x : rows[r].terms) {
+          const std::int32_t b = find(static_cast<std::int32_t>(tw_of(x)));
+          if (a != b) par[b] = a;
+        }
+      }
+      std::vector<std::int64_t> rank(NW, -1);
+      std::int64_t next = 0;
+      for (std::size_t r = 0; r < rows.size(); ++r)
+        if (brow[r])
+          for (std::int32_t x : rows[r].terms) {
+            const std::int32_t c = find(static_cast<std::int32_t>(tw_of(x)));
+            if (rank[c] < 0) rank[c] = next++;
+          }
+      std::vector<std::uint32_t> order;
+      for (std::uint32_t w = 0; w < NW; ++w)
+        if (pk[w]) {
+          const std::int32_t c = find(static_cast<std::int32_t>(w));
+          if (rank[c] < 0) rank[c] = next++;
+          order.push_back(w);
+        }
+      std::stable_sort(order.begin(), order.end(), [&](std::uint32_t a, std::uint32_t b) {
+        return rank[find(static_cast<std::int32_t>(a))] < rank[find(static_cast<std::int32_t>(b))];
+      });
+      for (std::uint32_t w : order) bitof[w] = static_cast<std::int32_t>(n_bits++);
+    }
+  }
+  // Reference word -> device word (packed cells: -1), and the device zero word.
+  std::vector<std::int32_t> dmap(NW, -1);
+  std::uint32_t n_int = 0;
+  for (std::uint32_t w = 0; w < NW; ++w) {
+    const bool in_bits = bitof[w] >= 0 || (w > 0 && bitof[w - 1] >= 0 && is_lb[w - 1]);
+    if (!in_bits) dmap[w] = static_cast<std::int32_t>(n_int++);
+  }
+  const std::uint32_t n_pairs = (n_bits + 31) / 32;
+  const std::uint32_t plane = packed ? (n_int + 1) & ~1u : n_int;
+  const std::uint32_t DW = packed ? plane + 2 * n_pairs : NW;  // device store words
+  out.dev_words = DW;
+  auto W = [&](std::uint32_t w) -> std::uint32_t {  // device word of a reference word (Z -> the device Z)
+    if (w >= NW) return DW;
+    if (dmap[w] < 0) bad("internal: a packed cell read as a word");
+    return static_cast<std::uint32_t>(dmap[w]);
+  };
+  auto WT = [&](std::int32_t t) -> std::int32_t {  // a packed term (coef << 20 | word), 0 = none
+    if (!t) return 0;
+    return static_cast<std::int32_t>((static_cast<std::uint32_t>(t) & ~kTermWordMask) |
+                                     W(static_cast<std::uint32_t>(t) & kTermWordMask));
+  };
+  if (packed) {
+    L.packed = 1;
+    L.plane = plane;
+    L.n_pairs = n_pairs;
+    L.ref_words = NW;
+    L.n_words = DW;
+    L.zero_word = DW;
+    for (NE& e : nes) e.x = static_cast<std::int32_t>(W(e.x & 0xffff) | (W(static_cast<std::uint32_t>(e.x) >> 16) << 16));
+    for (Reif& r : reifs) {
+      r.xy = static_cast<std::int32_t>(W(r.xy & 0xffff) | (W(static_cast<std::uint32_t>(r.xy) >> 16) << 16));
+      r.b = bitof[static_cast<std::uint32_t>(r.b)];
+    }
+    auto unit_map = [&](U1& r) {
+      const std::uint32_t x = static_cast<std::uint32_t>(r.x), w = static_cast<std::uint32_t>(r.w);
+      r.x = static_cast<std::int32_t>(W(x & 0xffffu) | (W(x >> 16) << 16));
+      r.w = static_cast<std::int32_t>((w & 0xc0000000u) | W(w & 0x7fffu) | (W((w >> 15) & 0x7fffu) << 15));
+    };
+    for (U1& r : unit1) unit_map(r);
+    for (auto& r : unit2) {
+      unit_map(r.first);
+      const std::uint32_t g2 = static_cast<std::uint32_t>(r.second.first);
+      r.second.first = static_cast<std::int32_t>(W(g2 & 0xffffu) | (W(g2 >> 16) << 16));
+    }
+    for (Small& s : smalls) {
+      for (int k = 0; k < 4; ++k) s.g[k] = WT(s.g[k]);
+      s.lbt = WT(s.lbt);
+      s.ubt = WT(s.ubt);
+      s.tw = static_cast<std::int32_t>(W(static_cast<std::uint32_t>(s.tw)));
+    }
+    for (std::size_t r = 0; r < rows.size(); ++r) {
+      rows[r].lsum = W(rows[r].lsum);
+      if (!brow[r])
+        for (std::int32_t& x : rows[r].terms) x = WT(x);
+    }
+    // device folds: word cells only (the packed cells' folds are applied by to_device)
+    std::vector<std::int32_t> fw2, fv2;
+    for (std::size_t i = 0; i < fold_w.size(); ++i) {
+      const std::uint32_t w = static_cast<std::uint32_t>(fold_w[i]) & 0x7fffffffu;
+      if (w < NW && dmap[w] < 0) continue;
+      fw2.push_back(static_cast<std::int32_t>((static_cast<std::uint32_t>(fold_w[i]) & 0x80000000u) | W(w)));
+      fv2.push_back(fold_v[i]);
+    }
+    fold_w.swap(fw2);
+    fold_v.swap(fv2);
+    out.bit_lbw.assign(n_bits, 0);
+    out.bit_fold_lb.assign(n_bits, 0);
+    out.bit_fold_ub.assign(n_bits, 1);
+    for (std::uint32_t w = 0; w < NW; ++w)
+      if (bitof[w] >= 0) {
+        out.bit_lbw[static_cast<std::uint32_t>(bitof[w])] = static_cast<std::int32_t>(w);
+        out.bit_fold_lb[static_cast<std::uint32_t>(bitof[w])] = flb[w];
+        out.bit_fold_ub[static_cast<std::uint32_t>(bitof[w])] = fub[w + 1];
+      }
+    out.dec.assign(NW, 0);
+    for (std::uint32_t w = 0; w < NW; ++w) {
+      if (dmap[w] >= 0) out.dec[w] = dmap[w];
+      else if (bitof[w] >= 0) out.dec[w] = -1 - 2 * bitof[w];
+      else out.dec[w] = -1 - (2 * bitof[w - 1] + 1);
+    }
+  }
+
   // ---- blob ----------------------------------------------------------------------
   std::vector<std::int32_t>& B = out.blob;
   auto reserve_arr = [&B](std::uint32_t n) {
@@ -616,7 +861,10 @@ Lowered lower_model(const pccp_model& m) {
   // consecutive y / b words (2-way bank conflicts).  RCPSP compiles them
   // j-major (rcpsp.cpp:241-242), which puts b_ij of a warp n words apart —
   // the same bank for every lane when n = 32.
-  std::stable_sort(reifs.begin(), reifs.end(), [](const Reif& a, const Reif& b) {
+  // Packed: by bit instead (y-major, RCPSP's compile order): a warp's b
+  // cells then share one plane pair (a broadcast) and x varies by word.
+  std::stable_sort(reifs.begin(), reifs.end(), [packed](const Reif& a, const Reif& b) {
+    if (packed) return a.b < b.b;
     const std::uint32_t ax = static_cast<std::uint32_t>(a.xy) & 0xffffu, bx = static_cast<std::uint32_t>(b.xy) & 0xffffu;
     if (ax != bx) return ax < bx;
     return (static_cast<std::uint32_t>(a.xy) >> 16) < (static_cast<std::uint32_t>(b.xy) >> 16);
@@ -652,7 +900,7 @@ Lowered lower_model(const pccp_model& m) {
   }
   // Per-word reader lists for the filtered rounds (opt-in, PCCP_FILTERED=1:
   // with fused NE records the eventless loop needs ~30% fewer rounds and wins).
-  L.filtered = (m.n_words <= 64 && smalls.empty() && rows.empty() && generic.empty() && reifs.empty() &&
+  L.filtered = (!packed && m.n_words <= 64 && smalls.empty() && rows.empty() && generic.empty() && reifs.empty() &&
                 std::getenv("PCCP_FILTERED") != nullptr)
                    ? 1u
                    : 0u;
@@ -689,14 +937,16 @@ Lowered lower_model(const pccp_model& m) {
     }
     std::uint32_t total = 0;
     for (const auto& r : readers) total += static_cast<std::uint32_t>(r.size());
-    L.wl_off = reserve_arr(m.n_words + 1);
+    L.wl_off = reserve_arr(L.filtered ? m.n_words + 1 : 1);
     L.wl = reserve_arr(total);
     std::uint32_t p = 0;
-    for (std::uint32_t w = 0; w < m.n_words; ++w) {
-      B[L.wl_off + w] = static_cast<std::int32_t>(p);
-      for (std::int32_t e : readers[w]) B[L.wl + p++] = e;
+    if (L.filtered) {
+      for (std::uint32_t w = 0; w < m.n_words; ++w) {
+        B[L.wl_off + w] = static_cast<std::int32_t>(p);
+        for (std::int32_t e : readers[w]) B[L.wl + p++] = e;
+      }
+      B[L.wl_off + m.n_words] = static_cast<std::int32_t>(p);
     }
-    B[L.wl_off + m.n_words] = static_cast<std::int32_t>(p);
   }
   const std::uint32_t ns = static_cast<std::uint32_t>(smalls.size());
   L.n_small = ns;
@@ -716,6 +966,12 @@ Lowered lower_model(const pccp_model& m) {
     B[L.small_ubk + i] = s.ubk;
     B[L.small_ubt + i] = s.ubt;
     B[L.small_tw + i] = s.tw;
+  }
+  std::vector<Row> bit_rows;  // packed: rows over bit cells
+  if (packed) {
+    std::vector<Row> word_rows;
+    for (std::size_t r = 0; r < rows.size(); ++r) (brow[r] ? bit_rows : word_rows).push_back(std::move(rows[r]));
+    rows.swap(word_rows);
   }
   L.n_rows = static_cast<std::uint32_t>(rows.size());
   std::uint32_t n_terms = 0, max_terms = 0;
@@ -754,7 +1010,7 @@ Lowered lower_model(const pccp_model& m) {
     for (std::size_t r = 0; r < rows.size(); ++r) {
       const auto& ts = rows[r].terms;
       for (std::size_t k = 0; k < ts.size(); ++k) {
-        if ((tw(ts[k]) & 1u) || tw(ts[k]) + 1 >= m.n_words) L.row_even = 0;
+        if ((tw(ts[k]) & 1u) || tw(ts[k]) + 1 >= DW) L.row_even = 0;
         if (k + 1 < ts.size() && tw(ts[k + 1]) == tw(ts[k]) + 2) ++contig;
         if (r + 1 < rows.size() && rows[r + 1].terms.size() == ts.size() && tw(rows[r + 1].terms[k]) == tw(ts[k]) + 2)
           ++contig;
@@ -771,68 +1027,112 @@ Lowered lower_model(const pccp_model& m) {
       B[L.row_meta + 4 * r + 3] = static_cast<std::int32_t>(rows[r].lsum);
     }
   }
-  // Rows whose terms all read class <= 1 words can be summed in 32 bits once
-  // the entry values are known to be small (fast_paths).
+  // Bit rows: each row's terms as offsets from its first bit; rows with the
+  // same (coef, offset) list share one pattern (RCPSP: one per resource).
   {
-    bool ok = L.n_rows > 0;
-    for (const Row& r : rows) {
-      std::int64_t s0 = 0, s1 = 0;
-      for (std::int32_t x : r.terms) {
-        const std::uint32_t w = static_cast<std::uint32_t>(x) & kTermWordMask;
-        const std::int64_t coef = std::abs(std::int64_t{x >> kTermWordBits});
-        if (w >= m.n_words || cls[w] == 2) {
-          ok = false;
-          continue;
+    std::map<std::vector<std::int32_t>, std::pair<std::uint32_t, std::uint32_t>> pat_of;
+    std::vector<std::int32_t> pat_terms, base(bit_rows.size());
+    std::vector<std::pair<std::uint32_t, std::uint32_t>> range(bit_rows.size());
+    std::uint32_t max_pt = 0;
+    for (std::size_t r = 0; r < bit_rows.size(); ++r) {
+      std::int32_t b0 = INT32_MAX;
+      for (std::int32_t x : bit_rows[r].terms)
+        b0 = std::min(b0, bitof[static_cast<std::uint32_t>(x) & kTermWordMask]);
+      std::vector<std::int32_t> pt;
+      for (std::int32_t x : bit_rows[r].terms)
+        pt.push_back(pack(x >> kTermWordBits,
+                          static_cast<std::uint32_t>(bitof[static_cast<std::uint32_t>(x) & kTermWordMask] - b0)));
+      auto it = pat_of.find(pt);
+      if (it == pat_of.end()) {
+        const std::uint32_t beg = static_cast<std::uint32_t>(pat_terms.size());
+        pat_terms.insert(pat_terms.end(), pt.begin(), pt.end());
+        it = pat_of.emplace(pt, std::make_pair(beg, static_cast<std::uint32_t>(pat_terms.size()))).first;
+      }
+      base[r] = b0;
+      range[r] = it->second;
+      max_pt = std::max<std::uint32_t>(max_pt, static_cast<std::uint32_t>(pt.size()));
+    }
+    L.n_brows = static_cast<std::uint32_t>(bit_rows.size());
+    L.brow_lanes = 1;
+    while (L.brow_lanes < 32 && L.brow_lanes * 8 < max_pt) L.brow_lanes <<= 1;
+    L.brow_meta = reserve_arr(4 * L.n_brows);
+    L.brow_base = reserve_arr(L.n_brows);
+    L.bpat = reserve_arr(static_cast<std::uint32_t>(pat_terms.size()));
+    for (std::uint32_t r = 0; r < L.n_brows; ++r) {
+      B[L.brow_meta + 4 * r + 0] = static_cast<std::int32_t>(range[r].first);
+      B[L.brow_meta + 4 * r + 1] = static_cast<std::int32_t>(range[r].second);
+      B[L.brow_meta + 4 * r + 2] = bit_rows[r].c;
+      B[L.brow_meta + 4 * r + 3] = static_cast<std::int32_t>(bit_rows[r].lsum);
+      B[L.brow_base + r] = base[r];
+    }
+    std::copy(pat_terms.begin(), pat_terms.end(), B.begin() + L.bpat);
+  }
+  // Value-range analysis over the reference words (plain layouts only: a
+  // packed layout takes the plain lowering's per-launch flags, engine.cu).
+  if (!packed) {
+    // Rows whose terms all read class <= 1 words can be summed in 32 bits once
+    // the entry values are known to be small (fast_paths).
+    {
+      bool ok = L.n_rows > 0;
+      for (const Row& r : rows) {
+        std::int64_t s0 = 0, s1 = 0;
+        for (std::int32_t x : r.terms) {
+          const std::uint32_t w = static_cast<std::uint32_t>(x) & kTermWordMask;
+          const std::int64_t coef = std::abs(std::int64_t{x >> kTermWordBits});
+          if (w >= m.n_words || cls[w] == 2) {
+            ok = false;
+            continue;
+          }
+          read_fast[w] = 1;
+          (cls[w] == 0 ? s0 : s1) += coef;
         }
+        out.row_sum0.push_back(s0);
+        out.row_sum1.push_back(s1);
+      }
+      out.rows_ok = ok;
+    }
+    out.ne_ok = L.n_ne > 0 && L.ne_even;
+    for (std::uint32_t i = 0; i < L.n_ne && out.ne_ok; ++i) {
+      for (std::uint32_t o : {0u, 3u}) {
+        const std::uint32_t lbw = static_cast<std::uint32_t>(B[L.ne + 4 * i + o]) / 4;
+        if (cls[lbw] == 2 || cls[lbw + 1] == 2) out.ne_ok = false;
+        read_fast[lbw] = read_fast[lbw + 1] = 1;
+      }
+    }
+    // unit records: guard words a, b (and the second guard's), tell source f
+    out.unit_ok = L.n_unit1 + L.n_unit2 > 0;
+    {
+      auto ok_word = [&](std::uint32_t w) {  // the constant-zero word Z = n_words is always fine
+        if (w == m.n_words) return true;
+        if (w > m.n_words || cls[w] == 2) return false;
         read_fast[w] = 1;
-        (cls[w] == 0 ? s0 : s1) += coef;
+        return true;
+      };
+      auto scan = [&](std::uint32_t off, std::uint32_t n) {
+        for (std::uint32_t i = 0; i < n && out.unit_ok; ++i) {
+          const std::uint32_t x = static_cast<std::uint32_t>(B[off + 4 * i]);
+          const std::uint32_t w = static_cast<std::uint32_t>(B[off + 4 * i + 3]);
+          if (!ok_word(x & 0xffffu) || !ok_word(x >> 16) || !ok_word((w >> 15) & 0x7fffu)) out.unit_ok = false;
+          out.unit_k = std::max(out.unit_k, std::abs(std::int64_t{B[off + 4 * i + 2]}));
+        }
+      };
+      scan(L.unit1, L.n_unit1);
+      scan(L.unit2, L.n_unit2);
+      for (std::uint32_t i = 0; i < L.n_unit2 && out.unit_ok; ++i) {
+        const std::uint32_t x = static_cast<std::uint32_t>(B[L.unit2g + 2 * i]);
+        if (!ok_word(x & 0xffffu) || !ok_word(x >> 16)) out.unit_ok = false;
       }
-      out.row_sum0.push_back(s0);
-      out.row_sum1.push_back(s1);
     }
-    out.rows_ok = ok;
-  }
-  out.ne_ok = L.n_ne > 0 && L.ne_even;
-  for (std::uint32_t i = 0; i < L.n_ne && out.ne_ok; ++i) {
-    for (std::uint32_t o : {0u, 3u}) {
-      const std::uint32_t lbw = static_cast<std::uint32_t>(B[L.ne + 4 * i + o]) / 4;
-      if (cls[lbw] == 2 || cls[lbw + 1] == 2) out.ne_ok = false;
-      read_fast[lbw] = read_fast[lbw + 1] = 1;
-    }
-  }
-  // unit records: guard words a, b (and the second guard's), tell source f
-  out.unit_ok = L.n_unit1 + L.n_unit2 > 0;
-  {
-    auto ok_word = [&](std::uint32_t w) {  // the constant-zero word Z = n_words is always fine
-      if (w == m.n_words) return true;
-      if (w > m.n_words || cls[w] == 2) return false;
-      read_fast[w] = 1;
-      return true;
-    };
-    auto scan = [&](std::uint32_t off, std::uint32_t n) {
-      for (std::uint32_t i = 0; i < n && out.unit_ok; ++i) {
-        const std::uint32_t x = static_cast<std::uint32_t>(B[off + 4 * i]);
-        const std::uint32_t w = static_cast<std::uint32_t>(B[off + 4 * i + 3]);
-        if (!ok_word(x & 0xffffu) || !ok_word(x >> 16) || !ok_word((w >> 15) & 0x7fffu)) out.unit_ok = false;
-        out.unit_k = std::max(out.unit_k, std::abs(std::int64_t{B[off + 4 * i + 2]}));
+    out.reif_ok = L.n_reif > 0;
+    for (std::uint32_t i = 0; i < L.n_reif && out.reif_ok; ++i) {
+      const std::uint32_t xy = static_cast<std::uint32_t>(B[L.reif + 4 * i]);
+      for (std::uint32_t lbw : {xy & 0xffffu, xy >> 16}) {
+        if (lbw + 1 >= m.n_words || cls[lbw] == 2 || cls[lbw + 1] == 2) out.reif_ok = false;
+        else read_fast[lbw] = read_fast[lbw + 1] = 1;
       }
-    };
-    scan(L.unit1, L.n_unit1);
-    scan(L.unit2, L.n_unit2);
-    for (std::uint32_t i = 0; i < L.n_unit2 && out.unit_ok; ++i) {
-      const std::uint32_t x = static_cast<std::uint32_t>(B[L.unit2g + 2 * i]);
-      if (!ok_word(x & 0xffffu) || !ok_word(x >> 16)) out.unit_ok = false;
+      out.reif_k = std::max({out.reif_k, std::abs(std::int64_t{B[L.reif + 4 * i + 2]}),
+                             std::abs(std::int64_t{B[L.reif + 4 * i + 3]})});
     }
-  }
-  out.reif_ok = L.n_reif > 0;
-  for (std::uint32_t i = 0; i < L.n_reif && out.reif_ok; ++i) {
-    const std::uint32_t xy = static_cast<std::uint32_t>(B[L.reif + 4 * i]);
-    for (std::uint32_t lbw : {xy & 0xffffu, xy >> 16}) {
-      if (lbw + 1 >= m.n_words || cls[lbw] == 2 || cls[lbw + 1] == 2) out.reif_ok = false;
-      else read_fast[lbw] = read_fast[lbw + 1] = 1;
-    }
-    out.reif_k = std::max({out.reif_k, std::abs(std::int64_t{B[L.reif + 4 * i + 2]}),
-                           std::abs(std::int64_t{B[L.reif + 4 * i + 3]})});
   }
   L.hot_words = static_cast<std::uint32_t>(B.size());
 
@@ -854,7 +1154,21 @@ Lowered lower_model(const pccp_model& m) {
     for (std::uint32_t k = 0; k < L.n_gen; ++k) {
       const std::uint32_t i = generic[k];
       B[L.gen_off + k] = static_cast<std::int32_t>(p);
+      const std::uint32_t c0 = p;
       for (std::uint32_t x = m.cmd_off[i]; x < m.cmd_off[i + 1]; ++x) B[L.gen_code + p++] = m.cmd_code[x];
+      if (packed) {  // the stream's words in the device layout (parse() checked its shape)
+        std::int32_t* q = &B[L.gen_code + c0];
+        const std::int32_t ng = q[0], mask = q[4];
+        q[3] = static_cast<std::int32_t>(W(static_cast<std::uint32_t>(q[3])));
+        std::int32_t* e = q + 5;
+        auto remap_expr = [&](std::int32_t* x) {  // [k, n, (coef, word) * n]
+          for (std::int32_t t = 0; t < x[1]; ++t) x[3 + 2 * t] = static_cast<std::int32_t>(W(static_cast<std::uint32_t>(x[3 + 2 * t])));
+          return x + 2 + 2 * x[1];
+        };
+        for (std::int32_t g = 0; g < ng; ++g) e = remap_expr(e + 2);  // [rel, rhs, expr]
+        for (std::int32_t f : {PCCP_FN_SCALAR, PCCP_FN_LB, PCCP_FN_UB})
+          if (mask & f) e = remap_expr(e);
+      }
     }
     B[L.gen_off + L.n_gen] = static_cast<std::int32_t>(p);
   }
@@ -863,9 +1177,9 @@ Lowered lower_model(const pccp_model& m) {
   for (std::uint32_t s = 0; s < m.n_slots; ++s) {
     const int k = m.slot_kind[s];
     if (k == PCCP_INTERVAL) {
-      iv.push_back(static_cast<std::int32_t>(m.slot_word[s]));
+      if (dmap[m.slot_word[s]] >= 0) iv.push_back(static_cast<std::int32_t>(W(m.slot_word[s])));  // not a bit cell
     } else {
-      scw.push_back(static_cast<std::int32_t>(m.slot_word[s]));
+      scw.push_back(static_cast<std::int32_t>(W(m.slot_word[s])));
       sct.push_back(k == PCCP_ZINC ? INT32_MAX : k == PCCP_ZDEC ? INT32_MIN : k == PCCP_BINC ? 1 : 0);
     }
   }
@@ -877,7 +1191,7 @@ Lowered lower_model(const pccp_model& m) {
   L.iv_prefix = 1;
   for (std::uint32_t i = 0; i < L.n_iv && L.iv_prefix; ++i)
     if (iv[i] != static_cast<std::int32_t>(2 * i)) L.iv_prefix = 0;
-  L.iv_dense = L.iv_prefix && L.n_iv * 2 == m.n_words ? 1 : 0;
+  L.iv_dense = !packed && L.iv_prefix && L.n_iv * 2 == m.n_words ? 1 : 0;
   L.n_sc = static_cast<std::uint32_t>(scw.size());
   L.sc_w = reserve_arr(L.n_sc);
   L.sc_top = reserve_arr(L.n_sc);
@@ -887,13 +1201,13 @@ Lowered lower_model(const pccp_model& m) {
   std::vector<std::int32_t> cand;
   if (m.n_cands == 0) {
     for (std::uint32_t s = 0; s < m.n_slots; ++s)
-      if (m.slot_kind[s] == PCCP_INTERVAL) cand.push_back(static_cast<std::int32_t>(m.slot_word[s]));
+      if (m.slot_kind[s] == PCCP_INTERVAL) cand.push_back(static_cast<std::int32_t>(W(m.slot_word[s])));
   } else {
     if (!m.cands) bad("null candidate table");
     for (std::uint32_t i = 0; i < m.n_cands; ++i) {
       const std::int32_t s = m.cands[i];
       if (s < 0 || static_cast<std::uint32_t>(s) >= m.n_slots) bad("candidate slot out of range");
-      if (m.slot_kind[s] == PCCP_INTERVAL) cand.push_back(static_cast<std::int32_t>(m.slot_word[s]));
+      if (m.slot_kind[s] == PCCP_INTERVAL) cand.push_back(static_cast<std::int32_t>(W(m.slot_word[s])));
     }
   }
   L.n_cand = static_cast<std::uint32_t>(cand.size());
@@ -903,7 +1217,7 @@ Lowered lower_model(const pccp_model& m) {
   if (m.obj_slot >= 0) {
     if (static_cast<std::uint32_t>(m.obj_slot) >= m.n_slots || m.slot_kind[m.obj_slot] != PCCP_INTERVAL)
       bad("objective must be an interval slot");
-    L.obj_lbw = static_cast<std::int32_t>(m.slot_word[m.obj_slot]);
+    L.obj_lbw = static_cast<std::int32_t>(W(m.slot_word[m.obj_slot]));
   } else {
     L.obj_lbw = -1;
   }
@@ -944,12 +1258,62 @@ Lowered lower_model(const pccp_model& m) {
       tb += 4.0 * (m.cmd_off[g + 1] - m.cmd_off[g]);
     }
     sb += 8.0 * L.n_iv + 4.0 * L.n_sc;  // the failure scan
+    for (const Row& r : bit_rows) sb += 4.0 + 8.0 * r.terms.size();  // lsum + each term's plane pair
+    tb += 20.0 * bit_rows.size();
+    for (std::uint32_t r = 0; r < L.n_brows; ++r) tb += 4.0 * (B[L.brow_meta + 4 * r + 1] - B[L.brow_meta + 4 * r]);
+    sb += 8.0 * L.n_pairs;  // the planes' failure scan
     out.store_bytes_per_round = sb;
     out.table_bytes_per_round = tb;
+  }
+  if (packed) {
+    L.dec = reserve_arr(NW);
+    std::copy(out.dec.begin(), out.dec.end(), B.begin() + L.dec);
   }
   L.blob_words = static_cast<std::uint32_t>(B.size());
   if (B.empty()) B.push_back(0);
   return out;
+}
+
+}  // namespace
+
+void to_device(const Lowered& d, const std::int32_t* ref, std::int32_t* dev) {
+  const DeviceLayout& L = d.L;
+  if (!L.packed) {
+    std::copy(ref, ref + L.n_words, dev);
+    return;
+  }
+  std::fill(dev, dev + L.n_words, 0);  // the pad word and the planes start at 0
+  for (std::uint32_t w = 0; w < L.ref_words; ++w)
+    if (d.dec[w] >= 0) dev[d.dec[w]] = ref[w];
+  for (std::size_t b = 0; b < d.bit_lbw.size(); ++b) {
+    const std::uint32_t w = static_cast<std::uint32_t>(d.bit_lbw[b]);
+    // the folded constants every entry point applies (lower_packed): lb >= 0,
+    // ub <= 1, so lb <= ub leaves (0,0), (0,1) or (1,1); anything else is the
+    // empty interval, kept as both bits (failed)
+    const std::int32_t lb = std::max(ref[w], d.bit_fold_lb[b]), ub = std::min(ref[w + 1], d.bit_fold_ub[b]);
+    const std::uint32_t m = 1u << (b & 31), k = L.plane + 2 * static_cast<std::uint32_t>(b >> 5);
+    if (lb > ub || lb >= 1) dev[k] |= static_cast<std::int32_t>(m);
+    if (lb > ub || ub <= 0) dev[k + 1] |= static_cast<std::int32_t>(m);
+  }
+}
+
+void to_reference(const Lowered& d, const std::int32_t* dev, std::int32_t* ref) {
+  const DeviceLayout& L = d.L;
+  if (!L.packed) {
+    std::copy(dev, dev + L.n_words, ref);
+    return;
+  }
+  for (std::uint32_t w = 0; w < L.ref_words; ++w) {
+    const std::int32_t e = d.dec[w];
+    if (e >= 0) {
+      ref[w] = dev[e];
+    } else {
+      const std::uint32_t code = static_cast<std::uint32_t>(-1 - e), b = code >> 1;
+      const std::uint32_t bits = static_cast<std::uint32_t>(dev[L.plane + 2 * (b >> 5) + (code & 1u)]);
+      const bool set = (bits >> (b & 31)) & 1u;
+      ref[w] = (code & 1u) ? (set ? 0 : 1) : (set ? 1 : 0);  // UB bit: ub <= 0; LB bit: lb >= 1
+    }
+  }
 }
 
 // The value-range analysis at run time.  Outside a failed round every

@@ -78,6 +78,24 @@ struct DeviceLayout {
   std::uint32_t rows_fast;  // set per launch: the same for the sum rows (fast_paths)
   std::uint32_t reif_fast;  // set per launch: the same for the reification records (fast_paths)
   std::uint32_t unit_fast;  // set per launch: the same for the unit records (fast_paths)
+  // Bit-plane 0/1 cells (lower_packed).  The 0/1 interval slots (RCPSP's
+  // overlap booleans, rcpsp.cpp:197-213) leave the word store: each becomes
+  // one bit of an (LB, UB) plane pair, LB bit = [lb >= 1], UB bit = [ub <= 0],
+  // both joined with red.shared.or (both only ever set: lb rises, ub falls);
+  // both set = the empty interval (failed).  The other words keep their
+  // reference order at device words [0, plane).
+  std::uint32_t packed;       // 1: this layout has bit planes
+  std::uint32_t plane;        // device word of plane pair 0 (even); pair k = words plane+2k (LB), plane+2k+1 (UB)
+  std::uint32_t n_pairs;      // plane pairs (32 cells each)
+  std::uint32_t ref_words;    // words of the reference store
+  std::uint32_t dec;          // per reference word: device word (>= 0) or -1 - (2 * bit + is_ub)
+  // Bit rows: compile_sum rows (propagation.cpp:314-335) over packed cells.
+  // Row r reads bits brow_base[r] + off for each term (coef << 20 | off) of
+  // its pattern [meta.x, meta.y) — RCPSP rows of one resource share a pattern.
+  std::uint32_t brow_meta;    // int4 per row: {pattern begin, pattern end, c, lsum word}
+  std::uint32_t brow_base;    // first bit of each row
+  std::uint32_t bpat;         // pattern terms
+  std::uint32_t n_brows, brow_lanes;
 };
 
 
@@ -105,10 +123,31 @@ struct Lowered {
   std::int64_t unit_k = 0;                   // max |k| over the unit tells
   std::vector<std::int64_t> row_sum0, row_sum1;  // per row: sum |coef| over class-0 / class-1 terms
   std::vector<std::int32_t> slot_of_word;  // for diagnostics
+  // Packed layouts (L.packed): the host side of the bit planes.
+  std::vector<std::int32_t> dec;          // L.dec on the host
+  std::vector<std::int32_t> bit_lbw;      // reference lb word of each bit
+  std::vector<std::int32_t> bit_fold_lb;  // max of the folded lb constants of each bit's cell (0 or 1)
+  std::vector<std::int32_t> bit_fold_ub;  // min of the folded ub constants (0 or 1)
+  std::uint32_t dev_words = 0;            // device store words (the reference's n_words when not packed)
 };
 
 // Throws std::runtime_error (mapped to PCCP_EMODEL) on malformed tables.
 Lowered lower_model(const pccp_model& m);
+
+// The device layout with bit-plane 0/1 cells when the model has them
+// (L.packed = 1), else the plain lowering.  A slot is packed when it is an
+// interval whose lb and ub are both folded to constants in {0, 1} (so every
+// store that reaches the device holds it at 0/1, or failed), whose only
+// writers are those folds, fused reifications (b <- (1,1) / (0,0)) and
+// compile_sum zeroing (b <- (0,0)), and whose only readers are reifications
+// and sum rows whose terms are all packed.  Every value such a cell can hold
+// is one of (0,1), (1,1), (0,0) or failed: the two bits are exact.
+Lowered lower_packed(const pccp_model& m);
+
+// Reference store -> packed device store (folding the packed cells' constant
+// tells, as every entry point folds) and back.  Plain layouts copy.
+void to_device(const Lowered& d, const std::int32_t* ref, std::int32_t* dev);
+void to_reference(const Lowered& d, const std::int32_t* dev, std::int32_t* ref);
 
 // Value-range analysis for the exact 32-bit paths (engine.cu sets
 // DeviceLayout::ne_fast / rows_fast per launch from the input stores): true

@@ -177,7 +177,7 @@ __device__ int classify(const G& g, volatile int* S, const int* __restrict__ T, 
     if (C.count && g.rank() == 0) ++cnt.fails;
     return 0;
   }
-  if (C.hash && C.count && g.rank() == 0) cnt.hash += store_hash(S, (int)L.n_words);
+  if (C.hash && C.count && g.rank() == 0) cnt.hash += store_hash_ref(S, T, L);
   const int b = branch(g, S, T, L, lbw, mid);
   if (b < 0) {
     if (g.rank() == 0) {

@@ -104,3 +104,63 @@ def test_value_range_analysis_decisions():
     # domains large enough that a row sum could pass 2^30: rows widened, units not
     big = Model.random_csp(1, dom_hi=10**8)
     assert fast_mask(big, big.bottom()) & ROWS == 0
+
+
+def layout(m, stores):
+    """pccp_lower_layout: (device words, device stores, stores converted back)."""
+    t = m.tables()
+    s, keep = t.as_struct()
+    a = np.ascontiguousarray(stores, np.int32).reshape(-1, t.n_words)
+    dw = C.c_uint32(0)
+    N.check(N.lib().pccp_lower_layout(C.byref(s), None, 0, None, None, C.byref(dw)))
+    dev = np.zeros((a.shape[0], dw.value), np.int32)
+    back = np.zeros_like(a)
+    N.check(N.lib().pccp_lower_layout(C.byref(s), a.ctypes.data_as(C.c_void_p), a.shape[0],
+                                      dev.ctypes.data_as(C.c_void_p), back.ctypes.data_as(C.c_void_p), C.byref(dw)))
+    return dw.value, dev, back
+
+
+def test_bit_plane_layout():
+    """lower_packed: RCPSP's n^2 overlap booleans (rcpsp.cpp:197-213) become bit
+    cells (RCPSP30: 2,240 words -> 256, RCPSP120: 30,500 -> 1,664); N-Queens
+    and the CSP have none.  Reference -> device -> reference is the identity on
+    every store whose 0/1 cells hold (0,0), (0,1), (1,1) or the empty (1,0),
+    and a cell outside [0, 1] after its folded constants stays empty."""
+    from oracle.port import Oracle
+    assert lower(Model.nqueens(14))[0].packed_cells == 0
+    assert lower(Model.random_csp(1))[0].packed_cells == 0
+    info = lower(Model.rcpsp_random(1, 120, 4))[0]
+    assert (info.packed_cells, info.device_words) == (122 * 122, 1664)
+    r = Model.rcpsp_random(1, 30, 4)
+    info = lower(r)[0]
+    assert (info.packed_cells, info.device_words) == (32 * 32, 256)
+    t = r.tables()
+    failed, root, _, _ = Oracle(t).run_sequential(r.bottom())
+    assert not failed
+    rng = np.random.default_rng(7)
+    n = 32  # tasks incl. dummies
+    bw = np.array([t.slot_word[n + k] for k in range(n * n)])  # overlap cells follow the starts
+    stores = np.repeat(root[None, :], 64, axis=0)
+    for s in stores[1:]:
+        v = rng.integers(0, 4, bw.size)  # (0,1), (1,1), (0,0), (1,0) = empty
+        s[bw] = np.where(v == 1, 1, np.where(v == 3, 1, 0))
+        s[bw + 1] = np.where(v == 2, 0, np.where(v == 3, 0, 1))
+    # the folded constants of each cell: the bottom store converted and back
+    _, _, fb = layout(r, r.bottom()[None, :])
+    flb, fub = fb[0, bw], fb[0, bw + 1]
+    assert set(np.unique(flb)) <= {0, 1} and set(np.unique(fub)) <= {0, 1}
+    want = stores.copy()
+    lb, ub = np.maximum(stores[:, bw], flb), np.minimum(stores[:, bw + 1], fub)
+    empty = lb > ub
+    want[:, bw], want[:, bw + 1] = np.where(empty, 1, lb), np.where(empty, 0, ub)
+    dw, dev, back = layout(r, stores)
+    assert dw == 256
+    assert np.array_equal(back, want)
+    assert np.array_equal(layout(r, root[None, :])[2][0], root)
+    assert np.array_equal(dev[:, :64], stores[:, :64])  # the starts keep their words
+    # outside [0, 1]: lb 2 / ub -1 are empty after the folds, and stay empty
+    s = root.copy()
+    s[bw[5]] = 2
+    s[bw[9] + 1] = -1
+    _, _, back = layout(r, s[None, :])
+    assert back[0, bw[5]] > back[0, bw[5] + 1] and back[0, bw[9]] > back[0, bw[9] + 1]
