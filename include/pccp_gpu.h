@@ -108,7 +108,7 @@ typedef struct pccp_gpu_cfg {
   int32_t shard_index;   /* this GPU's share of the EPS frontier: i mod shard_count == shard_index */
   int32_t shard_count;   /* 0/1 = unsharded */
   int32_t hash;          /* 1: accumulate the order-independent fixed-point hash-sum */
-  int32_t verbose;
+  int32_t verbose;       /* 1: one summary line per device search on stderr (layout, grid, times, counters) */
   int32_t value_order;   /* DFS branch order: 0 left (x <= mid) first, as dfs() (solver.cpp:139-143);
                             1 right first; 2 mixed (odd groups right first); -1 = 0.
                             The explored tree is the same,

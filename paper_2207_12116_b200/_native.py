@@ -188,6 +188,8 @@ def lib():
         "pccp_host_rcpsp_check": (C.c_int, [vp, vp]),
     }
     for name, (res, args) in sigs.items():
+        if os.environ.get("PCCP_LIB") and not hasattr(L, name):
+            continue  # an older build variant (A/B timing) may lack newer entry points
         f = getattr(L, name)
         f.restype = res
         f.argtypes = args

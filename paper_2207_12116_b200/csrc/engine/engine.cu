@@ -203,22 +203,32 @@ void plan(pccp_gpu_ctx* c) {
   const DeviceLayout& L = c->dl.L;
   c->store_stride = (int)align4(L.n_words + 1);  // + the constant-zero word
   const int gt = c->cfg.group_threads;
-  c->warp = gt == 32 || (gt == 0 && L.n_words <= 256);
+  // warp groups for small models: judged on the reference store (a packed
+  // RCPSP30 store is 256 words, but its 14k commands want a CTA per node:
+  // warp groups explored 12x the nodes and took 13x longer, measured)
+  c->warp = gt == 32 || (gt == 0 && (L.packed ? L.ref_words : L.n_words) <= 256);
   if (c->warp) {
     c->gpc = c->cfg.groups_per_cta > 0 ? std::min(c->cfg.groups_per_cta, 8) : 8;  // MaxThreads<WarpGroup>
     c->block = 32 * c->gpc;
   } else {
     int t = gt;
     if (t <= 0) {
+      // ~16 reference commands per thread, up to 1024; but tables streamed
+      // from L2 (too large for shared memory) want more resident groups per
+      // SM to hide that latency: 256 (RCPSP120: 6.95 M nodes/s at 256 threads,
+      // 6.48 at 512, 5.34 at 1024, measured)
+      const size_t base1 = 72 * 4 + (size_t)c->store_stride * 4 + sizeof(dev::Cnt) + sizeof(dev::Pf);
+      const bool l2_tables = base1 + (size_t)align4(L.hot_words) * 4 > 100 * 1024 && !std::getenv("PCCP_TABLE_SMEM");
       t = 128;
-      while (t < 1024 && (std::uint32_t)(2 * t) <= L.n_ref_cmds / 16) t *= 2;
+      while (t < (l2_tables ? 256 : 1024) && (std::uint32_t)(2 * t) <= L.n_ref_cmds / 16) t *= 2;
     }
     if (t < 64 || t > 1024 || (t & 31)) throw ArgError("group_threads must be 32 or a multiple of 32 in [64, 1024]");
     c->gpc = 1;
     c->block = t;
   }
-  const size_t base = 72 * 4 + (size_t)(c->warp ? c->gpc : 1) * (c->store_stride * 4 + 64);  // + one Cnt per group
-  const size_t table = (size_t)align4(L.blob_words) * 4;
+  const size_t base = 72 * 4 + (size_t)(c->warp ? c->gpc : 1) *
+                                   (c->store_stride * 4 + sizeof(dev::Cnt) + sizeof(dev::Pf));  // + per-group Cnt, Pf
+  const size_t table = (size_t)align4(L.hot_words) * 4;  // the staged (hot) prefix of the tables
   if (base > c->smem_optin) throw LimitError("store of " + std::to_string(L.n_words) + " words exceeds shared memory");
   c->ne_only = L.n_ne > 0 && !L.n_reif && !L.n_unit1 && !L.n_unit2 && !L.n_small && !L.n_rows && !L.n_gen &&
                        !L.filtered && !std::getenv("PCCP_NO_NE_KERNEL")
@@ -373,6 +383,7 @@ void run_search(pccp_gpu_ctx* c, int mode, const int32_t* root_words, int depth_
   const dev::Model M = c->model(var_order, var_seed, root_words, 1, (size_t)c->low.L.n_words);
   dev::SearchCtl C{};
   C.G = c->G;
+  C.blob = c->blob.p;
   C.n_peers = mode == 1 ? c->n_peers : 0;
   C.peers = c->d_peers.p;
   C.mode = mode;
@@ -633,6 +644,16 @@ void run_search(pccp_gpu_ctx* c, int mode, const int32_t* root_words, int depth_
                                  std::clamp(c->cfg.audit_shift, 0, 40),
                              (unsigned long long)c->cfg.audit_nodes)
                        : 0u;
+  if (c->cfg.verbose)
+    fprintf(stderr,
+            "pccp_gpu[dev %d shard %d/%d]: %s, %d %s groups (%d CTAs x %d threads, smem %zu B, tables in %s), "
+            "store %u words%s; root %.3f ms, decompose %.3f ms (%d subproblems, %llu levels), search %.3f ms; "
+            "nodes %llu, rounds %llu, donations %llu%s\n",
+            c->device, shard_index, shard_count, mode == 1 ? "minimise" : "enumerate", c->groups(),
+            c->warp ? "warp" : "CTA", c->ctas, c->block, c->smem, c->table_in_smem ? "smem" : "L2",
+            (unsigned)nw, L.packed ? " (bit-plane 0/1 cells)" : "", out.root_ms, out.decompose_ms - out.root_ms, count,
+            (unsigned long long)level, out.kernel_ms, out.g.nodes, out.g.rounds, out.g.donations,
+            out.g.incomplete ? ", incomplete" : "");
   if (out.g.stop == 2) {
     if (out.g.error_code == 1) throw std::runtime_error("branch: a candidate variable is unbounded");
     throw LimitError("DFS stack capacity exceeded");
@@ -869,7 +890,7 @@ int pccp_gpu_lowering_info(pccp_gpu_ctx* c, pccp_lowering_info* o) {
     o->n_rows = L.n_rows;
     o->n_row_terms = L.n_row_terms;
     o->n_generic = L.n_gen;
-    o->table_bytes = c->dl.L.blob_words * 4;
+    o->table_bytes = c->dl.L.hot_words * 4;
     o->store_bytes = c->dl.L.n_words * 4;
     o->packed_cells = (std::uint32_t)c->dl.bit_lbw.size();
     o->device_words = c->dl.L.n_words;
@@ -905,7 +926,7 @@ int pccp_lower_only(const pccp_model* m, pccp_lowering_info* o, uint32_t* shape_
     o->n_rows = L.n_rows;
     o->n_row_terms = L.n_row_terms;
     o->n_generic = L.n_gen;
-    o->table_bytes = L.blob_words * 4;
+    o->table_bytes = L.hot_words * 4;
     o->store_bytes = L.n_words * 4;
     o->alg_bytes_per_eval = low.alg_bytes_per_eval;
     o->store_bytes_per_round = low.store_bytes_per_round;

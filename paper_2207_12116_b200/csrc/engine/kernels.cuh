@@ -42,7 +42,10 @@ struct Globals {
   unsigned long long nodes_reserved;  // materialisations admitted against node_limit
   unsigned long long t0;           // %globaltimer at search start
   unsigned long long timeout_ns;   // 0: none
-  unsigned int cursor;             // EPS work queue
+  // {cursor, stop, incomplete, incumbent} and {hungry, active, wait_head,
+  // wait_tail} are 16-byte blocks: the search prefetches both per node with
+  // cp.async (search.cuh prefetch_ctl)
+  alignas(16) unsigned int cursor;  // EPS work queue
   int stop;                        // 1: limit reached, 2: model error
   int incomplete;                  // a subproblem was abandoned
   // [incumbent, n_impr): the cross-rank cells.  With peers linked they are
@@ -57,7 +60,7 @@ struct Globals {
   unsigned long long impr_ns[64];
   int error_code;
   // dynamic load balancing (search.cuh maybe_donate)
-  int hungry;                   // idle groups waiting for a donation
+  alignas(16) int hungry;       // idle groups waiting for a donation
   int active;                   // groups exploring, or promised a donation
   unsigned wait_head, wait_tail;
   unsigned long long donations;
@@ -755,10 +758,10 @@ __device__ bool eval_rows(const G& g, unsigned sb, const Tab<TS>& tab, const Dev
 // Sums are exact in 32 bits: lower_packed bounds sum |coef| by 2^29.
 template <class G, bool TS>
 __device__ bool eval_brows(const G& g, unsigned sb, const Tab<TS>& tab, const DeviceLayout& L) {
-  const int R = (int)L.brow_lanes;
+  const int R = (int)L.brow_lanes, lg = (int)L.brow_lg;
   const int sub = g.rank() & (R - 1);
-  const int per_pass = g.size() / R;
-  const int my = g.rank() / R;
+  const int per_pass = g.size() >> lg;
+  const int my = g.rank() >> lg;
   const int n_rows = (int)L.n_brows;
   const unsigned sp = sb + 4u * L.plane;
   unsigned ch = 0;
@@ -769,7 +772,7 @@ __device__ bool eval_brows(const G& g, unsigned sb, const Tab<TS>& tab, const De
     const int b0 = act ? tab.ld1(L.brow_base, row) : 0;
     const int j0 = meta.x + sub, end = meta.y, c = meta.z;
     const unsigned alsum = sb + ((unsigned)meta.w << 2);
-    const int n_my = end > j0 ? (end - j0 + R - 1) / R : 0;
+    const int n_my = end > j0 ? (end - j0 + R - 1) >> lg : 0;
     int x[kRowTerms];
     unsigned v = 0, z = 0;  // this lane's terms: LB bits, UB bits
 #pragma unroll
@@ -805,6 +808,77 @@ __device__ bool eval_brows(const G& g, unsigned sb, const Tab<TS>& tab, const De
             sred_or(sp + ((bit >> 5) << 3) + 4u, 1u << (bit & 31u));
             ch = 1u;
           }
+        }
+      }
+    }
+  }
+  return ch != 0;
+}
+
+// Bit rows, word-parallel (L.wrows, lower.cpp): lane q of a row's 2^wrow_lg
+// lanes takes the 32-bit chunk q of the row's bit window, funnel-shifted out
+// of two plane pairs: lb bits & term mask T.  The chunk's sum is
+// popc(lb & U0) + 2 popc(lb & U1) + 4 popc(lb & U2) (U_b: the terms whose
+// coefficient has bit b).  Zeroing, [coef + s - coef * lb > c] => b <- (0, 0):
+// every term when s > c (overload), else the terms with lb = 0 and coef >
+// c - s, a bit-sliced comparison of the planes against c - s.  A new UB bit
+// (not in the snapshot) is a change; the joins are red.or on the two words.
+__device__ __forceinline__ unsigned coef_gt(const int4& P, int thr) {  // terms with coef > thr >= 0
+  if (thr >= 8) return 0u;
+  unsigned gt = 0u, eq = (unsigned)P.x;
+  const unsigned U[3] = {(unsigned)P.y, (unsigned)P.z, (unsigned)P.w};
+#pragma unroll
+  for (int b = 2; b >= 0; --b) {
+    if ((thr >> b) & 1) {
+      eq &= U[b];
+    } else {
+      gt |= eq & U[b];
+      eq &= ~U[b];
+    }
+  }
+  return gt;
+}
+
+template <class G, bool TS>
+__device__ bool eval_wrows(const G& g, unsigned sb, const Tab<TS>& tab, const DeviceLayout& L) {
+  const int lg = (int)L.wrow_lg, Q = 1 << lg;
+  const int q = g.rank() & (Q - 1);
+  const int per_pass = g.size() >> lg;
+  const int my = g.rank() >> lg;
+  const int n_rows = (int)L.n_brows;
+  const unsigned sp = sb + 4u * L.plane;
+  unsigned ch = 0;
+  for (int base = 0; base < n_rows; base += per_pass) {
+    const int row = base + my;
+    const bool act = row < n_rows;
+    const int4 meta = act ? tab.ld4(L.wrow_meta, row) : make_int4(0, INT_MAX, 0, 0);  // {chunk0, c, lsum, bit0}
+    const int4 P = act ? tab.ld4(L.wpat, meta.x + q) : make_int4(0, 0, 0, 0);          // {T, U0, U1, U2}
+    const unsigned bit = (unsigned)meta.w + 32u * (unsigned)q, sh = bit & 31u;
+    const unsigned a = sp + ((bit >> 5) << 3);
+    const unsigned alsum = sb + ((unsigned)meta.z << 2);
+    const int lsum_now = act && q == 0 ? sld(alsum) : INT_MAX;
+    unsigned lbw = 0u, ubw = 0u;
+    if (P.x) {
+      const int2 w0 = sld2(a), w1 = sld2(a + 8u);
+      lbw = __funnelshift_r((unsigned)w0.x, (unsigned)w1.x, sh) & (unsigned)P.x;
+      ubw = __funnelshift_r((unsigned)w0.y, (unsigned)w1.y, sh) & (unsigned)P.x;
+    }
+    int s = __popc(lbw & (unsigned)P.y) + 2 * __popc(lbw & (unsigned)P.z) + 4 * __popc(lbw & (unsigned)P.w);
+    for (int o = Q >> 1; o > 0; o >>= 1) s += __shfl_xor_sync(kFull, s, o, Q);
+    if (act) {
+      const int c = meta.y;
+      const bool over = s > c;
+      const int cell = over ? INT_MAX : s;  // [lsum > c] => lsum <- +inf
+      if (q == 0 && cell > lsum_now) {
+        sred_max(alsum, cell);
+        ch = 1u;
+      }
+      if (c != INT_MAX && P.x) {
+        const unsigned z = (over ? (unsigned)P.x : coef_gt(P, c - s) & ~lbw) & ~ubw;
+        if (z) {
+          sred_or(a + 4u, z << sh);
+          if (sh && (z >> (32u - sh))) sred_or(a + 12u, z >> (32u - sh));
+          ch = 1u;
         }
       }
     }
@@ -916,7 +990,18 @@ __device__ __forceinline__ bool eval_other_families(const G& g, volatile int* S,
                                                     const DeviceLayout& L) {
     const int* __restrict__ T = tab.p;
     bool ch = false;
-    if (L.packed) {
+    if (L.reif8) {  // packed, 8-byte records
+      const unsigned sp = sb + 4u * L.plane;
+      auto rec = [&](int i) {
+        const int2 q = tab.ld2(L.reif, i);
+        return make_int4(q.x, q.y & 0x3ffff, (q.y << 7) >> 25, q.y >> 25);
+      };
+      if (L.reif_fast) {
+        for (int i = g.rank(); i < (int)L.n_reif; i += g.size()) ch |= eval_reif_bits<true>(sb, sp, rec(i));
+      } else {
+        for (int i = g.rank(); i < (int)L.n_reif; i += g.size()) ch |= eval_reif_bits<false>(sb, sp, rec(i));
+      }
+    } else if (L.packed) {
       const unsigned sp = sb + 4u * L.plane;
       if (L.reif_fast) {
         for (int i = g.rank(); i < (int)L.n_reif; i += g.size()) ch |= eval_reif_bits<true>(sb, sp, tab.ld4(L.reif, i));
@@ -953,7 +1038,7 @@ __device__ __forceinline__ bool eval_other_families(const G& g, volatile int* S,
     for (int i = g.rank(); i < (int)L.n_small; i += g.size()) ch |= eval_small(S, T, L, i);
     dbg_r(2);
     if (L.n_rows) ch |= eval_rows(g, sb, tab, L);
-    if (L.n_brows) ch |= eval_brows(g, sb, tab, L);
+    if (L.n_brows) ch |= L.wrows ? eval_wrows(g, sb, tab, L) : eval_brows(g, sb, tab, L);
     dbg_r(3);
     for (int i = g.rank(); i < (int)L.n_gen; i += g.size())
       ch |= eval_generic(S, T + L.gen_code + T[L.gen_off + i]);

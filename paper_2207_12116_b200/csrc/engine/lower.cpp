@@ -737,7 +737,9 @@ Lowered lower_impl(const pccp_model& m, bool want_bits) {
   }
   const std::uint32_t n_pairs = (n_bits + 31) / 32;
   const std::uint32_t plane = packed ? (n_int + 1) & ~1u : n_int;
-  const std::uint32_t DW = packed ? plane + 2 * n_pairs : NW;  // device store words
+  // + one zero pair after the planes: a row's 32-bit window may read the
+  // pair after its last bit (eval_wrows)
+  const std::uint32_t DW = packed ? plane + 2 * n_pairs + 2 : NW;  // device store words
   out.dev_words = DW;
   auto W = [&](std::uint32_t w) -> std::uint32_t {  // device word of a reference word (Z -> the device Z)
     if (w >= NW) return DW;
@@ -870,8 +872,21 @@ Lowered lower_impl(const pccp_model& m, bool want_bits) {
     return (static_cast<std::uint32_t>(a.xy) >> 16) < (static_cast<std::uint32_t>(b.xy) >> 16);
   });
   L.n_reif = static_cast<std::uint32_t>(reifs.size());
-  L.reif = reserve_arr(4 * L.n_reif);
+  // Packed layouts: 8-byte records {lx | ly << 16, bit | p << 18 | q << 25}
+  // (7-bit signed p, q; RCPSP: p = 0, q = 1 - d) when every record fits.
+  L.reif8 = packed ? 1u : 0u;
+  for (const Reif& r : reifs)
+    if (r.b < 0 || r.b >= (1 << 18) || r.p < -64 || r.p > 63 || r.q < -64 || r.q > 63) L.reif8 = 0;
+  if (std::getenv("PCCP_NO_REIF8")) L.reif8 = 0;
+  L.reif = reserve_arr((L.reif8 ? 2 : 4) * L.n_reif);
   for (std::uint32_t i = 0; i < L.n_reif; ++i) {
+    if (L.reif8) {
+      B[L.reif + 2 * i + 0] = reifs[i].xy;
+      B[L.reif + 2 * i + 1] = static_cast<std::int32_t>(static_cast<std::uint32_t>(reifs[i].b) |
+                                                        ((static_cast<std::uint32_t>(reifs[i].p) & 0x7fu) << 18) |
+                                                        ((static_cast<std::uint32_t>(reifs[i].q) & 0x7fu) << 25));
+      continue;
+    }
     B[L.reif + 4 * i + 0] = reifs[i].xy;
     B[L.reif + 4 * i + 1] = reifs[i].b;
     B[L.reif + 4 * i + 2] = reifs[i].p;
@@ -1066,6 +1081,63 @@ Lowered lower_impl(const pccp_model& m, bool want_bits) {
       B[L.brow_base + r] = base[r];
     }
     std::copy(pat_terms.begin(), pat_terms.end(), B.begin() + L.bpat);
+    // Word-parallel form (kernels.cuh eval_wrows) when every bit row has
+    // coefficients in [0, 8) and no repeated cell: per 32-bit chunk of the
+    // row's bit window, the term mask T and the coefficient bit-planes U0..U2,
+    // so a chunk's sum is popc arithmetic and its zeroing mask (coef > c - s)
+    // a bit-sliced comparison.
+    bool wok = L.n_brows > 0 && !std::getenv("PCCP_NO_WROWS");
+    std::uint32_t max_ch = 1;
+    for (std::size_t r = 0; r < bit_rows.size() && wok; ++r) {
+      std::vector<std::uint8_t> seen;
+      for (std::uint32_t k = range[r].first; k < range[r].second; ++k) {
+        const std::int32_t coef = pat_terms[k] >> kTermWordBits;
+        const std::uint32_t off = static_cast<std::uint32_t>(pat_terms[k]) & kTermWordMask;
+        if (coef < 0 || coef > 7 || off >= 32 * 32) wok = false;
+        if (!wok) break;
+        if (seen.size() <= off) seen.resize(off + 1, 0);
+        if (seen[off]++) wok = false;
+        max_ch = std::max<std::uint32_t>(max_ch, off / 32 + 1);
+      }
+    }
+    if (wok) {
+      L.wrows = 1;
+      L.wrow_lg = 0;
+      while ((1u << L.wrow_lg) < max_ch) ++L.wrow_lg;
+      const std::uint32_t chunks = 1u << L.wrow_lg;
+      std::map<std::pair<std::uint32_t, std::uint32_t>, std::uint32_t> wpat_of;  // pattern range -> first int4
+      std::vector<std::int32_t> wpat;
+      std::vector<std::uint32_t> wfirst(bit_rows.size());
+      for (std::size_t r = 0; r < bit_rows.size(); ++r) {
+        auto it = wpat_of.find(range[r]);
+        if (it == wpat_of.end()) {
+          const std::uint32_t first = static_cast<std::uint32_t>(wpat.size() / 4);
+          std::vector<std::uint32_t> q(4 * chunks, 0);
+          for (std::uint32_t k = range[r].first; k < range[r].second; ++k) {
+            const std::uint32_t coef = static_cast<std::uint32_t>(pat_terms[k] >> kTermWordBits);
+            const std::uint32_t off = static_cast<std::uint32_t>(pat_terms[k]) & kTermWordMask;
+            const std::uint32_t m = 1u << (off & 31), c4 = 4 * (off / 32);
+            q[c4] |= m;
+            for (int b = 0; b < 3; ++b)
+              if ((coef >> b) & 1u) q[c4 + 1 + b] |= m;
+          }
+          for (std::uint32_t v : q) wpat.push_back(static_cast<std::int32_t>(v));
+          it = wpat_of.emplace(range[r], first).first;
+        }
+        wfirst[r] = it->second;
+      }
+      L.wrow_meta = reserve_arr(4 * L.n_brows);
+      L.wpat = reserve_arr(static_cast<std::uint32_t>(wpat.size()));
+      for (std::uint32_t r = 0; r < L.n_brows; ++r) {
+        B[L.wrow_meta + 4 * r + 0] = static_cast<std::int32_t>(wfirst[r]);
+        B[L.wrow_meta + 4 * r + 1] = bit_rows[r].c;
+        B[L.wrow_meta + 4 * r + 2] = static_cast<std::int32_t>(bit_rows[r].lsum);
+        B[L.wrow_meta + 4 * r + 3] = base[r];
+      }
+      std::copy(wpat.begin(), wpat.end(), B.begin() + L.wpat);
+    }
+    L.brow_lg = 0;
+    while ((1u << L.brow_lg) < L.brow_lanes) ++L.brow_lg;
   }
   // Value-range analysis over the reference words (plain layouts only: a
   // packed layout takes the plain lowering's per-launch flags, engine.cu).
@@ -1134,16 +1206,6 @@ Lowered lower_impl(const pccp_model& m, bool want_bits) {
                              std::abs(std::int64_t{B[L.reif + 4 * i + 3]})});
     }
   }
-  L.hot_words = static_cast<std::uint32_t>(B.size());
-
-  L.n_fold = static_cast<std::uint32_t>(fold_w.size());
-  L.fold_w = reserve_arr(L.n_fold);
-  L.fold_v = reserve_arr(L.n_fold);
-  for (std::uint32_t i = 0; i < L.n_fold; ++i) {
-    B[L.fold_w + i] = fold_w[i];
-    B[L.fold_v + i] = fold_v[i];
-  }
-
   L.n_gen = static_cast<std::uint32_t>(generic.size());
   L.gen_off = reserve_arr(L.n_gen + 1);
   std::uint32_t gen_len = 0;
@@ -1221,12 +1283,24 @@ Lowered lower_impl(const pccp_model& m, bool want_bits) {
   } else {
     L.obj_lbw = -1;
   }
+  // Everything above is read per round or per node (staged into shared memory
+  // when it fits); the folds (node entry of a root) and the decode table
+  // (hash-sums of packed stores) stay in global memory.
+  L.hot_words = static_cast<std::uint32_t>(B.size());
+  L.n_fold = static_cast<std::uint32_t>(fold_w.size());
+  L.fold_w = reserve_arr(L.n_fold);
+  L.fold_v = reserve_arr(L.n_fold);
+  for (std::uint32_t i = 0; i < L.n_fold; ++i) {
+    B[L.fold_w + i] = fold_w[i];
+    B[L.fold_v + i] = fold_v[i];
+  }
+
   // Byte model of one round (lower.hpp): per record, the store words its
   // evaluation reads and its table entry.
   {
     double sb = 0, tb = 0;
     sb += 16.0 * L.n_ne, tb += 16.0 * L.n_ne;      // (lb, ub) of x and y; int4
-    sb += 24.0 * L.n_reif, tb += 16.0 * L.n_reif;  // x, y, b intervals; int4
+    sb += 24.0 * L.n_reif, tb += (L.reif8 ? 8.0 : 16.0) * L.n_reif;  // x, y, b intervals (or x, y, b's plane pair); int4 / int2
     auto unit_words = [&](std::uint32_t x, std::uint32_t w) {
       int k = 1;  // the target
       for (std::uint32_t v : {x & 0xffffu, x >> 16, (w >> 15) & 0x7fffu}) k += v != Z ? 1 : 0;
@@ -1258,9 +1332,14 @@ Lowered lower_impl(const pccp_model& m, bool want_bits) {
       tb += 4.0 * (m.cmd_off[g + 1] - m.cmd_off[g]);
     }
     sb += 8.0 * L.n_iv + 4.0 * L.n_sc;  // the failure scan
-    for (const Row& r : bit_rows) sb += 4.0 + 8.0 * r.terms.size();  // lsum + each term's plane pair
-    tb += 20.0 * bit_rows.size();
-    for (std::uint32_t r = 0; r < L.n_brows; ++r) tb += 4.0 * (B[L.brow_meta + 4 * r + 1] - B[L.brow_meta + 4 * r]);
+    if (L.wrows) {  // per row: lsum + two plane pairs per 32-bit chunk; meta + one int4 per chunk
+      sb += (4.0 + 16.0 * (1u << L.wrow_lg)) * L.n_brows;
+      tb += (16.0 + 16.0 * (1u << L.wrow_lg)) * L.n_brows;
+    } else {
+      for (const Row& r : bit_rows) sb += 4.0 + 8.0 * r.terms.size();  // lsum + each term's plane pair
+      tb += 20.0 * bit_rows.size();
+      for (std::uint32_t r = 0; r < L.n_brows; ++r) tb += 4.0 * (B[L.brow_meta + 4 * r + 1] - B[L.brow_meta + 4 * r]);
+    }
     sb += 8.0 * L.n_pairs;  // the planes' failure scan
     out.store_bytes_per_round = sb;
     out.table_bytes_per_round = tb;

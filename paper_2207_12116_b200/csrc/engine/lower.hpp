@@ -16,7 +16,8 @@
 //           into one row evaluated by a sub-warp from one read of the lbs (H2).
 //   generic anything else, interpreted from the flat stream on the device.
 //
-// Word indices are the reference's (H7), so stores round-trip unchanged.
+// Word indices are the reference's (H7), so stores round-trip unchanged;
+// lower_packed's layout moves 0/1 cells into bit planes (to_device / to_reference).
 #pragma once
 
 #include <cstdint>
@@ -71,7 +72,7 @@ struct DeviceLayout {
   std::uint32_t n_words;
   std::uint32_t n_ref_cmds;
   std::uint32_t blob_words;
-  std::uint32_t hot_words;  // prefix of the blob read every round (small + rows)
+  std::uint32_t hot_words;  // prefix of the blob read per round or per node (staged to smem); folds, decode after
   std::uint32_t var_order;  // set per launch: 0 first-fail (branch, solver.cpp:19-47), 1-3 smallest lb
   std::uint32_t var_seed;   // set per launch: var_order 3 tie-break seed
   std::uint32_t ne_fast;    // set per launch: value-range analysis proved the 32-bit NE path exact
@@ -96,6 +97,13 @@ struct DeviceLayout {
   std::uint32_t brow_base;    // first bit of each row
   std::uint32_t bpat;         // pattern terms
   std::uint32_t n_brows, brow_lanes;
+  std::uint32_t reif8;        // packed reification records are int2 {lx | ly << 16, bit | p << 18 | q << 25}
+  std::uint32_t brow_lg;      // log2 brow_lanes
+  // Word-parallel bit rows (eval_wrows): 2^wrow_lg lanes per row, one per
+  // 32-bit chunk of the row's bit window.
+  std::uint32_t wrows, wrow_lg;
+  std::uint32_t wrow_meta;    // int4 per row: {first chunk (int4 index into wpat), c, lsum word, first bit}
+  std::uint32_t wpat;         // int4 per chunk: {term mask, coefficient bit-planes 0, 1, 2}
 };
 
 

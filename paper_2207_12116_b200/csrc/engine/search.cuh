@@ -24,6 +24,7 @@ struct SearchCtl {
   int hash;              // accumulate the fixed-point hash-sum
   int depth_cap;         // < 0: none
   int count;             // accumulate counters (EPS on shard 0 only)
+  const int* blob;       // the tables in global memory (the cold ones: folds, decode table)
   // node audit (pccp_gpu_audit): every 2^audit_shift-th materialisation of the
   // persistent search, up to audit_n samples of (pre, post, failed)
   int* audit_pre;
@@ -52,15 +53,40 @@ __device__ __forceinline__ void flush(Globals* G, Cnt& c) {
 
 __device__ __forceinline__ unsigned long long word_bit(int w) { return w < 64 ? 1ull << w : 0ull; }
 
+// Per-group control prefetch (rank 0 only).  The search's per-node control
+// reads — the stop flag, the incumbent (solver.cpp:96-99) and the donation
+// hunger — are L2 round trips that the whole group would wait for at the
+// node's first barrier.  Rank 0 instead fetches both 16-byte Globals blocks
+// into shared memory with cp.async.cg (L2, coherent with the atomics) when a
+// node starts and reads them when the next one starts: the latency hides
+// behind the node's propagation.  Values one node old are sound: a stale stop
+// flag stops one node later; a stale incumbent is still some solution's value,
+// only a weaker bound (`own` keeps the group's own improvements exact).
+struct alignas(16) Pf {
+  int ctl[4];   // cursor, stop, incomplete, incumbent
+  int hung[4];  // hungry, active, wait_head, wait_tail
+  int own;      // best value this group recorded (INT_MAX: none)
+  int pad[3];
+};
+
+__device__ __forceinline__ void prefetch_ctl(Pf* pf, const Globals* G) {
+  const unsigned d0 = (unsigned)__cvta_generic_to_shared(pf->ctl), d1 = (unsigned)__cvta_generic_to_shared(pf->hung);
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(d0), "l"(&G->cursor) : "memory");
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(d1), "l"(&G->hungry) : "memory");
+  asm volatile("cp.async.commit_group;" ::: "memory");
+}
+__device__ __forceinline__ void prefetch_wait() { asm volatile("cp.async.wait_all;" ::: "memory"); }
+
 // Objective tightening at materialisation (solver.cpp:96-99): obj <= best-1.
 // Returns the dirty bit of the objective's ub word when it moved (uniform).
 template <class G>
 __device__ __forceinline__ unsigned long long join_objective(const G& g, volatile int* S, const DeviceLayout& L,
-                                                             const SearchCtl& C) {
+                                                             const SearchCtl& C, const Pf* pf = nullptr) {
   if (C.mode != 1 || !C.bound || L.obj_lbw < 0) return 0ull;
   int moved = 0;
   if (g.rank() == 0) {
-    const int best = *(volatile int*)&C.G->incumbent;
+    const int best = pf ? min(*(volatile const int*)&pf->ctl[3], *(volatile const int*)&pf->own)
+                        : *(volatile int*)&C.G->incumbent;
     if (best != INT_MAX) moved = join_min(S, L.obj_lbw + 1, best - 1) ? 1 : 0;
   }
   // Only the filtered rounds use the dirty mask; the eventless loop needs no
@@ -71,11 +97,11 @@ __device__ __forceinline__ unsigned long long join_objective(const G& g, volatil
 
 // SharedControl::should_stop (solver.cpp:68-76): stop flag, timeout, node limit.
 // The limit checks of one materialisation, on the group's rank 0.
-__device__ __forceinline__ int stop_rank0(const SearchCtl& C) {
+__device__ __forceinline__ int stop_rank0(const SearchCtl& C, const Pf* pf = nullptr) {
   int stop = 0;
   {
     Globals* Gl = C.G;
-    stop = *(volatile int*)&Gl->stop;  // also raised by a peer's proof (k_signal_done)
+    stop = pf ? *(volatile const int*)&pf->ctl[1] : *(volatile int*)&Gl->stop;  // also raised by a peer's proof (k_signal_done)
     if (!stop && Gl->timeout_ns && globaltimer() - Gl->t0 >= Gl->timeout_ns) {
       atomicCAS(&Gl->stop, 0, 1);
       stop = 1;
@@ -132,11 +158,13 @@ __device__ __forceinline__ bool time_stop(const G& g, const SearchCtl& C, unsign
 // best_value is an improvement: its store is copied, it is counted and it is
 // logged, so the log is strictly decreasing (test_solver.cpp:247-261).
 template <class G>
-__device__ void record_solution(const G& g, volatile int* S, const DeviceLayout& L, const SearchCtl& C, Cnt& cnt) {
+__device__ void record_solution(const G& g, volatile int* S, const DeviceLayout& L, const SearchCtl& C, Cnt& cnt,
+                                Pf* pf = nullptr) {
   Globals* Gl = C.G;
   const int value = S[L.obj_lbw];
   int improved = 0;
   if (g.rank() == 0) {
+    if (pf && value < pf->own) pf->own = value;
     const int old = atomicMin(&Gl->incumbent, value);
     improved = value < old;
     if (improved) {
@@ -172,12 +200,12 @@ __device__ void record_solution(const G& g, volatile int* S, const DeviceLayout&
 // must be expanded (lbw/mid set), 0 when it is a leaf, -1 on a model error.
 template <class G>
 __device__ int classify(const G& g, volatile int* S, const int* __restrict__ T, const DeviceLayout& L,
-                        const SearchCtl& C, Cnt& cnt, bool failed, int depth, int& lbw, int& mid) {
+                        const SearchCtl& C, Cnt& cnt, bool failed, int depth, int& lbw, int& mid, Pf* pf = nullptr) {
   if (failed) {
     if (C.count && g.rank() == 0) ++cnt.fails;
     return 0;
   }
-  if (C.hash && C.count && g.rank() == 0) cnt.hash += store_hash_ref(S, T, L);
+  if (C.hash && C.count && g.rank() == 0) cnt.hash += store_hash_ref(S, C.blob, L);
   const int b = branch(g, S, T, L, lbw, mid);
   if (b < 0) {
     if (g.rank() == 0) {
@@ -187,7 +215,7 @@ __device__ int classify(const G& g, volatile int* S, const int* __restrict__ T, 
     return -1;
   }
   if (b == 0) {  // every candidate fixed: a solution
-    if (C.mode == 1) record_solution(g, S, L, C, cnt);
+    if (C.mode == 1) record_solution(g, S, L, C, cnt, pf);
     else if (C.count && g.rank() == 0) ++cnt.sols;
     return 0;
   }
@@ -204,6 +232,7 @@ struct Frame {
   int* ring;
   unsigned long long* red;
   Cnt* cnt;  // one per group of the CTA
+  Pf* pf;    // one per group of the CTA
   int* stores;
 };
 
@@ -240,8 +269,8 @@ __device__ __forceinline__ Frame frame(const Model& M) {
   Frame f;
   int off = 0;
   f.T = M.blob;
-  if (M.table_in_smem) {
-    const int n4 = ((int)M.L.blob_words + 3) >> 2;
+  if (M.table_in_smem) {  // the hot prefix (lower.cpp hot_words); folds and the decode table stay global
+    const int n4 = ((int)M.L.hot_words + 3) >> 2;
     stage_table(M.blob, smem, (unsigned)n4 * 16u);
     f.T = smem;
     off = n4 * 4;
@@ -253,6 +282,9 @@ __device__ __forceinline__ Frame frame(const Model& M) {
   for (int i = threadIdx.x; i < M.cnt_slots * (int)(sizeof(Cnt) / 8); i += blockDim.x)
     reinterpret_cast<unsigned long long*>(f.cnt)[i] = 0ull;
   off += M.cnt_slots * (int)(sizeof(Cnt) / 4);
+  f.pf = reinterpret_cast<Pf*>(smem + off);
+  for (int i = threadIdx.x; i < M.cnt_slots; i += blockDim.x) f.pf[i].own = INT_MAX;
+  off += M.cnt_slots * (int)(sizeof(Pf) / 4);
   f.stores = smem + off;
   __syncthreads();
   return f;
@@ -328,7 +360,7 @@ __global__ void __launch_bounds__(MaxThreads<G, F>::value, MaxThreads<G, F>::min
     copy_words(g, S, io, (int)M.L.n_words);
     g.sync();
     if (fold) {
-      apply_fold(g, S, f.T, M.L);
+      apply_fold(g, S, M.blob, M.L);
       g.sync();
     }
     int r = 0;
@@ -354,7 +386,7 @@ __global__ void __launch_bounds__(MaxThreads<G, F>::value, MaxThreads<G, F>::min
   Cnt& cnt = f.cnt[GroupOf<G>::in_cta()];
   copy_words(g, S, store, (int)M.L.n_words);
   g.sync();
-  apply_fold(g, S, f.T, M.L);
+  apply_fold(g, S, M.blob, M.L);
   g.sync();
   join_objective(g, S, M.L, C);
   if (g.rank() == 0 && C.G->node_limit != ~0ull) atomicAdd(&C.G->nodes_reserved, 1ull);  // the root's materialisation
@@ -657,8 +689,9 @@ __device__ __forceinline__ void apply_pending(int* dst, int lbw_tag, int mid) {
 // propagated) into the receiver's mailbox.  The receiver materialises and
 // counts that node itself, so every node is still processed exactly once.
 // Rank 0: claim one unit of hunger (1) or not (0).
-__device__ __forceinline__ int claim_donation_rank0(Globals* Gl) {
-  if (*(volatile int*)&Gl->hungry <= 0) return 0;
+__device__ __forceinline__ int claim_donation_rank0(Globals* Gl, const Pf* pf) {
+  // the hunger from the prefetch when there is one; the claim itself is atomic
+  if ((pf ? *(volatile const int*)&pf->hung[0] : *(volatile int*)&Gl->hungry) <= 0) return 0;
   if (atomicAdd(&Gl->hungry, -1) > 0) return 1;
   atomicAdd(&Gl->hungry, 1);
   return 0;
@@ -712,6 +745,12 @@ __global__ void __launch_bounds__(MaxThreads<G, F>::value, MaxThreads<G, F>::min
   int* stk = P.stack_pool + (size_t)gid * (size_t)P.stack_depth * (size_t)P.entry_stride;
   Globals* Gl = C.G;
   Cnt& cnt = f.cnt[GroupOf<G>::in_cta()];
+  // the control prefetch pays for CTA groups, whose whole CTA waits at the
+  // node's first barrier; a warp group's wait is hidden by the SM's other
+  // warps, and the extra instructions cost the issue-bound Q14 kernel 4%
+  constexpr bool kPrefetch = std::is_same<G, CtaGroup>::value;
+  Pf* pf = kPrefetch ? f.pf + GroupOf<G>::in_cta() : nullptr;
+  if (kPrefetch && g.rank() == 0) prefetch_ctl(pf, Gl);
   bool queue_open = true;
   const bool right_first = P.value_order == 1 || (P.value_order == 2 && (gid & 1));
   for (;;) {
@@ -776,11 +815,14 @@ __global__ void __launch_bounds__(MaxThreads<G, F>::value, MaxThreads<G, F>::min
       g.sync();
     }
     for (;;) {
-      // one broadcast per node for the donation claim and the limit checks
+      // one broadcast per node for the donation claim and the limit checks,
+      // from the control words prefetched when the previous node started
       int ctl = 0;
       if (g.rank() == 0) {
-        if (P.balance && sp - bot >= P.balance) ctl |= claim_donation_rank0(Gl) << 1;
-        if (need_prop) ctl |= stop_rank0(C);
+        if constexpr (kPrefetch) prefetch_wait();
+        if (P.balance && sp - bot >= P.balance) ctl |= claim_donation_rank0(Gl, pf) << 1;
+        if (need_prop) ctl |= stop_rank0(C, pf);
+        if constexpr (kPrefetch) prefetch_ctl(pf, Gl);
       }
       ctl = g.bcast0(ctl);
       if (ctl & 2) hand_over(g, P, Gl, stk, nw, bot);
@@ -816,7 +858,7 @@ __global__ void __launch_bounds__(MaxThreads<G, F>::value, MaxThreads<G, F>::min
           if (remat) atomicAdd(&Gl->rematerialised, 1ull);
         }
         remat = false;
-        e = classify(g, S, f.T, L, C, cnt, failed, depth, lbw, mid);
+        e = classify(g, S, f.T, L, C, cnt, failed, depth, lbw, mid, pf);
       } else {
         e = branch(g, S, f.T, L, lbw, mid);
       }
@@ -846,7 +888,7 @@ __global__ void __launch_bounds__(MaxThreads<G, F>::value, MaxThreads<G, F>::min
         ++sp;
         ++depth;
         // rank 0 made the decision join and makes the objective join: one sync
-        dirty = word_bit(right_first ? lbw : lbw + 1) | join_objective(g, S, L, C);
+        dirty = word_bit(right_first ? lbw : lbw + 1) | join_objective(g, S, L, C, pf);
         g.sync();
         need_prop = true;
         continue;
@@ -864,7 +906,7 @@ __global__ void __launch_bounds__(MaxThreads<G, F>::value, MaxThreads<G, F>::min
       }
       depth = ent[nw + 2] + 1;
       dirty = word_bit(tag < 0 ? (tag & 0x7fffffff) + 1 : tag);
-      dirty |= join_objective(g, S, L, C);  // rank 0, after its decision join
+      dirty |= join_objective(g, S, L, C, pf);  // rank 0, after its decision join
       g.sync();
       need_prop = true;
     }
@@ -877,7 +919,10 @@ __global__ void __launch_bounds__(MaxThreads<G, F>::value, MaxThreads<G, F>::min
       break;
     }
   }
-  if (g.rank() == 0) flush(Gl, cnt);
+  if (g.rank() == 0) {
+    if (kPrefetch) prefetch_wait();  // no copy into shared memory outlives the CTA
+    flush(Gl, cnt);
+  }
 }
 
 }  // namespace dev
