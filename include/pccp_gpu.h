@@ -165,6 +165,7 @@ typedef struct pccp_stats {
                               the current bound, as solve_parallel's workers re-materialise their
                               subproblem roots (solver.cpp:266-268); distinct tree nodes = nodes -
                               rematerialised */
+  uint64_t stolen;      /* N linked shards: frontier subproblems this shard took from peers' shares */
 } pccp_stats;
 
 typedef struct pccp_enum_result {

@@ -83,6 +83,7 @@ class PccpStats(C.Structure):
         ("bfs_levels", C.c_uint64),
         ("donations", C.c_uint64),
         ("rematerialised", C.c_uint64),
+        ("stolen", C.c_uint64),
     ]
 
 

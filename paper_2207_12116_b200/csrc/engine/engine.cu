@@ -113,6 +113,7 @@ struct pccp_gpu_ctx {
   int store_stride = 4;
   int table_in_smem = 0;
   int ne_only = 0;  // lowered to NE records (and fold tells) only: the kNeOnly kernels
+  int packed_only = 0;  // packed reifications, unit records and word-parallel bit rows only: kPacked
   int dec_ctas = 0;  // grid of the persistent decomposition kernel
   long long plan_key = -1;  // last plan's (variant, block, smem) and its occupancies
   int plan_occ = 0, plan_occ_dec = 0;
@@ -123,8 +124,11 @@ struct pccp_gpu_ctx {
   DBuf<unsigned> rnd;
   dev::Globals* G = nullptr;
   std::vector<void*> opened;
-  DBuf<dev::Globals*> d_peers;  // peer contexts' globals (incumbent replicas, done flags)
+  DBuf<dev::Globals*> d_peers;  // peer contexts' globals (incumbent replicas, done flags, share cells)
+  DBuf<int> d_peer_shard;       // each peer's shard index
   int n_peers = 0;
+  unsigned epoch = 0;           // sharded searches with work stealing run so far (Globals::qcell tags)
+  DBuf<int> qlog;               // record_frontier in stealing searches: positions processed here
   // cfg.record_frontier: FNV hashes of the shared EPS frontier (phase A) and of
   // this shard's share of it, from the last search (pccp_gpu_frontier)
   std::vector<std::uint64_t> frontier_all, frontier_share;
@@ -187,7 +191,16 @@ template <class Fn>
 void dispatch(const pccp_gpu_ctx* c, Fn&& f) {
   using dev::kAllFamilies;
   using dev::kNeOnly;
-  if (c->warp && c->ne_only) {
+  using dev::kPacked;
+  if (c->packed_only) {
+    if (c->warp) {
+      if (c->table_in_smem) f.template operator()<dev::WarpGroup, true, kPacked>();
+      else f.template operator()<dev::WarpGroup, false, kPacked>();
+    } else {
+      if (c->table_in_smem) f.template operator()<dev::CtaGroup, true, kPacked>();
+      else f.template operator()<dev::CtaGroup, false, kPacked>();
+    }
+  } else if (c->warp && c->ne_only) {
     if (c->table_in_smem) f.template operator()<dev::WarpGroup, true, kNeOnly>();
     else f.template operator()<dev::WarpGroup, false, kNeOnly>();
   } else if (c->warp) {
@@ -217,7 +230,7 @@ void plan(pccp_gpu_ctx* c) {
       // from L2 (too large for shared memory) want more resident groups per
       // SM to hide that latency: 256 (RCPSP120: 6.95 M nodes/s at 256 threads,
       // 6.48 at 512, 5.34 at 1024, measured)
-      const size_t base1 = 72 * 4 + (size_t)c->store_stride * 4 + sizeof(dev::Cnt) + sizeof(dev::Pf);
+      const size_t base1 = dev::kFrameCtl * 4 + (size_t)c->store_stride * 4 + sizeof(dev::Cnt) + sizeof(dev::Pf);
       const bool l2_tables = base1 + (size_t)align4(L.hot_words) * 4 > 100 * 1024 && !std::getenv("PCCP_TABLE_SMEM");
       t = 128;
       while (t < (l2_tables ? 256 : 1024) && (std::uint32_t)(2 * t) <= L.n_ref_cmds / 16) t *= 2;
@@ -226,7 +239,7 @@ void plan(pccp_gpu_ctx* c) {
     c->gpc = 1;
     c->block = t;
   }
-  const size_t base = 72 * 4 + (size_t)(c->warp ? c->gpc : 1) *
+  const size_t base = dev::kFrameCtl * 4 + (size_t)(c->warp ? c->gpc : 1) *
                                    (c->store_stride * 4 + sizeof(dev::Cnt) + sizeof(dev::Pf));  // + per-group Cnt, Pf
   const size_t table = (size_t)align4(L.hot_words) * 4;  // the staged (hot) prefix of the tables
   if (base > c->smem_optin) throw LimitError("store of " + std::to_string(L.n_words) + " words exceeds shared memory");
@@ -234,6 +247,10 @@ void plan(pccp_gpu_ctx* c) {
                        !L.filtered && !std::getenv("PCCP_NO_NE_KERNEL")
                    ? 1
                    : 0;
+  c->packed_only = L.packed && L.reif8 && L.wrows && L.sc_in_rows && L.iv_prefix && !L.n_ne && !L.n_small &&
+                           !L.n_rows && !L.n_gen && !L.filtered && !std::getenv("PCCP_NO_PACKED_KERNEL")
+                       ? 1
+                       : 0;
   const char* env = std::getenv("PCCP_TABLE_SMEM");
   bool in_smem = base + table <= 100 * 1024;
   if (env) in_smem = std::atoi(env) != 0 && base + table <= c->smem_optin;
@@ -243,7 +260,7 @@ void plan(pccp_gpu_ctx* c) {
   int occ_dec = 0;
   // the attributes and occupancies depend only on (kernel variant, block,
   // smem): a reload of a model with the same plan reuses them
-  const long long key = ((long long)c->warp << 62) ^ ((long long)c->ne_only << 61) ^
+  const long long key = ((long long)c->warp << 62) ^ ((long long)c->ne_only << 61) ^ ((long long)c->packed_only << 59) ^
                         ((long long)c->table_in_smem << 60) ^ ((long long)c->block << 40) ^ (long long)c->smem;
   if (c->plan_key == key) {
     occ = c->plan_occ;
@@ -349,8 +366,10 @@ std::uint64_t host_store_hash(const std::int32_t* w, std::uint32_t n) {
 }
 
 // cfg.record_frontier: hashes of the frontier in (fa, ia) and of the share
-// i = shard (mod shards) this GPU keeps (tests of the partition).
-void record_frontier(pccp_gpu_ctx* c, int count, int stride, int shard, int shards) {
+// this GPU processes: positions i = shard (mod shards), or, with work
+// stealing, the positions it popped (`taken`, read after the search).
+void record_frontier(pccp_gpu_ctx* c, int count, int stride, int shard, int shards,
+                     const std::vector<int>* taken = nullptr) {
   const std::uint32_t nw = c->low.L.n_words;  // hashed in the reference layout
   std::vector<std::int32_t> ref(nw);
   std::vector<int> idx((size_t)count);
@@ -358,11 +377,18 @@ void record_frontier(pccp_gpu_ctx* c, int count, int stride, int shard, int shar
   std::vector<std::int32_t> st((size_t)c->fa.n);
   CK(cudaMemcpyAsync(st.data(), c->fa.p, c->fa.n * 4, cudaMemcpyDeviceToHost, c->stream));
   CK(cudaStreamSynchronize(c->stream));
+  std::vector<std::uint64_t> h((size_t)count);
   for (int i = 0; i < count; ++i) {
     to_reference(c->dl, st.data() + (size_t)idx[(size_t)i] * (size_t)stride, ref.data());
-    const std::uint64_t h = host_store_hash(ref.data(), nw);
-    c->frontier_all.push_back(h);
-    if (i % shards == shard) c->frontier_share.push_back(h);
+    h[(size_t)i] = host_store_hash(ref.data(), nw);
+  }
+  c->frontier_all.assign(h.begin(), h.end());
+  c->frontier_share.clear();
+  if (taken) {
+    for (int i : *taken)
+      if (i >= 0 && i < count) c->frontier_share.push_back(h[(size_t)i]);
+  } else {
+    for (int i = shard; i < count; i += shards) c->frontier_share.push_back(h[(size_t)i]);
   }
 }
 
@@ -380,6 +406,11 @@ void run_search(pccp_gpu_ctx* c, int mode, const int32_t* root_words, int depth_
   const int shard_count = sharded ? std::max(1, c->cfg.shard_count) : 1;
   const int shard_index = sharded ? c->cfg.shard_index : 0;
   if (shard_index < 0 || shard_index >= shard_count) throw ArgError("shard_index out of range");
+  // Linked shards steal from each other's shares of the shared phase-A
+  // frontier (search.cuh steal_pop); unlinked ones keep the static i mod N
+  // split and expand their share (phase B below).
+  const bool steal = shard_count > 1 && c->n_peers > 0 && !std::getenv("PCCP_NO_STEAL");
+  const unsigned epoch = steal ? ++c->epoch : 0u;
   const dev::Model M = c->model(var_order, var_seed, root_words, 1, (size_t)c->low.L.n_words);
   dev::SearchCtl C{};
   C.G = c->G;
@@ -558,7 +589,11 @@ void run_search(pccp_gpu_ctx* c, int mode, const int32_t* root_words, int depth_
   };
   c->frontier_all.clear();
   c->frontier_share.clear();
-  if (shard_count > 1) {
+  int steal_count = 0;  // stealing: the shared frontier's size (every position is popped once)
+  if (shard_count > 1 && steal) {
+    if (expand_until((int)target_a_ll) && count > 0) steal_count = count;
+    C.count = 1;  // the search below counts what this GPU processes
+  } else if (shard_count > 1) {
     if (expand_until((int)target_a_ll) && count > 0) {
       if (c->cfg.record_frontier) record_frontier(c, count, stride, shard_index, shard_count);
       const int mine = count > shard_index ? (count - shard_index + shard_count - 1) / shard_count : 0;
@@ -610,6 +645,20 @@ void run_search(pccp_gpu_ctx* c, int mode, const int32_t* root_words, int depth_
     P.value_order = c->cfg.value_order >= 0 ? std::min(c->cfg.value_order, 2) : 0;
     if (const char* vo = std::getenv("PCCP_VALUE_ORDER")) P.value_order = std::atoi(vo);
     P.waitq = c->waitq.p;
+    if (steal) {  // the whole shared frontier; positions come from the share cells
+      P.shard_index = shard_index;
+      P.shard_count = shard_count;
+      P.steal = 1;
+      P.epoch = epoch;
+      P.own_q = &c->G->qcell;
+      P.peers = c->d_peers.p;
+      P.peer_shard = c->d_peer_shard.p;
+      P.n_peers = c->n_peers;
+      if (c->cfg.record_frontier) {
+        c->qlog.ensure((size_t)count);
+        P.qlog = c->qlog.p;
+      }
+    }
     C.count = 1;
     if (C.audit_n > 0) dev::k_search<Gp, TS, F, true><<<c->ctas, c->block, c->smem, c->stream>>>(M, C, P);
     else dev::k_search<Gp, TS, F><<<c->ctas, c->block, c->smem, c->stream>>>(M, C, P);
@@ -621,6 +670,12 @@ void run_search(pccp_gpu_ctx* c, int mode, const int32_t* root_words, int depth_
   CK(cudaMemcpyAsync(&out.g, c->G, sizeof(dev::Globals), cudaMemcpyDeviceToHost, c->stream));
   CK(cudaStreamSynchronize(c->stream));
   out.d2h += sizeof(dev::Globals);
+  if (steal && c->cfg.record_frontier && steal_count > 0) {
+    std::vector<int> taken((size_t)std::min<unsigned long long>(out.g.qlog_n, (unsigned long long)steal_count));
+    if (!taken.empty())
+      CK(cudaMemcpy(taken.data(), c->qlog.p, taken.size() * 4, cudaMemcpyDeviceToHost));
+    record_frontier(c, steal_count, stride, shard_index, shard_count, &taken);
+  }
   out.launches = c->launches - launches0;
   out.levels = (std::uint64_t)level;
   // device time = root propagation (ev0..ev3) + decomposition and search (ev4..ev2)
@@ -682,6 +737,7 @@ void fill_stats(const pccp_gpu_ctx* c, const RunOut& r, pccp_stats& s) {
   s.bfs_levels = r.levels;
   s.donations = r.g.donations;
   s.rematerialised = r.g.rematerialised;
+  s.stolen = r.g.stolen;
 }
 
 // Counters of consecutive searches of one call (primal segments, exact
@@ -699,6 +755,7 @@ void merge_run(RunOut& acc, const RunOut& r, bool first) {
   g.max_depth = std::max(g.max_depth, acc.g.max_depth);
   g.donations += acc.g.donations;
   g.rematerialised += acc.g.rematerialised;
+  g.stolen += acc.g.stolen;
   acc.g = g;
   acc.bfs_rounds += r.bfs_rounds;
   acc.decompose_ms += r.decompose_ms;
@@ -802,6 +859,8 @@ void pccp_gpu_close(pccp_gpu_ctx* c) {
   c->st.release();
   c->rnd.release();
   c->d_peers.release();
+  c->d_peer_shard.release();
+  c->qlog.release();
   if (c->G) cudaFree(c->G);
   for (auto& e : c->ev)
     if (e) cudaEventDestroy(e);
@@ -1190,6 +1249,7 @@ int pccp_gpu_attach_peers(pccp_gpu_ctx* c, const uint8_t* handles, int32_t n, in
     if (!c || (n > 0 && !handles)) throw ArgError("null argument");
     CK(cudaSetDevice(c->device));
     std::vector<dev::Globals*> ptrs;
+    std::vector<int> shard;  // handle i belongs to shard i (distributed.attach_incumbents gathers by rank)
     for (int i = 0; i < n; ++i) {
       if (i == self) continue;
       cudaIpcMemHandle_t h;
@@ -1198,11 +1258,14 @@ int pccp_gpu_attach_peers(pccp_gpu_ctx* c, const uint8_t* handles, int32_t n, in
       CK(cudaIpcOpenMemHandle(&p, h, cudaIpcMemLazyEnablePeerAccess));
       c->opened.push_back(p);
       ptrs.push_back(static_cast<dev::Globals*>(p));
+      shard.push_back(i);
     }
     c->n_peers = (int)ptrs.size();
     if (!ptrs.empty()) {
       c->d_peers.ensure(ptrs.size());
       CK(cudaMemcpy(c->d_peers.p, ptrs.data(), ptrs.size() * sizeof(dev::Globals*), cudaMemcpyHostToDevice));
+      c->d_peer_shard.ensure(shard.size());
+      CK(cudaMemcpy(c->d_peer_shard.p, shard.data(), shard.size() * sizeof(int), cudaMemcpyHostToDevice));
     }
     return PCCP_OK;
   });
@@ -1273,6 +1336,7 @@ int pccp_gpu_link_peers(pccp_gpu_ctx* const* ctxs, int32_t n) {
       pccp_gpu_ctx* c = ctxs[i];
       CK(cudaSetDevice(c->device));
       std::vector<dev::Globals*> ptrs;
+      std::vector<int> shard;
       for (int j = 0; j < n; ++j) {
         if (j == i) continue;
         const int dj = ctxs[j]->device;
@@ -1285,11 +1349,14 @@ int pccp_gpu_link_peers(pccp_gpu_ctx* const* ctxs, int32_t n) {
           else CK(e);
         }
         ptrs.push_back(ctxs[j]->G);
+        shard.push_back(ctxs[j]->cfg.shard_index);
       }
       c->n_peers = (int)ptrs.size();
       if (!ptrs.empty()) {
         c->d_peers.ensure(ptrs.size());
         CK(cudaMemcpy(c->d_peers.p, ptrs.data(), ptrs.size() * sizeof(dev::Globals*), cudaMemcpyHostToDevice));
+        c->d_peer_shard.ensure(shard.size());
+        CK(cudaMemcpy(c->d_peer_shard.p, shard.data(), shard.size() * sizeof(int), cudaMemcpyHostToDevice));
       }
     }
     return PCCP_OK;

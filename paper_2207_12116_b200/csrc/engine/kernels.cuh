@@ -55,12 +55,24 @@ struct Globals {
   int best_lock;
   int best_value;
   int done;                        // a peer proved optimality over the whole tree: stop
+  // Cross-GPU work stealing (search.cuh steal_pop): this shard's share of the
+  // shared EPS frontier, popped as qcell = epoch << 32 | k (the k-th position
+  // of the share, shard + k * shards) with system-scope atomics by this GPU
+  // and, once their own share is exhausted, by its peers.  Kept across
+  // searches like the cells above (the epoch tags each sharded search); its
+  // own 128-byte line, away from the per-node reads of the cells above.
+  alignas(128) unsigned long long qcell;
+  unsigned long long qcell_pad[15];
   int n_impr;
   int impr_val[64];
   unsigned long long impr_ns[64];
   int error_code;
   // dynamic load balancing (search.cuh maybe_donate)
-  alignas(16) int hungry;       // idle groups waiting for a donation
+  // hungry is read by every busy group each node: its own 128-byte line,
+  // away from the idle groups' atomics on active / wait_* (sharing the line
+  // cost Q14 0.6%, measured); the prefetch copies its first 16 bytes
+  alignas(128) int hungry;      // idle groups waiting for a donation
+  int hungry_pad[31];
   int active;                   // groups exploring, or promised a donation
   unsigned wait_head, wait_tail;
   unsigned long long donations;
@@ -71,6 +83,8 @@ struct Globals {
   int stalled;
   unsigned long long audit_seen;   // materialisations offered to the node audit
   unsigned long long rematerialised;  // frontier nodes materialised again by the search (mode 1)
+  unsigned long long qlog_n;          // record_frontier: frontier positions this shard processed
+  unsigned long long stolen;          // frontier positions taken from peers' shares
 };
 
 __device__ __forceinline__ unsigned long long globaltimer() {
@@ -120,7 +134,7 @@ struct WarpGroup {
     any_fl = __any_sync(kFull, fl);
   }
   __device__ __forceinline__ bool any(bool p) const { return __any_sync(kFull, p); }
-  __device__ __forceinline__ unsigned long long min_u64(unsigned long long v) const {
+  __device__ __forceinline__ unsigned long long min_u64(unsigned long long v, int = 0) const {
     // all keys below 2^32 (small widths / bounds, or none): one redux.min
     if (__all_sync(kFull, (v >> 32) == 0ull || v == ~0ull)) {
       const unsigned m = __reduce_min_sync(kFull, v == ~0ull ? 0xffffffffu : (unsigned)v);
@@ -140,7 +154,7 @@ struct WarpGroup {
 struct CtaGroup {
   int tid, n;
   int* ring;                 // 4 ints of smem: 3-slot change ring + spare
-  unsigned long long* red;   // 33 u64 of smem
+  unsigned long long* red;   // 64 u64 of smem (two slots of 32 warps)
   __device__ __forceinline__ int rank() const { return tid; }
   __device__ __forceinline__ int size() const { return n; }
   __device__ __forceinline__ int warp() const { return tid >> 5; }
@@ -161,7 +175,7 @@ struct CtaGroup {
     any_ch = *(volatile int*)&ring[i % 3] != 0;
   }
   __device__ __forceinline__ bool any(bool p) const { return __syncthreads_or(p) != 0; }
-  __device__ __forceinline__ unsigned long long min_u64(unsigned long long v) const {
+  __device__ __forceinline__ unsigned long long min_u64(unsigned long long v, int = 0) const {
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) {
       const unsigned long long u = __shfl_xor_sync(kFull, v, o);
@@ -520,11 +534,19 @@ __device__ __forceinline__ void sred_or(unsigned a, unsigned v) {
 // sp is the shared address of plane pair 0.  lb b = LB bit, ub b = 1 - UB bit;
 // the joins b <- 1 / b <- 0 set the LB / UB bit (red.or), the only moves a
 // 0/1 cell has (nlb > lb only for nlb = 1, lb = 0; nub < ub only for 0 < 1).
-template <bool Fast>
+// Even: x's and y's lb words are even (kPacked: every interval sits at words
+// [0, 2 n_iv)), so each (lb, ub) pair is one 8-byte load.
+template <bool Fast, bool Even = false>
 __device__ __forceinline__ bool eval_reif_bits(unsigned sb, unsigned sp, int4 r) {
   const unsigned ax = sb + (((unsigned)r.x & 0xffffu) << 2), ay = sb + (((unsigned)r.x >> 16) << 2);
   const unsigned bit = (unsigned)r.y, ap = sp + ((bit >> 5) << 3), mk = 1u << (bit & 31u);
-  const int lx = sld(ax), ux = sld(ax + 4), ly = sld(ay), uy = sld(ay + 4);
+  int lx, ux, ly, uy;
+  if constexpr (Even) {
+    const int2 X = sld2(ax), Y = sld2(ay);
+    lx = X.x, ux = X.y, ly = Y.x, uy = Y.y;
+  } else {
+    lx = sld(ax), ux = sld(ax + 4), ly = sld(ay), uy = sld(ay + 4);
+  }
   const int2 P = sld2(ap);
   const int lb = ((unsigned)P.x & mk) ? 1 : 0, ub = ((unsigned)P.y & mk) ? 0 : 1;
   int nlb, nub, nux, nly, nuy, nlx;
@@ -839,12 +861,16 @@ __device__ __forceinline__ unsigned coef_gt(const int4& P, int thr) {  // terms 
   return gt;
 }
 
+// `rank` may be a rotation of g.rank() by a multiple of 32 (lane groups stay
+// aligned for the shuffles).  fl: set when a row is (or becomes) overloaded —
+// its lsum cell is (or is joined to) top, the failure the scan would find
+// next (kPacked kernels skip the scalar scan: every scalar is such a cell).
 template <class G, bool TS>
-__device__ bool eval_wrows(const G& g, unsigned sb, const Tab<TS>& tab, const DeviceLayout& L) {
+__device__ bool eval_wrows(const G& g, unsigned sb, const Tab<TS>& tab, const DeviceLayout& L, int rank, bool& fl) {
   const int lg = (int)L.wrow_lg, Q = 1 << lg;
-  const int q = g.rank() & (Q - 1);
+  const int q = rank & (Q - 1);
   const int per_pass = g.size() >> lg;
-  const int my = g.rank() >> lg;
+  const int my = rank >> lg;
   const int n_rows = (int)L.n_brows;
   const unsigned sp = sb + 4u * L.plane;
   unsigned ch = 0;
@@ -873,6 +899,7 @@ __device__ bool eval_wrows(const G& g, unsigned sb, const Tab<TS>& tab, const De
         sred_max(alsum, cell);
         ch = 1u;
       }
+      if (q == 0 && (over || lsum_now == INT_MAX)) fl = true;
       if (c != INT_MAX && P.x) {
         const unsigned z = (over ? (unsigned)P.x : coef_gt(P, c - s) & ~lbw) & ~ubw;
         if (z) {
@@ -1038,7 +1065,10 @@ __device__ __forceinline__ bool eval_other_families(const G& g, volatile int* S,
     for (int i = g.rank(); i < (int)L.n_small; i += g.size()) ch |= eval_small(S, T, L, i);
     dbg_r(2);
     if (L.n_rows) ch |= eval_rows(g, sb, tab, L);
-    if (L.n_brows) ch |= L.wrows ? eval_wrows(g, sb, tab, L) : eval_brows(g, sb, tab, L);
+    if (L.n_brows) {
+      bool fl_unused = false;  // the scalar scan finds overloaded rows here
+      ch |= L.wrows ? eval_wrows(g, sb, tab, L, g.rank(), fl_unused) : eval_brows(g, sb, tab, L);
+    }
     dbg_r(3);
     for (int i = g.rank(); i < (int)L.n_gen; i += g.size())
       ch |= eval_generic(S, T + L.gen_code + T[L.gen_off + i]);
@@ -1047,8 +1077,61 @@ __device__ __forceinline__ bool eval_other_families(const G& g, volatile int* S,
 
 // F selects the command families compiled into the loop: kAllFamilies, or
 // kNeOnly for models lowered to NE records alone (N-Queens): a smaller
-// kernel, fewer registers, more resident groups (engine.cu dispatch).
-constexpr int kAllFamilies = 0, kNeOnly = 1;
+// kernel, fewer registers, more resident groups (engine.cu dispatch); or
+// kPacked for packed models made of 8-byte bit reifications, unit records and
+// word-parallel bit rows only, whose scalars are all row sums (RCPSP).
+constexpr int kAllFamilies = 0, kNeOnly = 1, kPacked = 2;
+
+// One round of a kPacked model.  The reifications go from rank 0 up; unit
+// records, rows and the scans from the last warp down (a rotation by whole
+// warps), so the warps carrying one reification more than the others are
+// not the ones carrying the rows.  Failure: the start intervals (the words
+// [0, 2 n_iv)), the bit planes, and overloaded rows (eval_wrows).
+template <class G, bool TS>
+__device__ __forceinline__ bool packed_round(const G& g, unsigned sb, const Tab<TS>& tab, const DeviceLayout& L,
+                                             bool& fl) {
+  const unsigned sp = sb + 4u * L.plane;
+  auto rec = [&](int i) {
+    const int2 q = tab.ld2(L.reif, i);
+    return make_int4(q.x, q.y & 0x3ffff, (q.y << 7) >> 25, q.y >> 25);
+  };
+  bool ch = false;
+  if (L.reif_fast) {
+    for (int i = g.rank(); i < (int)L.n_reif; i += g.size()) ch |= eval_reif_bits<true, true>(sb, sp, rec(i));
+  } else {
+    for (int i = g.rank(); i < (int)L.n_reif; i += g.size()) ch |= eval_reif_bits<false, true>(sb, sp, rec(i));
+  }
+  const int rr = (g.size() - 32 * (g.rank() >> 5 ) - 32) + (g.rank() & 31);  // warps in reverse order
+  if (L.unit_fast) {
+    unsigned uch = 0;
+    const int2 none = make_int2(0, INT_MAX);
+    for (int i = rr; i < (int)L.n_unit1; i += g.size()) eval_unit_fast(sb, tab.ld4(L.unit1, i), none, uch);
+    for (int i = rr; i < (int)L.n_unit2; i += g.size()) eval_unit_fast(sb, tab.ld4(L.unit2, i), tab.ld2(L.unit2g, i), uch);
+    ch |= uch != 0;
+  } else {
+    for (int i = rr; i < (int)L.n_unit1; i += g.size()) {
+      const int4 q = tab.ld4(L.unit1, i);
+      if (unit_guard(sb, q.x, q.y)) ch |= unit_tell(sb, q.z, q.w);
+    }
+    for (int i = rr; i < (int)L.n_unit2; i += g.size()) {
+      const int4 q = tab.ld4(L.unit2, i);
+      if (unit_guard(sb, q.x, q.y)) {
+        const int2 q2 = tab.ld2(L.unit2g, i);
+        if (unit_guard(sb, q2.x, q2.y)) ch |= unit_tell(sb, q.z, q.w);
+      }
+    }
+  }
+  ch |= eval_wrows(g, sb, tab, L, rr, fl);
+  for (int i = rr; i < (int)L.n_iv; i += g.size()) {
+    const int2 v = sld2(sb + 8u * (unsigned)i);
+    fl |= v.x > v.y;
+  }
+  for (int i = rr; i < (int)L.n_pairs; i += g.size()) {
+    const int2 P = sld2(sp + 8u * (unsigned)i);
+    fl |= (P.x & P.y) != 0;
+  }
+  return ch;
+}
 
 template <class G, bool TS, int F = kAllFamilies>
 __device__ bool propagate(const G& g, volatile int* S, unsigned sb, const Tab<TS>& tab, const DeviceLayout& L,
@@ -1061,7 +1144,11 @@ __device__ bool propagate(const G& g, volatile int* S, unsigned sb, const Tab<TS
   int r = 0;
   bool failed = false;
   for (;;) {
-    bool ch = ne_round(g, sb, tab, L), fl = false;
+    bool ch, fl = false;
+    if constexpr (F == kPacked) {
+      ch = packed_round(g, sb, tab, L, fl);
+    } else {
+    ch = ne_round(g, sb, tab, L);
     if constexpr (F == kAllFamilies) ch |= eval_other_families(g, S, sb, tab, L);
     // The scan may see an intermediate state: failure is monotone, and a join
     // after it changed a word, so the next round scans again (H8).
@@ -1101,6 +1188,7 @@ __device__ bool propagate(const G& g, volatile int* S, unsigned sb, const Tab<TS
           fl |= (P.x & P.y) != 0;
         }
     }
+    }  // F != kPacked
     dbg_r(4);
     bool any_ch, any_fl;
     g.round_end(ch, fl, any_ch, any_fl, r);
@@ -1154,7 +1242,7 @@ __device__ int branch(const G& g, volatile int* S, const int* __restrict__ T, co
       const unsigned long long k = (unsigned)lo ^ 0x80000000u;
       if (lo < hi && k < m) m = k;
     }
-    m = g.min_u64(m);
+    m = g.min_u64(m, 1);
     if (m == ~0ull) return 0;
     const unsigned salt = mix24(L.var_seed * 0x9e3779b9u + g.uid()) << 8;
     for (int i = g.rank(); i < (int)L.n_cand; i += g.size()) {

@@ -1255,6 +1255,13 @@ Lowered lower_impl(const pccp_model& m, bool want_bits) {
     if (iv[i] != static_cast<std::int32_t>(2 * i)) L.iv_prefix = 0;
   L.iv_dense = !packed && L.iv_prefix && L.n_iv * 2 == m.n_words ? 1 : 0;
   L.n_sc = static_cast<std::uint32_t>(scw.size());
+  if (L.wrows) {  // a row's lsum is private to it (match_row): overload is its only way to top
+    std::vector<std::uint8_t> is_lsum(DW + 1, 0);
+    for (const Row& r : bit_rows) is_lsum[r.lsum] = 1;
+    L.sc_in_rows = 1;
+    for (std::int32_t w : scw)
+      if (!is_lsum[static_cast<std::uint32_t>(w)]) L.sc_in_rows = 0;
+  }
   L.sc_w = reserve_arr(L.n_sc);
   L.sc_top = reserve_arr(L.n_sc);
   std::copy(scw.begin(), scw.end(), B.begin() + L.sc_w);

@@ -104,6 +104,7 @@ struct DeviceLayout {
   std::uint32_t wrows, wrow_lg;
   std::uint32_t wrow_meta;    // int4 per row: {first chunk (int4 index into wpat), c, lsum word, first bit}
   std::uint32_t wpat;         // int4 per chunk: {term mask, coefficient bit-planes 0, 1, 2}
+  std::uint32_t sc_in_rows;   // every scalar slot is the lsum cell of a word-parallel bit row
 };
 
 

@@ -64,7 +64,7 @@ __device__ __forceinline__ unsigned long long word_bit(int w) { return w < 64 ? 
 // only a weaker bound (`own` keeps the group's own improvements exact).
 struct alignas(16) Pf {
   int ctl[4];   // cursor, stop, incomplete, incumbent
-  int hung[4];  // hungry, active, wait_head, wait_tail
+  int hung[4];  // hungry, padding
   int own;      // best value this group recorded (INT_MAX: none)
   int pad[3];
 };
@@ -198,14 +198,18 @@ __device__ void record_solution(const G& g, volatile int* S, const DeviceLayout&
 
 // After a node's fixed point: count, hash, classify.  Returns 1 when the node
 // must be expanded (lbw/mid set), 0 when it is a leaf, -1 on a model error.
-template <class G>
+template <int F = kAllFamilies, class G>
 __device__ int classify(const G& g, volatile int* S, const int* __restrict__ T, const DeviceLayout& L,
                         const SearchCtl& C, Cnt& cnt, bool failed, int depth, int& lbw, int& mid, Pf* pf = nullptr) {
   if (failed) {
     if (C.count && g.rank() == 0) ++cnt.fails;
     return 0;
   }
-  if (C.hash && C.count && g.rank() == 0) cnt.hash += store_hash_ref(S, C.blob, L);
+  if (C.hash && C.count && g.rank() == 0) {
+    // NE-only models are never packed: keep the decoding hash out of that kernel
+    if constexpr (F == kNeOnly) cnt.hash += store_hash(S, (int)L.n_words);
+    else cnt.hash += store_hash_ref(S, C.blob, L);
+  }
   const int b = branch(g, S, T, L, lbw, mid);
   if (b < 0) {
     if (g.rank() == 0) {
@@ -227,6 +231,7 @@ __device__ int classify(const G& g, volatile int* S, const int* __restrict__ T, 
 }
 
 // Kernel prologue: optional smem copy of the tables, CTA scratch, group store.
+constexpr int kFrameCtl = 4 + 2 * 64;  // ints: the 4-int ring + 64 u64 of reduction slots
 struct Frame {
   const int* __restrict__ T;
   int* ring;
@@ -277,7 +282,7 @@ __device__ __forceinline__ Frame frame(const Model& M) {
   }
   f.ring = smem + off;
   f.red = reinterpret_cast<unsigned long long*>(smem + off + 4);
-  off += 72;
+  off += kFrameCtl;
   f.cnt = reinterpret_cast<Cnt*>(smem + off);
   for (int i = threadIdx.x; i < M.cnt_slots * (int)(sizeof(Cnt) / 8); i += blockDim.x)
     reinterpret_cast<unsigned long long*>(f.cnt)[i] = 0ull;
@@ -398,7 +403,7 @@ __global__ void __launch_bounds__(MaxThreads<G, F>::value, MaxThreads<G, F>::min
     cnt.rounds += (unsigned long long)r;
   }
   int lbw = 0, mid = 0;
-  const int e = classify(g, S, f.T, M.L, C, cnt, failed, 0, lbw, mid);
+  const int e = classify<F>(g, S, f.T, M.L, C, cnt, failed, 0, lbw, mid);
   copy_out(g, store, S, (int)M.L.n_words);
   if (g.rank() == 0) {
     *flag = e == 1 ? 1 : 0;
@@ -500,7 +505,7 @@ __device__ void expand_level(const G& g, volatile int* S, unsigned sb, const Tab
           if ((unsigned long long)child_depth > cnt.maxd) cnt.maxd = (unsigned long long)child_depth;
         }
         int clbw, cmid;
-        const int e = classify(g, S, f.T, L, C, cnt, failed, child_depth, clbw, cmid);
+        const int e = classify<F>(g, S, f.T, L, C, cnt, failed, child_depth, clbw, cmid);
         dbg_mark(5 + 5 * side);
         if (e == 1) {
           copy_out(g, children + (size_t)(2 * p + side) * stride, S, (int)L.n_words);
@@ -668,7 +673,56 @@ struct SearchParams {
   int* waitq;        // ring of idle group ids (-1: empty)
   int n_groups;
   int value_order;   // 0 left first, 1 right first, 2 odd groups right first
+  // cross-GPU work stealing (steal_pop): frontier = the shared phase-A
+  // frontier of all shards, this shard's share popped from own_q, then peers'
+  int steal;
+  unsigned epoch;
+  unsigned long long* own_q;
+  Globals* const* peers;   // peer contexts' globals (their qcells)
+  const int* peer_shard;   // each peer's shard index
+  int n_peers;
+  int* qlog;               // record_frontier: the positions this shard processed (or null)
 };
+
+// Pop from an epoch-tagged share cell (Globals::qcell): k < n_share of this
+// epoch, or -1.  A cell still tagged with an older epoch (its owner has not
+// started this search) gets this epoch installed by whoever comes first — the
+// owner or a thief — with position 0 going to the installer; every position
+// of an epoch is handed out once, whoever pops it.  Linked shards run the
+// same sequence of sharded searches (epochs 1, 2, ...), on the same root.
+__device__ __forceinline__ long long qpop(unsigned long long* q, unsigned e, long long n_share) {
+  for (;;) {
+    const unsigned long long v = atomicAdd_system(q, 1ull);
+    const unsigned ep = (unsigned)(v >> 32);
+    if (ep == e) return (long long)(unsigned)v < n_share ? (long long)(unsigned)v : -1;
+    if (ep > e) return -1;  // a later search owns the cell: this one's share was handed out
+    unsigned long long cur = v + 1;
+    while ((unsigned)(cur >> 32) < e) {
+      const unsigned long long prev = atomicCAS_system(q, cur, ((unsigned long long)e << 32) | 1ull);
+      if (prev == cur) return 0;
+      cur = prev;
+    }
+  }
+}
+
+// The next frontier position for a group of this shard: its own share first,
+// then the peers' shares (work stealing: a GPU that drained its share takes
+// positions another GPU has not reached yet).  -1 when all are handed out.
+__device__ __forceinline__ long long steal_pop(const SearchParams& P, Globals* Gl) {
+  const long long N = P.shard_count, n = P.n_frontier;
+  auto share = [&](long long s) { return n > s ? (n - s + N - 1) / N : 0ll; };
+  long long k = qpop(P.own_q, P.epoch, share(P.shard_index));
+  if (k >= 0) return P.shard_index + k * N;
+  for (int j = 0; j < P.n_peers; ++j) {
+    const int s = P.peer_shard[j];
+    k = qpop(&P.peers[j]->qcell, P.epoch, share(s));
+    if (k >= 0) {
+      atomicAdd(&Gl->stolen, 1ull);
+      return s + k * N;
+    }
+  }
+  return -1;
+}
 
 // A pending stack entry stores (parent fixed point, lbw | pending_left << 31,
 // mid, depth); apply its pending branch to a store.
@@ -724,6 +778,22 @@ __device__ __forceinline__ void hand_over(const G& g, const SearchParams& P, Glo
   ++bot;
 }
 
+// Rank 0's control for the next node of a CTA group: claim (bit 1), stop
+// (bit 0), from the prefetched control words, then the next prefetch.
+__device__ __forceinline__ int node_ctl_rank0(const SearchCtl& C, const SearchParams& P, Globals* Gl, Pf* pf,
+                                              int pending, bool need_prop) {
+  int c = 0;
+  prefetch_wait();
+  if (P.balance && pending >= P.balance) c |= claim_donation_rank0(Gl, pf) << 1;
+  if (need_prop) c |= stop_rank0(C, pf);
+  prefetch_ctl(pf, Gl);
+  return c;
+}
+
+#ifndef PCCP_CTL_MERGE
+#define PCCP_CTL_MERGE 1
+#endif
+
 // ---- K4 + K6: persistent DFS over the EPS work queue ------------------------------
 // Each group pops subproblem k (this GPU owns frontier i = shard_index +
 // k*shard_count) and explores it depth-first, left branch first (dfs,
@@ -749,6 +819,7 @@ __global__ void __launch_bounds__(MaxThreads<G, F>::value, MaxThreads<G, F>::min
   // node's first barrier; a warp group's wait is hidden by the SM's other
   // warps, and the extra instructions cost the issue-bound Q14 kernel 4%
   constexpr bool kPrefetch = std::is_same<G, CtaGroup>::value;
+  constexpr bool kMerge = kPrefetch && PCCP_CTL_MERGE;  // the control of the next node before the last barrier
   Pf* pf = kPrefetch ? f.pf + GroupOf<G>::in_cta() : nullptr;
   if (kPrefetch && g.rank() == 0) prefetch_ctl(pf, Gl);
   bool queue_open = true;
@@ -758,10 +829,18 @@ __global__ void __launch_bounds__(MaxThreads<G, F>::value, MaxThreads<G, F>::min
     bool need_prop = C.mode == 1;
     unsigned long long dirty = 0;  // words changed since the store was last a fixed point
     if (queue_open) {
-      int k = 0;
-      if (g.rank() == 0) k = (int)atomicAdd(&Gl->cursor, 1u);
-      k = g.bcast0(k);
-      const long long idx = (long long)P.shard_index + (long long)k * (long long)P.shard_count;
+      long long idx = 0;
+      if (g.rank() == 0) {
+        if (P.steal) {
+          idx = steal_pop(P, Gl);
+          if (idx < 0) idx = P.n_frontier;
+          else if (P.qlog) P.qlog[atomicAdd(&Gl->qlog_n, 1ull)] = (int)idx;
+        } else {
+          idx = (long long)P.shard_index + (long long)atomicAdd(&Gl->cursor, 1u) * (long long)P.shard_count;
+        }
+        if (idx > P.n_frontier) idx = P.n_frontier;
+      }
+      idx = g.bcast0((int)idx);
       if (idx >= P.n_frontier) queue_open = false;
       else {
         int stop = 0;
@@ -814,17 +893,32 @@ __global__ void __launch_bounds__(MaxThreads<G, F>::value, MaxThreads<G, F>::min
       dirty |= join_objective(g, S, L, C);
       g.sync();
     }
+    // Rank 0's per-node control (donation claim, limit checks) from the
+    // control words prefetched when the previous node started.  CTA groups
+    // compute it at the end of the previous node, before that node's last
+    // barrier, and publish it in shared memory (pf->pad[0]): no broadcast of
+    // its own (two barriers per node fewer).
+    bool ctl_ready = false;
     for (;;) {
-      // one broadcast per node for the donation claim and the limit checks,
-      // from the control words prefetched when the previous node started
       int ctl = 0;
-      if (g.rank() == 0) {
-        if constexpr (kPrefetch) prefetch_wait();
-        if (P.balance && sp - bot >= P.balance) ctl |= claim_donation_rank0(Gl, pf) << 1;
-        if (need_prop) ctl |= stop_rank0(C, pf);
-        if constexpr (kPrefetch) prefetch_ctl(pf, Gl);
+      if constexpr (kMerge) {
+        if (ctl_ready) {
+          ctl = *(volatile int*)&pf->pad[0];
+        } else {
+          if (g.rank() == 0) ctl = node_ctl_rank0(C, P, Gl, pf, sp - bot, need_prop);
+          ctl = g.bcast0(ctl);
+        }
+        ctl_ready = false;
+      } else if constexpr (kPrefetch) {
+        if (g.rank() == 0) ctl = node_ctl_rank0(C, P, Gl, pf, sp - bot, need_prop);
+        ctl = g.bcast0(ctl);
+      } else {
+        if (g.rank() == 0) {
+          if (P.balance && sp - bot >= P.balance) ctl |= claim_donation_rank0(Gl, pf) << 1;
+          if (need_prop) ctl |= stop_rank0(C, pf);
+        }
+        ctl = g.bcast0(ctl);
       }
-      ctl = g.bcast0(ctl);
       if (ctl & 2) hand_over(g, P, Gl, stk, nw, bot);
       int lbw = 0, mid = 0, e;
       if (need_prop) {
@@ -858,7 +952,7 @@ __global__ void __launch_bounds__(MaxThreads<G, F>::value, MaxThreads<G, F>::min
           if (remat) atomicAdd(&Gl->rematerialised, 1ull);
         }
         remat = false;
-        e = classify(g, S, f.T, L, C, cnt, failed, depth, lbw, mid, pf);
+        e = classify<F>(g, S, f.T, L, C, cnt, failed, depth, lbw, mid, pf);
       } else {
         e = branch(g, S, f.T, L, lbw, mid);
       }
@@ -889,8 +983,12 @@ __global__ void __launch_bounds__(MaxThreads<G, F>::value, MaxThreads<G, F>::min
         ++depth;
         // rank 0 made the decision join and makes the objective join: one sync
         dirty = word_bit(right_first ? lbw : lbw + 1) | join_objective(g, S, L, C, pf);
-        g.sync();
         need_prop = true;
+        if constexpr (kMerge) {
+          if (g.rank() == 0) pf->pad[0] = node_ctl_rank0(C, P, Gl, pf, sp - bot, true);
+          ctl_ready = true;
+        }
+        g.sync();
         continue;
       }
       if (sp == bot) break;
@@ -907,8 +1005,12 @@ __global__ void __launch_bounds__(MaxThreads<G, F>::value, MaxThreads<G, F>::min
       depth = ent[nw + 2] + 1;
       dirty = word_bit(tag < 0 ? (tag & 0x7fffffff) + 1 : tag);
       dirty |= join_objective(g, S, L, C, pf);  // rank 0, after its decision join
-      g.sync();
       need_prop = true;
+      if constexpr (kMerge) {
+        if (g.rank() == 0) pf->pad[0] = node_ctl_rank0(C, P, Gl, pf, sp - bot, true);
+        ctl_ready = true;
+      }
+      g.sync();
     }
     if (g.rank() == 0) {
       if (abandoned) Gl->incomplete = 1;

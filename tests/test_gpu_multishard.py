@@ -190,3 +190,53 @@ def test_sharded_micro_rcpsp_optima(n_shards):
             assert comb["status"] == "UNSAT"
         else:
             assert comb["status"] == "OPTIMAL" and comb["objective"] == bf, (rec, comb)
+
+
+# ---- cross-GPU work stealing -----------------------------------------------------
+# Linked shards pop their share of the shared phase-A frontier from an
+# epoch-tagged cell and, once it is exhausted, take positions from the peers'
+# cells (search.cuh steal_pop).  Run one after the other, shard 0 finds every
+# peer share untouched and drains all of them: no shard waits while another
+# share still has subproblems, and every position is processed exactly once.
+@pytest.mark.parametrize("n_shards", [2, 4])
+def test_linked_enumeration_steals_and_stays_exact(n_shards, golden):
+    import numpy as np
+
+    from paper_2207_12116_b200 import Engine, Model
+    from paper_2207_12116_b200.distributed import combine_enum
+    from paper_2207_12116_b200.engine import link_peers
+    for name, depth in (("nqueens10", -1), ("csp1", 12)):
+        m = Model.nqueens(10) if name == "nqueens10" else Model.random_csp(1)
+        g = golden[name]["enumerate" if depth < 0 else "enumerate_d12"]
+        engs = [Engine(0, shard_index=k, shard_count=n_shards, hash=True, record_frontier=True) for k in range(n_shards)]
+        try:
+            for e in engs:
+                e.load(m)
+            link_peers(engs)
+            for rep in range(2):  # a second sharded search on the same contexts (epoch 2)
+                parts, fronts = [], []
+                for e in engs:
+                    parts.append(e.enumerate(depth_cap=depth))
+                    fronts.append(e.frontier())
+                tot = combine_enum(parts)
+                for key in ("nodes", "failures", "solutions", "open_leaves", "hash_sum"):
+                    assert tot[key] == g[key], (name, n_shards, rep, key)
+                assert tot["exhausted"]
+                _check_partition(fronts)
+                assert parts[0]["stolen"] > 0 and fronts[0][1].size == fronts[0][0].size, (name, rep)
+                assert all(f[1].size == 0 for f in fronts[1:])  # nothing was left for the later shards
+        finally:
+            for e in engs:
+                e.close()
+
+
+def test_unlinked_shards_keep_the_static_split(golden):
+    """Without peers there is nothing to steal from: shard k processes the
+    positions k mod N of the frontier, as before."""
+    from paper_2207_12116_b200 import Engine, Model
+    m = Model.nqueens(10)
+    for k in range(3):
+        with Engine(0, shard_index=k, shard_count=3, record_frontier=True) as e:
+            r = e.load(m).enumerate()
+            a, s = e.frontier()
+            assert r["stolen"] == 0 and s.size == len(range(k, a.size, 3))
