@@ -540,6 +540,9 @@ def main():
     model = build_model(w)
     tables = model.tables()
     eng = Engine(local, shard_index=rank, shard_count=world)
+    if world > 1:  # linked shards: the share cells (work stealing) and the incumbent, over IPC
+        from paper_2207_12116_b200.distributed import attach_incumbents
+        attach_incumbents(eng)
     flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.int32, device=f"cuda:{local}")
 
     def step():
@@ -597,6 +600,8 @@ def main():
     parity = {k: counts[k] == exp[k] for k in counts if k in exp}
     if "hash_sum" in exp:
         heng = Engine(local, shard_index=rank, shard_count=world, hash=True)
+        if world > 1:
+            attach_incumbents(heng)
         hr = heng.load(tables).enumerate(depth_cap=w["depth"])
         hs = int(hr["hash_sum"])
         if world > 1:

@@ -114,6 +114,7 @@ struct pccp_gpu_ctx {
   int table_in_smem = 0;
   int ne_only = 0;  // lowered to NE records (and fold tells) only: the kNeOnly kernels
   int packed_only = 0;  // packed reifications, unit records and word-parallel bit rows only: kPacked
+  int packed_filter = 0;  // ... with filtered rounds (kPackedF)
   int dec_ctas = 0;  // grid of the persistent decomposition kernel
   long long plan_key = -1;  // last plan's (variant, block, smem) and its occupancies
   int plan_occ = 0, plan_occ_dec = 0;
@@ -135,6 +136,11 @@ struct pccp_gpu_ctx {
   std::uint64_t launches = 0;
 
   int groups() const { return ctas * (warp ? gpc : 1); }
+  // Per group: three dirty masks of (starts + plane words) bits, in ints (x4 for alignment).
+  int dm_words() const {
+    const DeviceLayout& L = dl.L;
+    return (int)align4(3u * ((L.n_iv + 31) / 32 + (L.n_pairs + 31) / 32));
+  }
 
   // Per-launch layout: branching order, and the value-range analyses of the
   // input stores (lower.cpp fast_paths) that admit the 32-bit
@@ -155,6 +161,12 @@ struct pccp_gpu_ctx {
     M.table_in_smem = table_in_smem;
     M.store_stride = store_stride;
     M.cnt_slots = warp ? gpc : 1;
+    // filtered kPacked rounds (kernels.cuh propagate_packed); PCCP_EVENTLESS=1
+    // keeps the eventless loop (every record every round)
+    M.L.dm_s = (dl.L.n_iv + 31) / 32;
+    M.L.dm_p = (dl.L.n_pairs + 31) / 32;
+    M.L.pfilter = packed_filter ? 1u : 0u;
+    M.dm_words = packed_filter ? dm_words() : 0;
     return M;
   }
 };
@@ -192,7 +204,11 @@ void dispatch(const pccp_gpu_ctx* c, Fn&& f) {
   using dev::kAllFamilies;
   using dev::kNeOnly;
   using dev::kPacked;
-  if (c->packed_only) {
+  using dev::kPackedF;
+  if (c->packed_only && c->packed_filter) {  // CTA groups only (plan)
+    if (c->table_in_smem) f.template operator()<dev::CtaGroup, true, kPackedF>();
+    else f.template operator()<dev::CtaGroup, false, kPackedF>();
+  } else if (c->packed_only) {
     if (c->warp) {
       if (c->table_in_smem) f.template operator()<dev::WarpGroup, true, kPacked>();
       else f.template operator()<dev::WarpGroup, false, kPacked>();
@@ -215,11 +231,27 @@ void dispatch(const pccp_gpu_ctx* c, Fn&& f) {
 void plan(pccp_gpu_ctx* c) {
   const DeviceLayout& L = c->dl.L;
   c->store_stride = (int)align4(L.n_words + 1);  // + the constant-zero word
+  c->packed_only = L.packed && L.reif8 && L.wrows && L.sc_in_rows && L.iv_prefix && !L.n_ne && !L.n_small &&
+                           !L.n_rows && !L.n_gen && !L.filtered && !std::getenv("PCCP_NO_PACKED_KERNEL")
+                       ? 1
+                       : 0;
+  // Filtered rounds (kPackedF) for packed models whose tables stream from L2
+  // (RCPSP120), CTA groups; PCCP_PACKED_FILTER=0/1 forces the choice.
+  {
+    const size_t hot = (size_t)align4(L.hot_words) * 4;
+    bool f = c->packed_only && L.rfilt && hot > 96 * 1024;
+    if (const char* pf = std::getenv("PCCP_PACKED_FILTER")) f = c->packed_only && L.rfilt && std::atoi(pf) != 0;
+    c->packed_filter = f ? 1 : 0;
+  }
+  // per group in shared memory: the store, counters, control prefetch, dirty masks
+  const size_t per_group = (size_t)c->store_stride * 4 + sizeof(dev::Cnt) + sizeof(dev::Pf) +
+                           (c->packed_filter ? (size_t)c->dm_words() * 4 : 0);
   const int gt = c->cfg.group_threads;
   // warp groups for small models: judged on the reference store (a packed
   // RCPSP30 store is 256 words, but its 14k commands want a CTA per node:
   // warp groups explored 12x the nodes and took 13x longer, measured)
   c->warp = gt == 32 || (gt == 0 && (L.packed ? L.ref_words : L.n_words) <= 256);
+  if (c->warp) c->packed_filter = 0;  // kPackedF has CTA groups only
   if (c->warp) {
     c->gpc = c->cfg.groups_per_cta > 0 ? std::min(c->cfg.groups_per_cta, 8) : 8;  // MaxThreads<WarpGroup>
     c->block = 32 * c->gpc;
@@ -230,7 +262,7 @@ void plan(pccp_gpu_ctx* c) {
       // from L2 (too large for shared memory) want more resident groups per
       // SM to hide that latency: 256 (RCPSP120: 6.95 M nodes/s at 256 threads,
       // 6.48 at 512, 5.34 at 1024, measured)
-      const size_t base1 = dev::kFrameCtl * 4 + (size_t)c->store_stride * 4 + sizeof(dev::Cnt) + sizeof(dev::Pf);
+      const size_t base1 = dev::kFrameCtl * 4 + per_group;
       const bool l2_tables = base1 + (size_t)align4(L.hot_words) * 4 > 100 * 1024 && !std::getenv("PCCP_TABLE_SMEM");
       t = 128;
       while (t < (l2_tables ? 256 : 1024) && (std::uint32_t)(2 * t) <= L.n_ref_cmds / 16) t *= 2;
@@ -239,18 +271,13 @@ void plan(pccp_gpu_ctx* c) {
     c->gpc = 1;
     c->block = t;
   }
-  const size_t base = dev::kFrameCtl * 4 + (size_t)(c->warp ? c->gpc : 1) *
-                                   (c->store_stride * 4 + sizeof(dev::Cnt) + sizeof(dev::Pf));  // + per-group Cnt, Pf
+  const size_t base = dev::kFrameCtl * 4 + (size_t)(c->warp ? c->gpc : 1) * per_group;
   const size_t table = (size_t)align4(L.hot_words) * 4;  // the staged (hot) prefix of the tables
   if (base > c->smem_optin) throw LimitError("store of " + std::to_string(L.n_words) + " words exceeds shared memory");
   c->ne_only = L.n_ne > 0 && !L.n_reif && !L.n_unit1 && !L.n_unit2 && !L.n_small && !L.n_rows && !L.n_gen &&
                        !L.filtered && !std::getenv("PCCP_NO_NE_KERNEL")
                    ? 1
                    : 0;
-  c->packed_only = L.packed && L.reif8 && L.wrows && L.sc_in_rows && L.iv_prefix && !L.n_ne && !L.n_small &&
-                           !L.n_rows && !L.n_gen && !L.filtered && !std::getenv("PCCP_NO_PACKED_KERNEL")
-                       ? 1
-                       : 0;
   const char* env = std::getenv("PCCP_TABLE_SMEM");
   bool in_smem = base + table <= 100 * 1024;
   if (env) in_smem = std::atoi(env) != 0 && base + table <= c->smem_optin;
@@ -260,7 +287,7 @@ void plan(pccp_gpu_ctx* c) {
   int occ_dec = 0;
   // the attributes and occupancies depend only on (kernel variant, block,
   // smem): a reload of a model with the same plan reuses them
-  const long long key = ((long long)c->warp << 62) ^ ((long long)c->ne_only << 61) ^ ((long long)c->packed_only << 59) ^
+  const long long key = ((long long)c->warp << 62) ^ ((long long)c->ne_only << 61) ^ ((long long)c->packed_only << 59) ^ ((long long)c->packed_filter << 58) ^
                         ((long long)c->table_in_smem << 60) ^ ((long long)c->block << 40) ^ (long long)c->smem;
   if (c->plan_key == key) {
     occ = c->plan_occ;

@@ -33,6 +33,7 @@ struct Model {
   int table_in_smem;             // copy the blob into shared memory at kernel start
   int store_stride;              // words per group store in smem (>= n_words, multiple of 4)
   int cnt_slots;                 // groups per CTA (one Cnt each in smem)
+  int dm_words;                  // per group: the dirty masks of filtered kPacked rounds (3 x (starts + pairs) words)
 };
 
 // Counters and control shared by all groups of one search (global memory).
@@ -309,12 +310,32 @@ __device__ __forceinline__ void sred_max(unsigned a, int v) {
   asm volatile("red.shared.max.s32 [%0], %1;" ::"r"(a), "r"(v) : "memory");
 }
 
+// Dirty masks of filtered kPacked rounds (packed_round_f): bit i of a mask
+// in shared memory.
+__device__ __forceinline__ void smark(unsigned m, unsigned i) {  // bit i of a shared mask
+  asm volatile("red.shared.or.b32 [%0], %1;" ::"r"(m + 4u * (i >> 5)), "r"(1u << (i & 31u)) : "memory");
+}
+__device__ __forceinline__ unsigned sldu(unsigned a) {
+  unsigned v;
+  asm volatile("ld.volatile.shared.b32 %0, [%1];" : "=r"(v) : "r"(a));
+  return v;
+}
+__device__ __forceinline__ void sst(unsigned a, int v) {
+  asm volatile("st.volatile.shared.b32 [%0], %1;" ::"r"(a), "r"(v) : "memory");
+}
+__device__ __forceinline__ unsigned stest(unsigned m, unsigned i) {
+  unsigned v;
+  asm volatile("ld.volatile.shared.b32 %0, [%1];" : "=r"(v) : "r"(m + 4u * (i >> 5)));
+  return (v >> (i & 31u)) & 1u;
+}
+
 // Unit record under L.unit_fast (the value-range analysis bounds every word
 // it reads): all four words loaded at once, 32-bit arithmetic, and the tell
 // joined without a return value when it beats the target's snapshot (a
 // change this round, as in eval_ne_fast).  g2 (unit2 records) is the second
 // guard {a | b << 16, T}, or T = INT_MAX for none.
-__device__ __forceinline__ void eval_unit_fast(unsigned sb, int4 q, int2 g2, unsigned& ch) {
+template <bool Marks = false>
+__device__ __forceinline__ void eval_unit_fast(unsigned sb, int4 q, int2 g2, unsigned& ch, unsigned ms = 0) {
   const unsigned tw = (unsigned)q.w & 0x7fffu, f = ((unsigned)q.w >> 15) & 0x7fffu;
   const unsigned at = sb + (tw << 2);
   const int va = sld(sb + (((unsigned)q.x & 0xffffu) << 2)), vb = sld(sb + (((unsigned)q.x >> 16) << 2));
@@ -326,6 +347,7 @@ __device__ __forceinline__ void eval_unit_fast(unsigned sb, int4 q, int2 g2, uns
       if (q.w < 0) sred_max(at, val);
       else sred_min(at, val);
       ch = 1u;
+      if constexpr (Marks) smark(ms, tw >> 1);
     }
   }
 }
@@ -536,8 +558,11 @@ __device__ __forceinline__ void sred_or(unsigned a, unsigned v) {
 // 0/1 cell has (nlb > lb only for nlb = 1, lb = 0; nub < ub only for 0 < 1).
 // Even: x's and y's lb words are even (kPacked: every interval sits at words
 // [0, 2 n_iv)), so each (lb, ub) pair is one 8-byte load.
-template <bool Fast, bool Even = false>
-__device__ __forceinline__ bool eval_reif_bits(unsigned sb, unsigned sp, int4 r) {
+// Marks: filtered kPacked rounds — a join that beats its snapshot marks its
+// start (ms, bit = start index = lb word / 2) or its plane word (mp, bit =
+// cell / 32) in the next round's dirty masks.
+template <bool Fast, bool Even = false, bool Marks = false>
+__device__ __forceinline__ bool eval_reif_bits(unsigned sb, unsigned sp, int4 r, unsigned ms = 0, unsigned mp = 0) {
   const unsigned ax = sb + (((unsigned)r.x & 0xffffu) << 2), ay = sb + (((unsigned)r.x >> 16) << 2);
   const unsigned bit = (unsigned)r.y, ap = sp + ((bit >> 5) << 3), mk = 1u << (bit & 31u);
   int lx, ux, ly, uy;
@@ -559,6 +584,11 @@ __device__ __forceinline__ bool eval_reif_bits(unsigned sb, unsigned sp, int4 r)
     sred_max(ay, c4 ? nly : INT_MIN);
     sred_min(ay + 4, c5 ? nuy : INT_MAX);
     sred_max(ax, c6 ? nlx : INT_MIN);
+    if constexpr (Marks) {
+      if (c1 | c2) smark(mp, bit >> 5);
+      if (c3 | c6) smark(ms, ((unsigned)r.x & 0xffffu) >> 1);
+      if (c4 | c5) smark(ms, ((unsigned)r.x >> 16) >> 1);
+    }
     return true;
   }
   return false;
@@ -865,8 +895,12 @@ __device__ __forceinline__ unsigned coef_gt(const int4& P, int thr) {  // terms 
 // aligned for the shuffles).  fl: set when a row is (or becomes) overloaded —
 // its lsum cell is (or is joined to) top, the failure the scan would find
 // next (kPacked kernels skip the scalar scan: every scalar is such a cell).
-template <class G, bool TS>
-__device__ bool eval_wrows(const G& g, unsigned sb, const Tab<TS>& tab, const DeviceLayout& L, int rank, bool& fl) {
+// Filt (filtered kPacked rounds): a warp whose rows' windows hold no plane
+// word marked in `cp` skips the pass (warp-uniform: the shuffles below need
+// every lane); zeroing joins mark the plane words they write in `np`.
+template <class G, bool TS, bool Filt = false>
+__device__ bool eval_wrows(const G& g, unsigned sb, const Tab<TS>& tab, const DeviceLayout& L, int rank, bool& fl,
+                           unsigned cp = 0, unsigned np = 0) {
   const int lg = (int)L.wrow_lg, Q = 1 << lg;
   const int q = rank & (Q - 1);
   const int per_pass = g.size() >> lg;
@@ -881,6 +915,10 @@ __device__ bool eval_wrows(const G& g, unsigned sb, const Tab<TS>& tab, const De
     const int4 P = act ? tab.ld4(L.wpat, meta.x + q) : make_int4(0, 0, 0, 0);          // {T, U0, U1, U2}
     const unsigned bit = (unsigned)meta.w + 32u * (unsigned)q, sh = bit & 31u;
     const unsigned a = sp + ((bit >> 5) << 3);
+    if constexpr (Filt) {
+      const bool d = act && P.x && (stest(cp, bit >> 5) | (sh ? stest(cp, (bit >> 5) + 1u) : 0u));
+      if (!__any_sync(kFull, d)) continue;
+    }
     const unsigned alsum = sb + ((unsigned)meta.z << 2);
     const int lsum_now = act && q == 0 ? sld(alsum) : INT_MAX;
     unsigned lbw = 0u, ubw = 0u;
@@ -906,6 +944,10 @@ __device__ bool eval_wrows(const G& g, unsigned sb, const Tab<TS>& tab, const De
           sred_or(a + 4u, z << sh);
           if (sh && (z >> (32u - sh))) sred_or(a + 12u, z >> (32u - sh));
           ch = 1u;
+          if constexpr (Filt) {
+            if (z << sh) smark(np, bit >> 5);
+            if (sh && (z >> (32u - sh))) smark(np, (bit >> 5) + 1u);
+          }
         }
       }
     }
@@ -1080,48 +1122,125 @@ __device__ __forceinline__ bool eval_other_families(const G& g, volatile int* S,
 // kernel, fewer registers, more resident groups (engine.cu dispatch); or
 // kPacked for packed models made of 8-byte bit reifications, unit records and
 // word-parallel bit rows only, whose scalars are all row sums (RCPSP).
-constexpr int kAllFamilies = 0, kNeOnly = 1, kPacked = 2;
+constexpr int kAllFamilies = 0, kNeOnly = 1, kPacked = 2, kPackedF = 3;  // kPackedF: kPacked, filtered rounds
 
 // One round of a kPacked model.  The reifications go from rank 0 up; unit
 // records, rows and the scans from the last warp down (a rotation by whole
 // warps), so the warps carrying one reification more than the others are
 // not the ones carrying the rows.  Failure: the start intervals (the words
 // [0, 2 n_iv)), the bit planes, and overloaded rows (eval_wrows).
-template <class G, bool TS>
+//
+// Filt (L.pfilter, propagate_packed): a record is evaluated only when a start
+// or plane word it reads is marked in this round's dirty masks (cs, cp): one
+// whose inputs did not change since it was last evaluated would join the
+// same values again, a no-op.  Its joins mark the next round's masks (ns, np).
+template <class G, bool TS, bool Filt = false>
 __device__ __forceinline__ bool packed_round(const G& g, unsigned sb, const Tab<TS>& tab, const DeviceLayout& L,
-                                             bool& fl) {
+                                             bool& fl, unsigned cs = 0, unsigned cp = 0, unsigned ns = 0,
+                                             unsigned np = 0) {
   const unsigned sp = sb + 4u * L.plane;
+  const unsigned n2 = 2u * L.n_iv;  // the start words
   auto rec = [&](int i) {
     const int2 q = tab.ld2(L.reif, i);
     return make_int4(q.x, q.y & 0x3ffff, (q.y << 7) >> 25, q.y >> 25);
   };
+  auto clean = [&](const int4& q) {  // reification inputs: x, y starts and b's plane word
+    if constexpr (Filt) {
+      return !(stest(cs, ((unsigned)q.x & 0xffffu) >> 1) | stest(cs, ((unsigned)q.x >> 16) >> 1) |
+               stest(cp, (unsigned)q.y >> 5));
+    }
+    return false;
+  };
+  auto wdirty = [&](unsigned w) { return w < n2 ? stest(cs, w >> 1) : 0u; };  // the zero word never changes
   bool ch = false;
-  if (L.reif_fast) {
-    for (int i = g.rank(); i < (int)L.n_reif; i += g.size()) ch |= eval_reif_bits<true, true>(sb, sp, rec(i));
-  } else {
-    for (int i = g.rank(); i < (int)L.n_reif; i += g.size()) ch |= eval_reif_bits<false, true>(sb, sp, rec(i));
+  auto reif = [&](int i) {
+    const int4 q = rec(i);
+    if (L.reif_fast) ch |= eval_reif_bits<true, true, Filt>(sb, sp, q, ns, np);
+    else ch |= eval_reif_bits<false, true, Filt>(sb, sp, q, ns, np);
+  };
+  bool segs = false;
+  if constexpr (Filt) {
+    // The reifications that read a marked start or plane word, by segment
+    // (lower.cpp: the y range, the x list and the plane word's range of each):
+    // every thread walks the same marked bits, so the loops stay uniform and a
+    // warp's lanes evaluate records that are all due.  When the marks cover
+    // too much (a third of the records or more: every record sits in three
+    // segments), the round walks all records instead.
+    if (L.rfilt) {
+      unsigned n_s = 0, n_p = 0;
+      for (unsigned w = 0; w < L.dm_s; ++w) n_s += __popc(sldu(cs + 4u * w));
+      for (unsigned w = 0; w < L.dm_p; ++w) n_p += __popc(sldu(cp + 4u * w));
+      const unsigned est = n_s * (2u * L.n_reif / max(L.r_ns, 1u)) + 32u * n_p;
+      segs = 3u * est < L.n_reif;
+    }
+    if (segs) {
+      for (unsigned w = 0; w < L.dm_s; ++w) {
+        for (unsigned bits = sldu(cs + 4u * w); bits; bits &= bits - 1u) {
+          const unsigned k = 32u * w + (unsigned)(__ffs((int)bits) - 1);
+          if (k >= L.r_ns) continue;
+          const int2 yr = tab.ld2(L.r_y, (int)k);
+          for (int i = yr.x + g.rank(); i < yr.y; i += g.size()) reif(i);
+          const int xb = tab.ld1(L.r_xoff, (int)k), xe = tab.ld1(L.r_xoff, (int)k + 1);
+          for (int i = xb + g.rank(); i < xe; i += g.size()) reif(tab.ld1(L.r_xrec, i));
+        }
+      }
+      for (unsigned w = 0; w < L.dm_p; ++w) {
+        for (unsigned bits = sldu(cp + 4u * w); bits; bits &= bits - 1u) {
+          const unsigned p = 32u * w + (unsigned)(__ffs((int)bits) - 1);
+          if (p >= L.n_pairs) continue;
+          const int pe = tab.ld1(L.r_p, (int)p + 1);
+          for (int i = tab.ld1(L.r_p, (int)p) + g.rank(); i < pe; i += g.size()) reif(i);
+        }
+      }
+    }
+  }
+  if (!segs) {
+    for (int i = g.rank(); i < (int)L.n_reif; i += g.size()) {
+      if (Filt && clean(rec(i))) continue;
+      reif(i);
+    }
   }
   const int rr = (g.size() - 32 * (g.rank() >> 5 ) - 32) + (g.rank() & 31);  // warps in reverse order
+  auto unit_clean = [&](const int4& q, const int2& g2) {
+    if constexpr (Filt) {
+      const unsigned x = (unsigned)q.x, f = ((unsigned)q.w >> 15) & 0x7fffu, y = (unsigned)g2.x;
+      return !(wdirty(x & 0xffffu) | wdirty(x >> 16) | wdirty(f) | wdirty(y & 0xffffu) | wdirty(y >> 16));
+    }
+    return false;
+  };
+  const int2 none = make_int2((int)(L.zero_word | (L.zero_word << 16)), INT_MAX);  // Z - Z <= INT_MAX: no second guard
   if (L.unit_fast) {
     unsigned uch = 0;
-    const int2 none = make_int2(0, INT_MAX);
-    for (int i = rr; i < (int)L.n_unit1; i += g.size()) eval_unit_fast(sb, tab.ld4(L.unit1, i), none, uch);
-    for (int i = rr; i < (int)L.n_unit2; i += g.size()) eval_unit_fast(sb, tab.ld4(L.unit2, i), tab.ld2(L.unit2g, i), uch);
+    for (int i = rr; i < (int)L.n_unit1; i += g.size()) {
+      const int4 q = tab.ld4(L.unit1, i);
+      if (!unit_clean(q, none)) eval_unit_fast<Filt>(sb, q, none, uch, ns);
+    }
+    for (int i = rr; i < (int)L.n_unit2; i += g.size()) {
+      const int4 q = tab.ld4(L.unit2, i);
+      const int2 q2 = tab.ld2(L.unit2g, i);
+      if (!unit_clean(q, q2)) eval_unit_fast<Filt>(sb, q, q2, uch, ns);
+    }
     ch |= uch != 0;
   } else {
     for (int i = rr; i < (int)L.n_unit1; i += g.size()) {
       const int4 q = tab.ld4(L.unit1, i);
-      if (unit_guard(sb, q.x, q.y)) ch |= unit_tell(sb, q.z, q.w);
+      if (unit_clean(q, none)) continue;
+      if (unit_guard(sb, q.x, q.y) && unit_tell(sb, q.z, q.w)) {
+        ch = true;
+        if constexpr (Filt) smark(ns, ((unsigned)q.w & 0x7fffu) >> 1);
+      }
     }
     for (int i = rr; i < (int)L.n_unit2; i += g.size()) {
       const int4 q = tab.ld4(L.unit2, i);
-      if (unit_guard(sb, q.x, q.y)) {
-        const int2 q2 = tab.ld2(L.unit2g, i);
-        if (unit_guard(sb, q2.x, q2.y)) ch |= unit_tell(sb, q.z, q.w);
+      const int2 q2 = tab.ld2(L.unit2g, i);
+      if (unit_clean(q, q2)) continue;
+      if (unit_guard(sb, q.x, q.y) && unit_guard(sb, q2.x, q2.y) && unit_tell(sb, q.z, q.w)) {
+        ch = true;
+        if constexpr (Filt) smark(ns, ((unsigned)q.w & 0x7fffu) >> 1);
       }
     }
   }
-  ch |= eval_wrows(g, sb, tab, L, rr, fl);
+  ch |= eval_wrows<G, TS, Filt>(g, sb, tab, L, rr, fl, cp, np);
   for (int i = rr; i < (int)L.n_iv; i += g.size()) {
     const int2 v = sld2(sb + 8u * (unsigned)i);
     fl |= v.x > v.y;
@@ -1133,12 +1252,53 @@ __device__ __forceinline__ bool packed_round(const G& g, unsigned sb, const Tab<
   return ch;
 }
 
+// Filtered rounds of a kPacked model (F = kPackedF): three rotating dirty masks
+// D[r % 3] (read by round r), D[(r+1) % 3] (marked by round r's joins),
+// D[(r+2) % 3] (cleared during round r: round r-1 read it, round r+1 marks
+// it).  Each mask is `starts` bits then `plane words` bits (DeviceLayout
+// dm_s, dm_p words).  On entry D[0] holds the node's changes — every start
+// and plane word when dirty == kAllDirty, else the marks the caller made (the
+// decision's start and the objective's); D[1] and D[2] are zero, and all three
+// are zero again on return.  A record whose inputs are unmarked is skipped:
+// its inputs are unchanged since it was last evaluated, so it would join the
+// same values again.  The loop ends, as the eventless one, at the first round
+// without a change or with a failure.
+template <class G, bool TS>
+__device__ bool propagate_packed(const G& g, unsigned sb, const Tab<TS>& tab, const DeviceLayout& L, int& rounds,
+                                 unsigned long long dirty, unsigned dm) {
+  const int W = (int)(L.dm_s + L.dm_p);
+  if (dirty == kAllDirty)
+    for (int i = g.rank(); i < W; i += g.size()) sst(dm + 4u * i, -1);
+  g.round_begin();
+  int r = 0;
+  bool failed = false;
+  for (;;) {
+    const unsigned cur = dm + 4u * (unsigned)(W * (r % 3)), nxt = dm + 4u * (unsigned)(W * ((r + 1) % 3)),
+                   clr = dm + 4u * (unsigned)(W * ((r + 2) % 3));
+    for (int i = g.rank(); i < W; i += g.size()) sst(clr + 4u * i, 0);
+    bool fl = false;
+    const bool ch = packed_round<G, TS, true>(g, sb, tab, L, fl, cur, cur + 4u * L.dm_s, nxt, nxt + 4u * L.dm_s);
+    bool any_ch, any_fl;
+    g.round_end(ch, fl, any_ch, any_fl, r);
+    ++r;
+    if (any_fl) {
+      failed = true;
+      break;
+    }
+    if (!any_ch) break;
+  }
+  for (int i = g.rank(); i < 3 * W; i += g.size()) sst(dm + 4u * i, 0);
+  rounds = r;
+  return failed;
+}
+
 template <class G, bool TS, int F = kAllFamilies>
 __device__ bool propagate(const G& g, volatile int* S, unsigned sb, const Tab<TS>& tab, const DeviceLayout& L,
-                          int& rounds, unsigned long long dirty = kAllDirty) {
+                          int& rounds, unsigned long long dirty = kAllDirty, unsigned dm = 0) {
   if constexpr (std::is_same<G, WarpGroup>::value && F == kAllFamilies) {
     if (L.filtered) return propagate_filtered(g, S, sb, tab, L, dirty, rounds);
   }
+  if constexpr (F == kPackedF) return propagate_packed(g, sb, tab, L, rounds, dirty, dm);
   const int* __restrict__ T = tab.p;
   g.round_begin();
   int r = 0;

@@ -707,6 +707,24 @@ Lowered lower_impl(const pccp_model& m, bool want_bits) {
           if (a != b) par[b] = a;
         }
       }
+      // reifications of one y join their cells' components too (RCPSP: a
+      // task that uses no resource has no row terms, but its b_{i,j} belongs
+      // to column j), so the records of one y are one range of bits
+      // (filtered rounds: lower.cpp r_y)
+      {
+        std::map<std::uint32_t, std::int32_t> first_of_y;
+        for (const Reif& r : reifs) {
+          const std::uint32_t y = static_cast<std::uint32_t>(r.xy) >> 16;
+          const std::int32_t b = find(r.b);
+          auto it = first_of_y.find(y);
+          if (it == first_of_y.end()) {
+            first_of_y.emplace(y, b);
+          } else {
+            const std::int32_t a = find(it->second);
+            if (a != b) par[b] = a;
+          }
+        }
+      }
       std::vector<std::int64_t> rank(NW, -1);
       std::int64_t next = 0;
       for (std::size_t r = 0; r < rows.size(); ++r)
@@ -891,6 +909,57 @@ Lowered lower_impl(const pccp_model& m, bool want_bits) {
     B[L.reif + 4 * i + 1] = reifs[i].b;
     B[L.reif + 4 * i + 2] = reifs[i].p;
     B[L.reif + 4 * i + 3] = reifs[i].q;
+  }
+  // Segments of the filtered kPacked rounds (kernels.cuh packed_round): the
+  // records that read start k as y (a contiguous range: records are sorted by
+  // b's bit, and a component of bits is one y), as x (CSR of record indices),
+  // and the records whose b lies in plane word p (a range).
+  if (packed && L.reif8 && L.n_reif) {
+    std::uint32_t ns = 0;
+    for (const Reif& r : reifs)
+      ns = std::max({ns, ((static_cast<std::uint32_t>(r.xy) & 0xffffu) >> 1) + 1,
+                     ((static_cast<std::uint32_t>(r.xy) >> 16) >> 1) + 1});
+    std::vector<std::int32_t> yb(ns, 0), ye(ns, 0), xoff(ns + 1, 0), xrec(L.n_reif), pb(n_pairs + 1, 0);
+    std::vector<std::uint8_t> seen(ns, 0);
+    bool contiguous = true;
+    for (std::uint32_t i = 0; i < L.n_reif; ++i) {
+      const std::uint32_t ky = (static_cast<std::uint32_t>(reifs[i].xy) >> 16) >> 1;
+      if (!seen[ky]) {
+        seen[ky] = 1;
+        yb[ky] = ye[ky] = static_cast<std::int32_t>(i);
+      } else if (ye[ky] != static_cast<std::int32_t>(i)) {
+        contiguous = false;
+      }
+      ye[ky] = static_cast<std::int32_t>(i + 1);
+      ++xoff[((static_cast<std::uint32_t>(reifs[i].xy) & 0xffffu) >> 1) + 1];
+    }
+    for (std::uint32_t k = 0; k < ns; ++k) xoff[k + 1] += xoff[k];
+    {
+      std::vector<std::int32_t> fill(xoff.begin(), xoff.end() - 1);
+      for (std::uint32_t i = 0; i < L.n_reif; ++i)
+        xrec[static_cast<std::uint32_t>(fill[(static_cast<std::uint32_t>(reifs[i].xy) & 0xffffu) >> 1]++)] =
+            static_cast<std::int32_t>(i);
+    }
+    for (std::uint32_t p = 0, i = 0; p <= n_pairs; ++p) {
+      while (i < L.n_reif && static_cast<std::uint32_t>(reifs[i].b) < 32 * p) ++i;
+      pb[p] = static_cast<std::int32_t>(i);
+    }
+    pb[n_pairs] = static_cast<std::int32_t>(L.n_reif);
+    if (contiguous) {
+      L.rfilt = 1;
+      L.r_ns = ns;
+      L.r_y = reserve_arr(2 * ns);
+      L.r_xoff = reserve_arr(ns + 1);
+      L.r_xrec = reserve_arr(L.n_reif);
+      L.r_p = reserve_arr(n_pairs + 1);
+      for (std::uint32_t k = 0; k < ns; ++k) {
+        B[L.r_y + 2 * k] = yb[k];
+        B[L.r_y + 2 * k + 1] = ye[k];
+      }
+      std::copy(xoff.begin(), xoff.end(), B.begin() + L.r_xoff);
+      std::copy(xrec.begin(), xrec.end(), B.begin() + L.r_xrec);
+      std::copy(pb.begin(), pb.end(), B.begin() + L.r_p);
+    }
   }
   L.n_unit1 = static_cast<std::uint32_t>(unit1.size());
   L.unit1 = reserve_arr(4 * L.n_unit1);

@@ -105,6 +105,14 @@ struct DeviceLayout {
   std::uint32_t wrow_meta;    // int4 per row: {first chunk (int4 index into wpat), c, lsum word, first bit}
   std::uint32_t wpat;         // int4 per chunk: {term mask, coefficient bit-planes 0, 1, 2}
   std::uint32_t sc_in_rows;   // every scalar slot is the lsum cell of a word-parallel bit row
+  // Filtered kPacked rounds (kernels.cuh propagate_packed), set per launch:
+  // dirty masks of dm_s words (one bit per start interval) + dm_p words (one
+  // bit per plane word) per round buffer.
+  std::uint32_t pfilter, dm_s, dm_p;
+  // Reification segments for those rounds (lower.cpp): by y start (int2 [begin,
+  // end) ranges), by x start (CSR r_xoff / r_xrec of record indices), by plane
+  // word (r_p: begin of each word's range); r_ns starts.
+  std::uint32_t rfilt, r_ns, r_y, r_xoff, r_xrec, r_p;
 };
 
 

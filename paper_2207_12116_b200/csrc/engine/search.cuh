@@ -79,15 +79,18 @@ __device__ __forceinline__ void prefetch_wait() { asm volatile("cp.async.wait_al
 
 // Objective tightening at materialisation (solver.cpp:96-99): obj <= best-1.
 // Returns the dirty bit of the objective's ub word when it moved (uniform).
+// dm (filtered kPacked rounds): rank 0 marks the objective's start when it moved.
 template <class G>
 __device__ __forceinline__ unsigned long long join_objective(const G& g, volatile int* S, const DeviceLayout& L,
-                                                             const SearchCtl& C, const Pf* pf = nullptr) {
+                                                             const SearchCtl& C, const Pf* pf = nullptr,
+                                                             unsigned dm = 0) {
   if (C.mode != 1 || !C.bound || L.obj_lbw < 0) return 0ull;
   int moved = 0;
   if (g.rank() == 0) {
     const int best = pf ? min(*(volatile const int*)&pf->ctl[3], *(volatile const int*)&pf->own)
                         : *(volatile int*)&C.G->incumbent;
     if (best != INT_MAX) moved = join_min(S, L.obj_lbw + 1, best - 1) ? 1 : 0;
+    if (moved && dm) smark(dm, (unsigned)L.obj_lbw >> 1);
   }
   // Only the filtered rounds use the dirty mask; the eventless loop needs no
   // broadcast (callers sync before propagating).
@@ -238,6 +241,8 @@ struct Frame {
   unsigned long long* red;
   Cnt* cnt;  // one per group of the CTA
   Pf* pf;    // one per group of the CTA
+  int* dm;   // dirty masks of filtered kPacked rounds, dm_words per group
+  int dm_words;
   int* stores;
 };
 
@@ -290,6 +295,10 @@ __device__ __forceinline__ Frame frame(const Model& M) {
   f.pf = reinterpret_cast<Pf*>(smem + off);
   for (int i = threadIdx.x; i < M.cnt_slots; i += blockDim.x) f.pf[i].own = INT_MAX;
   off += M.cnt_slots * (int)(sizeof(Pf) / 4);
+  f.dm = smem + off;  // filtered kPacked rounds: zero between propagations (propagate_packed)
+  for (int i = threadIdx.x; i < M.cnt_slots * M.dm_words; i += blockDim.x) f.dm[i] = 0;
+  off += M.cnt_slots * M.dm_words;
+  f.dm_words = M.dm_words;
   f.stores = smem + off;
   __syncthreads();
   return f;
@@ -328,6 +337,13 @@ struct GroupOf<CtaGroup> {
   static __device__ __forceinline__ int in_cta() { return 0; }
   static __device__ __forceinline__ int per_cta() { return 1; }
 };
+
+// Shared address of this group's dirty masks (filtered kPacked rounds; 0 when none).
+template <class G>
+__device__ __forceinline__ unsigned dm_addr(const Frame& f) {
+  if (!f.dm_words) return 0u;
+  return (unsigned)__cvta_generic_to_shared(f.dm + GroupOf<G>::in_cta() * f.dm_words);
+}
 
 // Launch bounds: warp groups run <= 8 warps per CTA; CTA groups up to 1024
 // threads.  Both give ptxas a 64-register budget (at least 4 CTAs of 8 warps);
@@ -369,7 +385,7 @@ __global__ void __launch_bounds__(MaxThreads<G, F>::value, MaxThreads<G, F>::min
       g.sync();
     }
     int r = 0;
-    const bool failed = propagate<G, TS, F>(g, S, sb, tab, M.L, r);
+    const bool failed = propagate<G, TS, F>(g, S, sb, tab, M.L, r, kAllDirty, dm_addr<G>(f));
     copy_out(g, io, S, (int)M.L.n_words);
     if (g.rank() == 0) {
       status[i] = failed ? 1 : 0;
@@ -397,7 +413,7 @@ __global__ void __launch_bounds__(MaxThreads<G, F>::value, MaxThreads<G, F>::min
   if (g.rank() == 0 && C.G->node_limit != ~0ull) atomicAdd(&C.G->nodes_reserved, 1ull);  // the root's materialisation
   g.sync();
   int r = 0;
-  const bool failed = propagate<G, TS, F>(g, S, sb, tab, M.L, r);
+  const bool failed = propagate<G, TS, F>(g, S, sb, tab, M.L, r, kAllDirty, dm_addr<G>(f));
   if (C.count && g.rank() == 0) {
     ++cnt.nodes;
     cnt.rounds += (unsigned long long)r;
@@ -494,7 +510,9 @@ __device__ void expand_level(const G& g, volatile int* S, unsigned sb, const Tab
         g.sync();
         int r = 0;
         dbg_mark(3 + 5 * side);
-        const bool failed = propagate<G, TS, F>(g, S, sb, tab, L, r, dirty);
+        // (filtered kPacked rounds: every word of a child, no per-node marks here)
+        const bool failed =
+            propagate<G, TS, F>(g, S, sb, tab, L, r, F == kPackedF ? kAllDirty : dirty, dm_addr<G>(f));
         dbg_mark(4 + 5 * side);
 #ifdef PCCP_DEBUG_TIMELINE
         if (g_dbg_tl && blockIdx.x == 0 && threadIdx.x == 0) g_dbg_tl[20 + side] = r;
@@ -822,6 +840,9 @@ __global__ void __launch_bounds__(MaxThreads<G, F>::value, MaxThreads<G, F>::min
   constexpr bool kMerge = kPrefetch && PCCP_CTL_MERGE;  // the control of the next node before the last barrier
   Pf* pf = kPrefetch ? f.pf + GroupOf<G>::in_cta() : nullptr;
   if (kPrefetch && g.rank() == 0) prefetch_ctl(pf, Gl);
+  // filtered kPacked rounds: a node's changes (decision, objective) are marked
+  // in the first dirty mask by rank 0 before the propagation
+  const unsigned dm = F == kPackedF ? dm_addr<G>(f) : 0u;
   bool queue_open = true;
   const bool right_first = P.value_order == 1 || (P.value_order == 2 && (gid & 1));
   for (;;) {
@@ -886,6 +907,7 @@ __global__ void __launch_bounds__(MaxThreads<G, F>::value, MaxThreads<G, F>::min
     int sp = 0, bot = 0;
     bool abandoned = false;
     bool remat = need_prop && dirty != kAllDirty;  // a frontier node re-materialised under the bound (mode 1)
+    if (dm) dirty = kAllDirty;  // a subproblem's first propagation evaluates everything
     // Enumeration: a frontier node was counted and classified during the
     // decomposition.  Minimisation: re-materialise it with the current bound,
     // as dfs() does for its subproblem root.  A donated node is unpropagated.
@@ -938,7 +960,7 @@ __global__ void __launch_bounds__(MaxThreads<G, F>::value, MaxThreads<G, F>::min
           if (slot >= 0) copy_out(g, C.audit_pre + (size_t)slot * nw, S, nw);
         }
         int r = 0;
-        const bool failed = propagate<G, TS, F>(g, S, sb, tab, L, r, dirty);
+        const bool failed = propagate<G, TS, F>(g, S, sb, tab, L, r, dirty, dm);
         if constexpr (Audit) {
           if (slot >= 0) {
             copy_out(g, C.audit_post + (size_t)slot * nw, S, nw);
@@ -978,11 +1000,12 @@ __global__ void __launch_bounds__(MaxThreads<G, F>::value, MaxThreads<G, F>::min
           ent[nw + 2] = depth;
           if (right_first) join_max(S, lbw, mid + 1);  // x >= mid+1 first
           else join_min(S, lbw + 1, mid);              // x <= mid first (dfs(), solver.cpp:139-143)
+          if (dm) smark(dm, (unsigned)lbw >> 1);
         }
         ++sp;
         ++depth;
         // rank 0 made the decision join and makes the objective join: one sync
-        dirty = word_bit(right_first ? lbw : lbw + 1) | join_objective(g, S, L, C, pf);
+        dirty = word_bit(right_first ? lbw : lbw + 1) | join_objective(g, S, L, C, pf, dm);
         need_prop = true;
         if constexpr (kMerge) {
           if (g.rank() == 0) pf->pad[0] = node_ctl_rank0(C, P, Gl, pf, sp - bot, true);
@@ -1001,10 +1024,11 @@ __global__ void __launch_bounds__(MaxThreads<G, F>::value, MaxThreads<G, F>::min
       if (g.rank() == 0) {
         if (tag < 0) join_min(S, (tag & 0x7fffffff) + 1, ent[nw + 1]);  // pending x <= mid
         else join_max(S, tag, ent[nw + 1] + 1);                        // pending x >= mid+1
+        if (dm) smark(dm, (unsigned)(tag & 0x7fffffff) >> 1);
       }
       depth = ent[nw + 2] + 1;
       dirty = word_bit(tag < 0 ? (tag & 0x7fffffff) + 1 : tag);
-      dirty |= join_objective(g, S, L, C, pf);  // rank 0, after its decision join
+      dirty |= join_objective(g, S, L, C, pf, dm);  // rank 0, after its decision join
       need_prop = true;
       if constexpr (kMerge) {
         if (g.rank() == 0) pf->pad[0] = node_ctl_rank0(C, P, Gl, pf, sp - bot, true);

@@ -1,11 +1,12 @@
 """Multi-GPU driver: one process per GPU, the EPS frontier sharded i mod N.
 
 Enumeration (configs 1-3) has no data-path exchange: every rank computes the
-same deterministic frontier, drains its own shard, and the counters are
-combined once at the end (sums; the hash-sum mod 2^64).  Minimisation (configs
-4-5) shares one int32: each rank exports the IPC handle of its incumbent cell,
-attaches every peer's, and improving solutions are pushed with system-scope
-atomicMin over NVLink from inside the search kernel.
+same deterministic frontier, drains its own shard (and, with peers attached,
+steals positions of the peers' shards nobody has reached), and the counters
+are combined once at the end (sums; the hash-sum mod 2^64).  Minimisation
+(configs 4-5) shares one int32: each rank exports the IPC handle of its
+control cells, attaches every peer's, and improving solutions are pushed with
+system-scope atomicMin over NVLink from inside the search kernel.
 
 Collectives here go through torch.distributed (NCCL on the GPU box, gloo in
 the CPU tests); they run once per call, never per node.
@@ -79,7 +80,10 @@ def run_enumerate(engine, depth_cap: int = -1, root=None, group=None) -> dict:
 
 
 def attach_incumbents(engine, group=None) -> None:
-    """Exchange incumbent IPC handles and attach every peer (optimisation only)."""
+    """Exchange the IPC handles of every rank's control cells (incumbent, done
+    flag, share cell) in rank order and attach every peer: minimisation shares
+    the incumbent, and any sharded search steals untouched frontier positions
+    from the peers' shares (engine.cu run_search)."""
     import torch.distributed as dist
     handles = _gather(engine.incumbent_handle(), group)
     engine.attach_peers(handles, dist.get_rank(group))

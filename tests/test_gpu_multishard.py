@@ -205,10 +205,12 @@ def test_linked_enumeration_steals_and_stays_exact(n_shards, golden):
     from paper_2207_12116_b200 import Engine, Model
     from paper_2207_12116_b200.distributed import combine_enum
     from paper_2207_12116_b200.engine import link_peers
-    for name, depth in (("nqueens10", -1), ("csp1", 12)):
+    for name, depth in (("nqueens10", -1), ("csp1", 22)):
         m = Model.nqueens(10) if name == "nqueens10" else Model.random_csp(1)
-        g = golden[name]["enumerate" if depth < 0 else "enumerate_d12"]
-        engs = [Engine(0, shard_index=k, shard_count=n_shards, hash=True, record_frontier=True) for k in range(n_shards)]
+        g = golden[name]["enumerate" if depth < 0 else "enumerate_d22"]
+        # one group per SM: a shared frontier of 148 x N nodes, well inside these trees
+        engs = [Engine(0, shard_index=k, shard_count=n_shards, hash=True, record_frontier=True, ctas_per_sm=1,
+                       groups_per_cta=1) for k in range(n_shards)]
         try:
             for e in engs:
                 e.load(m)
@@ -223,6 +225,7 @@ def test_linked_enumeration_steals_and_stays_exact(n_shards, golden):
                     assert tot[key] == g[key], (name, n_shards, rep, key)
                 assert tot["exhausted"]
                 _check_partition(fronts)
+                assert fronts[0][0].size > 0, (name, rep)
                 assert parts[0]["stolen"] > 0 and fronts[0][1].size == fronts[0][0].size, (name, rep)
                 assert all(f[1].size == 0 for f in fronts[1:])  # nothing was left for the later shards
         finally:
