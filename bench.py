@@ -316,9 +316,22 @@ def rcpsp120(local, rank, world, dist, budget_s):
         r0 = e0.solve(timeout_s=3.0)
         ref_order = {"status": r0.status, "nodes": r0.stats["nodes"], "device_ms": r0.stats["device_ms"],
                      "nodes_per_s": r0.stats["nodes"] / (r0.stats["device_ms"] / 1e3),
-                     "roofline": roofline(r0.stats, e0.lowering_info(), sm)}
+                     "rounds": "filtered (kPackedF, the default for this model)"}
         if world > 1:
             ref_order["nodes_per_s_all_ranks"] = sum(_gather_obj(dist, ref_order["nodes_per_s"]))
+    # the same search in eventless rounds (every record every round): the
+    # roofline's byte model describes this loop; filtered rounds do less work
+    # per node, not the same work faster
+    os.environ["PCCP_PACKED_FILTER"] = "0"
+    try:
+        with Engine(local, shard_index=rank, shard_count=world) as e1:
+            e1.load(m)
+            r1 = e1.solve(timeout_s=3.0)
+            ref_order["eventless"] = {"nodes": r1.stats["nodes"], "device_ms": r1.stats["device_ms"],
+                                      "nodes_per_s": r1.stats["nodes"] / (r1.stats["device_ms"] / 1e3),
+                                      "roofline": roofline(r1.stats, e1.lowering_info(), sm)}
+    finally:
+        del os.environ["PCCP_PACKED_FILTER"]
     eng = Engine(local, shard_index=rank, shard_count=world, primal_ms=int(budget_s * 1e3))
     eng.load(m)
     if world > 1:
