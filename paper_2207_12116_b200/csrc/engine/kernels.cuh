@@ -1137,7 +1137,7 @@ constexpr int kAllFamilies = 0, kNeOnly = 1, kPacked = 2, kPackedF = 3;  // kPac
 template <class G, bool TS, bool Filt = false>
 __device__ __forceinline__ bool packed_round(const G& g, unsigned sb, const Tab<TS>& tab, const DeviceLayout& L,
                                              bool& fl, unsigned cs = 0, unsigned cp = 0, unsigned ns = 0,
-                                             unsigned np = 0) {
+                                             unsigned np = 0, bool full = false) {
   const unsigned sp = sb + 4u * L.plane;
   const unsigned n2 = 2u * L.n_iv;  // the start words
   auto rec = [&](int i) {
@@ -1161,42 +1161,45 @@ __device__ __forceinline__ bool packed_round(const G& g, unsigned sb, const Tab<
   bool segs = false;
   if constexpr (Filt) {
     // The reifications that read a marked start or plane word, by segment
-    // (lower.cpp: the y range, the x list and the plane word's range of each):
-    // every thread walks the same marked bits, so the loops stay uniform and a
-    // warp's lanes evaluate records that are all due.  When the marks cover
-    // too much (a third of the records or more: every record sits in three
-    // segments), the round walks all records instead.
-    if (L.rfilt) {
-      unsigned n_s = 0, n_p = 0;
-      for (unsigned w = 0; w < L.dm_s; ++w) n_s += __popc(sldu(cs + 4u * w));
-      for (unsigned w = 0; w < L.dm_p; ++w) n_p += __popc(sldu(cp + 4u * w));
-      const unsigned est = n_s * (2u * L.n_reif / max(L.r_ns, 1u)) + 32u * n_p;
-      segs = 3u * est < L.n_reif;
-    }
+    // (lower.cpp: the y range, the x list and the plane word's range of each),
+    // cut into 32-record chunks dealt to the warps in turn: every warp walks
+    // the same marked bits, so the loops stay uniform, and a warp's lanes
+    // evaluate records that are all due.  A round whose marks are everything
+    // (`full`: a subproblem's first round) walks all records instead.
+    segs = L.rfilt && !full;
     if (segs) {
+      const int nwarps = g.warps(), wid = g.warp(), lane = g.rank() & 31;
+      int turn = 0;  // the warp that takes the next chunk (the same sequence in every warp)
+      auto seg = [&](int b, int e, bool indirect) {
+        for (int c0 = b; c0 < e; c0 += 32) {
+          const bool mine = turn == wid;
+          if (++turn == nwarps) turn = 0;
+          if (!mine) continue;
+          const int i = c0 + lane;
+          if (i < e) reif(indirect ? tab.ld1(L.r_xrec, i) : i);
+        }
+      };
       for (unsigned w = 0; w < L.dm_s; ++w) {
         for (unsigned bits = sldu(cs + 4u * w); bits; bits &= bits - 1u) {
           const unsigned k = 32u * w + (unsigned)(__ffs((int)bits) - 1);
           if (k >= L.r_ns) continue;
           const int2 yr = tab.ld2(L.r_y, (int)k);
-          for (int i = yr.x + g.rank(); i < yr.y; i += g.size()) reif(i);
-          const int xb = tab.ld1(L.r_xoff, (int)k), xe = tab.ld1(L.r_xoff, (int)k + 1);
-          for (int i = xb + g.rank(); i < xe; i += g.size()) reif(tab.ld1(L.r_xrec, i));
+          seg(yr.x, yr.y, false);
+          seg(tab.ld1(L.r_xoff, (int)k), tab.ld1(L.r_xoff, (int)k + 1), true);
         }
       }
       for (unsigned w = 0; w < L.dm_p; ++w) {
         for (unsigned bits = sldu(cp + 4u * w); bits; bits &= bits - 1u) {
           const unsigned p = 32u * w + (unsigned)(__ffs((int)bits) - 1);
           if (p >= L.n_pairs) continue;
-          const int pe = tab.ld1(L.r_p, (int)p + 1);
-          for (int i = tab.ld1(L.r_p, (int)p) + g.rank(); i < pe; i += g.size()) reif(i);
+          seg(tab.ld1(L.r_p, (int)p), tab.ld1(L.r_p, (int)p + 1), false);
         }
       }
     }
   }
   if (!segs) {
     for (int i = g.rank(); i < (int)L.n_reif; i += g.size()) {
-      if (Filt && clean(rec(i))) continue;
+      if (Filt && !full && clean(rec(i))) continue;
       reif(i);
     }
   }
@@ -1277,7 +1280,8 @@ __device__ bool propagate_packed(const G& g, unsigned sb, const Tab<TS>& tab, co
                    clr = dm + 4u * (unsigned)(W * ((r + 2) % 3));
     for (int i = g.rank(); i < W; i += g.size()) sst(clr + 4u * i, 0);
     bool fl = false;
-    const bool ch = packed_round<G, TS, true>(g, sb, tab, L, fl, cur, cur + 4u * L.dm_s, nxt, nxt + 4u * L.dm_s);
+    const bool ch = packed_round<G, TS, true>(g, sb, tab, L, fl, cur, cur + 4u * L.dm_s, nxt, nxt + 4u * L.dm_s,
+                                              r == 0 && dirty == kAllDirty);
     bool any_ch, any_fl;
     g.round_end(ch, fl, any_ch, any_fl, r);
     ++r;

@@ -66,7 +66,8 @@ struct alignas(16) Pf {
   int ctl[4];   // cursor, stop, incomplete, incumbent
   int hung[4];  // hungry, padding
   int own;      // best value this group recorded (INT_MAX: none)
-  int pad[3];
+  int inc;      // the incumbent of the last completed prefetch (ctl[3] may be in flight again)
+  int pad[2];   // pad[0]: the next node's control word (CTA groups)
 };
 
 __device__ __forceinline__ void prefetch_ctl(Pf* pf, const Globals* G) {
@@ -87,7 +88,7 @@ __device__ __forceinline__ unsigned long long join_objective(const G& g, volatil
   if (C.mode != 1 || !C.bound || L.obj_lbw < 0) return 0ull;
   int moved = 0;
   if (g.rank() == 0) {
-    const int best = pf ? min(*(volatile const int*)&pf->ctl[3], *(volatile const int*)&pf->own)
+    const int best = pf ? min(*(volatile const int*)&pf->inc, *(volatile const int*)&pf->own)
                         : *(volatile int*)&C.G->incumbent;
     if (best != INT_MAX) moved = join_min(S, L.obj_lbw + 1, best - 1) ? 1 : 0;
     if (moved && dm) smark(dm, (unsigned)L.obj_lbw >> 1);
@@ -293,7 +294,7 @@ __device__ __forceinline__ Frame frame(const Model& M) {
     reinterpret_cast<unsigned long long*>(f.cnt)[i] = 0ull;
   off += M.cnt_slots * (int)(sizeof(Cnt) / 4);
   f.pf = reinterpret_cast<Pf*>(smem + off);
-  for (int i = threadIdx.x; i < M.cnt_slots; i += blockDim.x) f.pf[i].own = INT_MAX;
+  for (int i = threadIdx.x; i < M.cnt_slots; i += blockDim.x) f.pf[i].own = f.pf[i].inc = INT_MAX;
   off += M.cnt_slots * (int)(sizeof(Pf) / 4);
   f.dm = smem + off;  // filtered kPacked rounds: zero between propagations (propagate_packed)
   for (int i = threadIdx.x; i < M.cnt_slots * M.dm_words; i += blockDim.x) f.dm[i] = 0;
@@ -802,6 +803,7 @@ __device__ __forceinline__ int node_ctl_rank0(const SearchCtl& C, const SearchPa
                                               int pending, bool need_prop) {
   int c = 0;
   prefetch_wait();
+  pf->inc = pf->ctl[3];  // join_objective reads this copy: the next prefetch rewrites ctl[]
   if (P.balance && pending >= P.balance) c |= claim_donation_rank0(Gl, pf) << 1;
   if (need_prop) c |= stop_rank0(C, pf);
   prefetch_ctl(pf, Gl);
