@@ -205,6 +205,7 @@ def time_to_optimum(local, rank, world, dist):
     from paper_2207_12116_b200 import Engine, Model
     from paper_2207_12116_b200.distributed import attach_incumbents, run_solve
     eng = Engine(local, shard_index=rank, shard_count=world)
+    ref = Engine(local, mix_order=-1) if world == 1 else None  # the reference's order alone, for comparison
     attached = False
     out = {}
     for seed in TTO_SEEDS:
@@ -236,9 +237,19 @@ def time_to_optimum(local, rank, world, dist):
                           "nodes": local_r.stats["nodes"],
                           "tree_nodes": local_r.stats["nodes"] - local_r.stats["rematerialised"],
                           "roofline": roofline(st, eng.lowering_info(), sm_mhz)}
+        if ref is not None:
+            rr = ref.load(m).solve(timeout_s=120)
+            out[str(seed)]["reference_order"] = {
+                "status": rr.status, "objective": rr.objective, "t_proof_ms": rr.stats["device_ms"],
+                "t_first_optimal_ms": min((ms for v, ms in rr.improvements if v == rr.objective), default=None),
+                "nodes": rr.stats["nodes"]}
     eng.close()
+    if ref is not None:
+        ref.close()
     return {"config": "rcpsp 30 tasks x 4 resources, random_patterson(mt19937_64(seed)), minimise makespan",
-            "note": "node counts differ from the CPU only through search order and incumbent timing",
+            "note": "node counts differ from the CPU only through search order and incumbent timing; the "
+                    "default search mixes branching orders (every 48th group branches by smallest lb, LST "
+                    "ties: cfg mix_order), 'reference_order' is the same solve in branch()'s order alone",
             "gpu": out}
 
 
@@ -311,7 +322,8 @@ def rcpsp120(local, rank, world, dist, budget_s):
     from paper_2207_12116_b200.distributed import attach_incumbents
     m = Model.rcpsp_random(1, 120, 4)
     sm = load_peaks().get("sm_max_mhz", 1965.0)
-    with Engine(local, shard_index=rank, shard_count=world) as e0:  # unlinked: nothing to share
+    # the reference's order alone: no mixed orders (cfg mix_order -1)
+    with Engine(local, shard_index=rank, shard_count=world, mix_order=-1) as e0:  # unlinked: nothing to share
         e0.load(m)
         r0 = e0.solve(timeout_s=3.0)
         ref_order = {"status": r0.status, "nodes": r0.stats["nodes"], "device_ms": r0.stats["device_ms"],
@@ -324,7 +336,7 @@ def rcpsp120(local, rank, world, dist, budget_s):
     # per node, not the same work faster
     os.environ["PCCP_PACKED_FILTER"] = "0"
     try:
-        with Engine(local, shard_index=rank, shard_count=world) as e1:
+        with Engine(local, shard_index=rank, shard_count=world, mix_order=-1) as e1:
             e1.load(m)
             r1 = e1.solve(timeout_s=3.0)
             ref_order["eventless"] = {"nodes": r1.stats["nodes"], "device_ms": r1.stats["device_ms"],

@@ -129,6 +129,11 @@ typedef struct pccp_gpu_cfg {
   int32_t audit_shift;
   int32_t record_frontier; /* 1: keep the hashes of the last search's shared EPS frontier and of this
                               shard's share of it (pccp_gpu_frontier; tests of the partition) */
+  int32_t mix_order;     /* minimisation, a portfolio of branching orders: every mix_order-th search
+                            group branches in var_order 2 (smallest lb, latest start on ties) inside
+                            whatever box it explores, the others in the cfg's var_order.  Every box
+                            is still searched completely, so optima and proofs are unchanged; node
+                            counts differ.  0 = auto (the measured default), -1 = off. */
 } pccp_gpu_cfg;
 
 typedef struct pccp_limits {

@@ -54,6 +54,7 @@ class PccpGpuCfg(C.Structure):
         ("audit_nodes", C.c_int32),
         ("audit_shift", C.c_int32),
         ("record_frontier", C.c_int32),
+        ("mix_order", C.c_int32),
     ]
 
 

@@ -82,6 +82,10 @@ struct DBuf {
 
 std::uint32_t align4(std::uint32_t x) { return (x + 3u) & ~3u; }
 
+// cfg.mix_order = 0: every kMixOrder-th group of a minimisation branches in
+// var_order 2 (measured: the six RCPSP30 parity seeds, DESIGN "Mixed orders").
+constexpr int kMixOrder = 48;
+
 double now_ms() {
   return std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now().time_since_epoch()).count();
 }
@@ -662,6 +666,11 @@ void run_search(pccp_gpu_ctx* c, int mode, const int32_t* root_words, int depth_
     // dynamic load balancing: per-group mailboxes + the wait ring
     P.balance = std::getenv("PCCP_NO_BALANCE") ? 0 : 2;
     if (const char* dm = std::getenv("PCCP_DONATE_MIN")) P.balance = std::max(1, std::atoi(dm));
+    if (const char* dd = std::getenv("PCCP_DONATE_DEEP")) P.donate_deep = std::atoi(dd) != 0 ? 1 : 0;
+    // a portfolio of branching orders for minimisation (cfg.mix_order; kMixOrder
+    // measured on the RCPSP30 parity seeds, DESIGN "Mixed orders")
+    P.mix_order = c->cfg.mix_order > 0 ? c->cfg.mix_order : (c->cfg.mix_order == 0 ? kMixOrder : 0);
+    if (const char* mo = std::getenv("PCCP_MIX_ORDER")) P.mix_order = std::max(0, std::atoi(mo));
     P.n_groups = c->groups();
     P.mb_stride = mb_stride;
     CK(cudaMemsetAsync(c->mailbox.p, 0, (size_t)P.n_groups * P.mb_stride * 4, c->stream));

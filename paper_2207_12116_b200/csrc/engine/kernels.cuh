@@ -912,13 +912,13 @@ __device__ bool eval_wrows(const G& g, unsigned sb, const Tab<TS>& tab, const De
     const int row = base + my;
     const bool act = row < n_rows;
     const int4 meta = act ? tab.ld4(L.wrow_meta, row) : make_int4(0, INT_MAX, 0, 0);  // {chunk0, c, lsum, bit0}
-    const int4 P = act ? tab.ld4(L.wpat, meta.x + q) : make_int4(0, 0, 0, 0);          // {T, U0, U1, U2}
     const unsigned bit = (unsigned)meta.w + 32u * (unsigned)q, sh = bit & 31u;
     const unsigned a = sp + ((bit >> 5) << 3);
-    if constexpr (Filt) {
-      const bool d = act && P.x && (stest(cp, bit >> 5) | (sh ? stest(cp, (bit >> 5) + 1u) : 0u));
+    if constexpr (Filt) {  // before the chunk's table entry is fetched
+      const bool d = act && (stest(cp, bit >> 5) | (sh ? stest(cp, (bit >> 5) + 1u) : 0u));
       if (!__any_sync(kFull, d)) continue;
     }
+    const int4 P = act ? tab.ld4(L.wpat, meta.x + q) : make_int4(0, 0, 0, 0);  // {T, U0, U1, U2}
     const unsigned alsum = sb + ((unsigned)meta.z << 2);
     const int lsum_now = act && q == 0 ? sld(alsum) : INT_MAX;
     unsigned lbw = 0u, ubw = 0u;
@@ -1384,9 +1384,9 @@ __device__ __forceinline__ unsigned mix24(unsigned x) {
 }
 template <class G>
 __device__ int branch(const G& g, volatile int* S, const int* __restrict__ T, const DeviceLayout& L, int& lbw,
-                      int& mid) {
+                      int& mid, int vo_group = -1) {
   unsigned long long best = ~0ull;
-  const unsigned vo = L.var_order;
+  const unsigned vo = vo_group >= 0 ? (unsigned)vo_group : L.var_order;
   if (vo <= 1) {
     for (int i = g.rank(); i < (int)L.n_cand; i += g.size()) {
       const int w = T[L.cand_lbw + i];

@@ -204,7 +204,8 @@ __device__ void record_solution(const G& g, volatile int* S, const DeviceLayout&
 // must be expanded (lbw/mid set), 0 when it is a leaf, -1 on a model error.
 template <int F = kAllFamilies, class G>
 __device__ int classify(const G& g, volatile int* S, const int* __restrict__ T, const DeviceLayout& L,
-                        const SearchCtl& C, Cnt& cnt, bool failed, int depth, int& lbw, int& mid, Pf* pf = nullptr) {
+                        const SearchCtl& C, Cnt& cnt, bool failed, int depth, int& lbw, int& mid, Pf* pf = nullptr,
+                        int vo = -1) {
   if (failed) {
     if (C.count && g.rank() == 0) ++cnt.fails;
     return 0;
@@ -214,7 +215,7 @@ __device__ int classify(const G& g, volatile int* S, const int* __restrict__ T, 
     if constexpr (F == kNeOnly) cnt.hash += store_hash(S, (int)L.n_words);
     else cnt.hash += store_hash_ref(S, C.blob, L);
   }
-  const int b = branch(g, S, T, L, lbw, mid);
+  const int b = branch(g, S, T, L, lbw, mid, vo);
   if (b < 0) {
     if (g.rank() == 0) {
       C.G->error_code = 1;
@@ -687,6 +688,8 @@ struct SearchParams {
   int entry_stride;  // words per entry: store + (lbw, mid, depth)
   // dynamic load balancing (donation of the shallowest pending right branch)
   int balance;       // 0: off; else the pending branches a group needs before it donates one
+  int donate_deep;   // 1: donate the deepest pending branch (the sibling nearest the group's DFS position)
+  int mix_order;     // > 0: groups gid % mix_order == 0 branch in var_order 2 (minimisation)
   int* mailbox;      // per group: store (n_words) + (unused, depth, state)
   int mb_stride;
   int* waitq;        // ring of idle group ids (-1: empty)
@@ -773,7 +776,8 @@ __device__ __forceinline__ int claim_donation_rank0(Globals* Gl, const Pf* pf) {
 // After a claim: take the receiver from the wait ring and hand it the
 // shallowest pending node.
 template <class G>
-__device__ __forceinline__ void hand_over(const G& g, const SearchParams& P, Globals* Gl, int* stk, int nw, int& bot) {
+__device__ __forceinline__ void hand_over(const G& g, const SearchParams& P, Globals* Gl, int* stk, int nw, int& bot,
+                                          int& sp) {
   int recv = -1;
   if (g.rank() == 0) {
     const unsigned h = atomicAdd(&Gl->wait_head, 1u) % (unsigned)P.n_groups;
@@ -784,7 +788,8 @@ __device__ __forceinline__ void hand_over(const G& g, const SearchParams& P, Glo
     atomicAdd(&Gl->donations, 1ull);
   }
   recv = g.bcast0(recv);
-  const int* ent = stk + (size_t)bot * P.entry_stride;
+  const int at = P.donate_deep ? sp - 1 : bot;
+  const int* ent = stk + (size_t)at * P.entry_stride;
   int* dst = P.mailbox + (size_t)recv * P.mb_stride;
   for (int i = g.rank(); i < nw; i += g.size()) dst[i] = ent[i];
   g.sync();
@@ -794,7 +799,8 @@ __device__ __forceinline__ void hand_over(const G& g, const SearchParams& P, Glo
     __threadfence();
     *(volatile int*)&dst[nw + 2] = 1;
   }
-  ++bot;
+  if (P.donate_deep) --sp;
+  else ++bot;
 }
 
 // Rank 0's control for the next node of a CTA group: claim (bit 1), stop
@@ -847,6 +853,11 @@ __global__ void __launch_bounds__(MaxThreads<G, F>::value, MaxThreads<G, F>::min
   const unsigned dm = F == kPackedF ? dm_addr<G>(f) : 0u;
   bool queue_open = true;
   const bool right_first = P.value_order == 1 || (P.value_order == 2 && (gid & 1));
+  // mixed orders (minimisation): every mix_order-th group branches by the
+  // smallest lb, latest start first (var_order 2, the primal dives' order)
+  // inside whatever box it explores; every box is still searched completely,
+  // so proofs and optima are unchanged (DESIGN: mixed orders)
+  const int vo = P.mix_order > 0 && C.mode == 1 && gid % P.mix_order == 0 ? 2 : -1;
   for (;;) {
     int depth = P.depth0;
     bool need_prop = C.mode == 1;
@@ -943,7 +954,7 @@ __global__ void __launch_bounds__(MaxThreads<G, F>::value, MaxThreads<G, F>::min
         }
         ctl = g.bcast0(ctl);
       }
-      if (ctl & 2) hand_over(g, P, Gl, stk, nw, bot);
+      if (ctl & 2) hand_over(g, P, Gl, stk, nw, bot, sp);
       int lbw = 0, mid = 0, e;
       if (need_prop) {
         if (ctl & 1) {
@@ -976,9 +987,9 @@ __global__ void __launch_bounds__(MaxThreads<G, F>::value, MaxThreads<G, F>::min
           if (remat) atomicAdd(&Gl->rematerialised, 1ull);
         }
         remat = false;
-        e = classify<F>(g, S, f.T, L, C, cnt, failed, depth, lbw, mid, pf);
+        e = classify<F>(g, S, f.T, L, C, cnt, failed, depth, lbw, mid, pf, vo);
       } else {
-        e = branch(g, S, f.T, L, lbw, mid);
+        e = branch(g, S, f.T, L, lbw, mid, vo);
       }
       if (e < 0) {
         abandoned = true;

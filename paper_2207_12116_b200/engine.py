@@ -50,11 +50,11 @@ class Engine:
     def __init__(self, device: int = 0, *, group_threads: int = 0, groups_per_cta: int = 0, ctas_per_sm: int = 0,
                  eps_factor: int = 0, shard_index: int = 0, shard_count: int = 1, hash: bool = False,
                  value_order: int = -1, var_order: int = 0, primal_ms: int = 0, audit_nodes: int = 0,
-                 audit_shift: int = 0, record_frontier: bool = False, verbose: bool = False):
+                 audit_shift: int = 0, record_frontier: bool = False, verbose: bool = False, mix_order: int = 0):
         L = N.lib()
         self.cfg = N.PccpGpuCfg(device, group_threads, groups_per_cta, ctas_per_sm, eps_factor, shard_index,
                                 shard_count, int(hash), int(verbose), value_order, var_order, primal_ms, audit_nodes,
-                                audit_shift, int(record_frontier))
+                                audit_shift, int(record_frontier), mix_order)
         h = C.c_void_p()
         N.check(L.pccp_gpu_open(C.byref(self.cfg), C.byref(h)))
         self._h = h
