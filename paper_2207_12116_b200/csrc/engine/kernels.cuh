@@ -691,11 +691,11 @@ __device__ __forceinline__ bool eval_small(volatile int* S, const int* __restric
 // change this round, issued return-free like eval_ne_fast's.
 constexpr int kRowTerms = 8;
 template <class G, bool TS, bool Pair>
-__device__ bool eval_rows_fast(const G& g, unsigned sb, const Tab<TS>& tab, const DeviceLayout& L) {
-  const int R = (int)L.row_lanes;
+__device__ bool eval_rows_fast(const G& g, unsigned sb, const Tab<TS>& tab, const DeviceLayout& L, bool& fl) {
+  const int R = (int)L.row_lanes, lg = (int)L.row_lg;  // R = 2^lg: shifts, not divisions (CSP: 10% of instructions)
   const int sub = g.rank() & (R - 1);
-  const int per_pass = g.size() / R;
-  const int my = g.rank() / R;
+  const int per_pass = g.size() >> lg;
+  const int my = g.rank() >> lg;
   const int n_rows = (int)L.n_rows;
   const unsigned off_meta = L.row_meta, off_terms = L.row_terms;
   unsigned ch = 0;
@@ -707,7 +707,7 @@ __device__ bool eval_rows_fast(const G& g, unsigned sb, const Tab<TS>& tab, cons
     const int4 meta = act ? tab.ld4(off_meta, row) : make_int4(0, 0, INT_MAX, 0);  // {beg, end, c, lsum}
     const int j0 = meta.x + sub, end = meta.y, c = meta.z;
     const unsigned alsum = sb + ((unsigned)meta.w << 2);
-    const int n_my = end > j0 ? (end - j0 + R - 1) / R : 0;  // this lane's terms (<= kRowTerms)
+    const int n_my = end > j0 ? (end - j0 + R - 1) >> lg : 0;  // this lane's terms (<= kRowTerms)
 #pragma unroll
     for (int t = 0; t < kRowTerms; ++t) x[t] = t < n_my ? tab.ld1(off_terms, j0 + t * R) : 0;
     const int lsum_now = act && sub == 0 ? sld(alsum) : INT_MAX;  // snapshot for the lsum join
@@ -731,6 +731,7 @@ __device__ bool eval_rows_fast(const G& g, unsigned sb, const Tab<TS>& tab, cons
         sred_max(alsum, cell);
         ch = 1u;
       }
+      if (sub == 0 && (over || lsum_now == INT_MAX)) fl = true;  // the cell is (or becomes) top: failed
       if (c != INT_MAX) {
 #pragma unroll
         for (int t = 0; t < kRowTerms; ++t) {
@@ -758,13 +759,16 @@ __device__ bool eval_rows_fast(const G& g, unsigned sb, const Tab<TS>& tab, cons
   return ch != 0;
 }
 
+// fl: set when a row's lsum cell is (or becomes) top (the overload rule), the
+// failure the scalar scan would find (skipped when every scalar is a row's cell).
 template <class G, bool TS>
-__device__ bool eval_rows(const G& g, unsigned sb, const Tab<TS>& tab, const DeviceLayout& L) {
-  if (L.rows_fast) return L.row_even ? eval_rows_fast<G, TS, true>(g, sb, tab, L) : eval_rows_fast<G, TS, false>(g, sb, tab, L);
-  const int R = (int)L.row_lanes;
+__device__ bool eval_rows(const G& g, unsigned sb, const Tab<TS>& tab, const DeviceLayout& L, bool& fl) {
+  if (L.rows_fast)
+    return L.row_even ? eval_rows_fast<G, TS, true>(g, sb, tab, L, fl) : eval_rows_fast<G, TS, false>(g, sb, tab, L, fl);
+  const int R = (int)L.row_lanes, lg = (int)L.row_lg;
   const int sub = g.rank() & (R - 1);
-  const int per_pass = g.size() / R;
-  const int my = g.rank() / R;
+  const int per_pass = g.size() >> lg;
+  const int my = g.rank() >> lg;
   bool ch = false;
   for (int base = 0; base < (int)L.n_rows; base += per_pass) {
     const int row = base + my;
@@ -784,7 +788,11 @@ __device__ bool eval_rows(const G& g, unsigned sb, const Tab<TS>& tab, const Dev
       const int c = tab.ld1(L.row_c, row);
       const int lsum = narrow(s);
       const int cell = lsum > c ? INT_MAX : lsum;  // [lsum > c] => lsum <- +inf
-      if (sub == 0) ch |= sjoin_max(sb + ((unsigned)tab.ld1(L.row_lsum, row) << 2), cell);
+      if (sub == 0) {
+        const unsigned al = sb + ((unsigned)tab.ld1(L.row_lsum, row) << 2);
+        ch |= sjoin_max(al, cell);
+        if (cell == INT_MAX || sld(al) == INT_MAX) fl = true;
+      }
       if (c != INT_MAX) {
         const long long wl = tv(1, cell);
         for (int j = beg + sub; j < end; j += R) {
@@ -1056,7 +1064,7 @@ __device__ __forceinline__ void dbg_r(int k) {
 // One round of every family but NE (propagate below).
 template <class G, bool TS>
 __device__ __forceinline__ bool eval_other_families(const G& g, volatile int* S, unsigned sb, const Tab<TS>& tab,
-                                                    const DeviceLayout& L) {
+                                                    const DeviceLayout& L, bool& fl) {
     const int* __restrict__ T = tab.p;
     bool ch = false;
     if (L.reif8) {  // packed, 8-byte records
@@ -1106,11 +1114,8 @@ __device__ __forceinline__ bool eval_other_families(const G& g, volatile int* S,
     dbg_r(1);
     for (int i = g.rank(); i < (int)L.n_small; i += g.size()) ch |= eval_small(S, T, L, i);
     dbg_r(2);
-    if (L.n_rows) ch |= eval_rows(g, sb, tab, L);
-    if (L.n_brows) {
-      bool fl_unused = false;  // the scalar scan finds overloaded rows here
-      ch |= L.wrows ? eval_wrows(g, sb, tab, L, g.rank(), fl_unused) : eval_brows(g, sb, tab, L);
-    }
+    if (L.n_rows) ch |= eval_rows(g, sb, tab, L, fl);
+    if (L.n_brows) ch |= L.wrows ? eval_wrows(g, sb, tab, L, g.rank(), fl) : eval_brows(g, sb, tab, L);
     dbg_r(3);
     for (int i = g.rank(); i < (int)L.n_gen; i += g.size())
       ch |= eval_generic(S, T + L.gen_code + T[L.gen_off + i]);
@@ -1313,7 +1318,7 @@ __device__ bool propagate(const G& g, volatile int* S, unsigned sb, const Tab<TS
       ch = packed_round(g, sb, tab, L, fl);
     } else {
     ch = ne_round(g, sb, tab, L);
-    if constexpr (F == kAllFamilies) ch |= eval_other_families(g, S, sb, tab, L);
+    if constexpr (F == kAllFamilies) ch |= eval_other_families(g, S, sb, tab, L, fl);
     // The scan may see an intermediate state: failure is monotone, and a join
     // after it changed a word, so the next round scans again (H8).
     // NE-only kernels keep the plain test (iv_dense): the extra scalar branch
@@ -1331,7 +1336,7 @@ __device__ bool propagate(const G& g, volatile int* S, unsigned sb, const Tab<TS
           fl |= v.x > v.y;
         }
       }
-      if (F == kAllFamilies && !L.iv_dense)
+      if (F == kAllFamilies && !L.iv_dense && !L.sc_in_rows)  // (every scalar a row's cell: the rows report it)
         for (int i = g.rank(); i < (int)L.n_sc; i += g.size())
           fl |= sld(sb + 4u * (unsigned)tab.ld1(L.sc_w, i)) == tab.ld1(L.sc_top, i);
       if (F == kAllFamilies && L.packed)  // bit cells: empty = both bits
@@ -1344,8 +1349,9 @@ __device__ bool propagate(const G& g, volatile int* S, unsigned sb, const Tab<TS
         const unsigned a = sb + 4u * (unsigned)tab.ld1(L.iv_lb, i);
         fl |= sld(a) > sld(a + 4);
       }
-      for (int i = g.rank(); i < (int)L.n_sc; i += g.size())
-        fl |= sld(sb + 4u * (unsigned)tab.ld1(L.sc_w, i)) == tab.ld1(L.sc_top, i);
+      if (!L.sc_in_rows)
+        for (int i = g.rank(); i < (int)L.n_sc; i += g.size())
+          fl |= sld(sb + 4u * (unsigned)tab.ld1(L.sc_w, i)) == tab.ld1(L.sc_top, i);
       if (F == kAllFamilies && L.packed)
         for (int i = g.rank(); i < (int)L.n_pairs; i += g.size()) {
           const int2 P = sld2(sb + 4u * (L.plane + 2u * (unsigned)i));

@@ -1072,6 +1072,8 @@ Lowered lower_impl(const pccp_model& m, bool want_bits) {
     const unsigned v = static_cast<unsigned>(std::atoi(rl));
     if (v >= 1 && v <= 32 && (v & (v - 1)) == 0) L.row_lanes = v;
   }
+  L.row_lg = 0;
+  while ((1u << L.row_lg) < L.row_lanes) ++L.row_lg;
   L.row_off = reserve_arr(L.n_rows + 1);
   L.row_lsum = reserve_arr(L.n_rows);
   L.row_c = reserve_arr(L.n_rows);
@@ -1324,9 +1326,14 @@ Lowered lower_impl(const pccp_model& m, bool want_bits) {
     if (iv[i] != static_cast<std::int32_t>(2 * i)) L.iv_prefix = 0;
   L.iv_dense = !packed && L.iv_prefix && L.n_iv * 2 == m.n_words ? 1 : 0;
   L.n_sc = static_cast<std::uint32_t>(scw.size());
-  if (L.wrows) {  // a row's lsum is private to it (match_row): overload is its only way to top
+  // Every scalar a row's lsum cell, and every row reporting its overload
+  // (kernels.cuh eval_rows, eval_wrows; not the per-term bit rows): the
+  // failure scan skips the scalars.  A row's lsum is private to it
+  // (match_row), so the overload rule is its only way to top.
+  if (!scw.empty() && (bit_rows.empty() || L.wrows) && !std::getenv("PCCP_SCALAR_SCAN")) {
     std::vector<std::uint8_t> is_lsum(DW + 1, 0);
     for (const Row& r : bit_rows) is_lsum[r.lsum] = 1;
+    for (const Row& r : rows) is_lsum[r.lsum] = 1;
     L.sc_in_rows = 1;
     for (std::int32_t w : scw)
       if (!is_lsum[static_cast<std::uint32_t>(w)]) L.sc_in_rows = 0;
