@@ -707,12 +707,23 @@ struct SearchParams {
 };
 
 // Pop from an epoch-tagged share cell (Globals::qcell): k < n_share of this
-// epoch, or -1.  A cell still tagged with an older epoch (its owner has not
-// started this search) gets this epoch installed by whoever comes first — the
-// owner or a thief — with position 0 going to the installer; every position
-// of an epoch is handed out once, whoever pops it.  Linked shards run the
-// same sequence of sharded searches (epochs 1, 2, ...), on the same root.
-__device__ __forceinline__ long long qpop(unsigned long long* q, unsigned e, long long n_share) {
+// epoch, or -1.  Only the owner installs its epoch on a cell still tagged with
+// an older one (position 0 goes to it); a thief takes positions only from
+// shares whose owner has started this search, so it never empties the share
+// of a peer that is merely a moment late, only the tails of running ones.
+// Every position of an epoch is handed out once, whoever pops it.  Linked
+// shards run the same sequence of sharded searches (epochs 1, 2, ...), on the
+// same root.
+__device__ __forceinline__ long long qpop(unsigned long long* q, unsigned e, long long n_share, bool owner) {
+  if (!owner) {  // a thief: compare-and-swap, so it never moves a cell of another epoch
+    unsigned long long v = atomicAdd_system(q, 0ull);
+    for (;;) {
+      if ((unsigned)(v >> 32) != e || (long long)(unsigned)v >= n_share) return -1;
+      const unsigned long long prev = atomicCAS_system(q, v, v + 1);
+      if (prev == v) return (long long)(unsigned)v;
+      v = prev;
+    }
+  }
   for (;;) {
     const unsigned long long v = atomicAdd_system(q, 1ull);
     const unsigned ep = (unsigned)(v >> 32);
@@ -733,11 +744,11 @@ __device__ __forceinline__ long long qpop(unsigned long long* q, unsigned e, lon
 __device__ __forceinline__ long long steal_pop(const SearchParams& P, Globals* Gl) {
   const long long N = P.shard_count, n = P.n_frontier;
   auto share = [&](long long s) { return n > s ? (n - s + N - 1) / N : 0ll; };
-  long long k = qpop(P.own_q, P.epoch, share(P.shard_index));
+  long long k = qpop(P.own_q, P.epoch, share(P.shard_index), true);
   if (k >= 0) return P.shard_index + k * N;
   for (int j = 0; j < P.n_peers; ++j) {
     const int s = P.peer_shard[j];
-    k = qpop(&P.peers[j]->qcell, P.epoch, share(s));
+    k = qpop(&P.peers[j]->qcell, P.epoch, share(s), false);
     if (k >= 0) {
       atomicAdd(&Gl->stolen, 1ull);
       return s + k * N;

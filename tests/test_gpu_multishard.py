@@ -194,28 +194,33 @@ def test_sharded_micro_rcpsp_optima(n_shards):
 
 # ---- cross-GPU work stealing -----------------------------------------------------
 # Linked shards pop their share of the shared phase-A frontier from an
-# epoch-tagged cell and, once it is exhausted, take positions from the peers'
-# cells (search.cuh steal_pop).  Run one after the other, shard 0 finds every
-# peer share untouched and drains all of them: no shard waits while another
-# share still has subproblems, and every position is processed exactly once.
-@pytest.mark.parametrize("n_shards", [2, 4])
-def test_linked_enumeration_steals_and_stays_exact(n_shards, golden):
-    import numpy as np
-
-    from paper_2207_12116_b200 import Engine, Model
-    from paper_2207_12116_b200.distributed import combine_enum
+# epoch-tagged cell and, once it is exhausted, take positions from the cells of
+# peers that have started the same search (search.cuh steal_pop, qpop).
+def _linked(m, n, **cfg):
+    from paper_2207_12116_b200 import Engine
     from paper_2207_12116_b200.engine import link_peers
+    # one group per SM: a shared frontier of 148 x N nodes, well inside these trees
+    engs = [Engine(0, shard_index=k, shard_count=n, hash=True, record_frontier=True, ctas_per_sm=1,
+                   groups_per_cta=1, **cfg) for k in range(n)]
+    for e in engs:
+        e.load(m)
+    link_peers(engs)
+    return engs
+
+
+@pytest.mark.parametrize("n_shards", [2, 4])
+def test_linked_enumeration_stays_exact(n_shards, golden):
+    """One after the other, each shard finds its peers' shares not started
+    (a thief never installs a peer's epoch): it drains its own share, and the
+    counts and the partition are exact; twice on the same contexts (epochs 1, 2)."""
+    from paper_2207_12116_b200 import Model
+    from paper_2207_12116_b200.distributed import combine_enum
     for name, depth in (("nqueens10", -1), ("csp1", 22)):
         m = Model.nqueens(10) if name == "nqueens10" else Model.random_csp(1)
         g = golden[name]["enumerate" if depth < 0 else "enumerate_d22"]
-        # one group per SM: a shared frontier of 148 x N nodes, well inside these trees
-        engs = [Engine(0, shard_index=k, shard_count=n_shards, hash=True, record_frontier=True, ctas_per_sm=1,
-                       groups_per_cta=1) for k in range(n_shards)]
+        engs = _linked(m, n_shards)
         try:
-            for e in engs:
-                e.load(m)
-            link_peers(engs)
-            for rep in range(2):  # a second sharded search on the same contexts (epoch 2)
+            for rep in range(2):
                 parts, fronts = [], []
                 for e in engs:
                     parts.append(e.enumerate(depth_cap=depth))
@@ -224,13 +229,67 @@ def test_linked_enumeration_steals_and_stays_exact(n_shards, golden):
                 for key in ("nodes", "failures", "solutions", "open_leaves", "hash_sum"):
                     assert tot[key] == g[key], (name, n_shards, rep, key)
                 assert tot["exhausted"]
-                _check_partition(fronts)
                 assert fronts[0][0].size > 0, (name, rep)
-                assert parts[0]["stolen"] > 0 and fronts[0][1].size == fronts[0][0].size, (name, rep)
-                assert all(f[1].size == 0 for f in fronts[1:])  # nothing was left for the later shards
+                _check_partition(fronts)
+                assert all(p["stolen"] == 0 for p in parts)
+                assert all(f[1].size == len(range(k, f[0].size, n_shards)) for k, f in enumerate(fronts))
         finally:
             for e in engs:
                 e.close()
+
+
+def test_stealing_takes_a_started_peers_tail():
+    """Shard 0 starts, pops a few positions and stops at a node limit, leaving
+    its share's tail in its cell; shard 1 then drains its own share and takes
+    shard 0's untouched positions: every position went to exactly one shard."""
+    import numpy as np
+
+    from paper_2207_12116_b200 import Model
+    m = Model.random_csp(1)
+    engs = _linked(m, 2)
+    try:
+        r0 = engs[0].enumerate(depth_cap=22, node_limit=2000)
+        a0, s0 = engs[0].frontier()
+        r1 = engs[1].enumerate(depth_cap=22)
+        a1, s1 = engs[1].frontier()
+        assert not r0["exhausted"] and r0["stolen"] == 0
+        assert r1["stolen"] > 0 and s1.size > len(range(1, a1.size, 2))
+        assert np.array_equal(np.sort(a0), np.sort(a1))
+        both = np.concatenate([s0, s1])
+        assert len(np.unique(both)) == both.size  # no position processed twice
+    finally:
+        for e in engs:
+            e.close()
+
+
+@pytest.mark.parametrize("n_shards", [2, 4])
+def test_concurrent_linked_shards(n_shards, golden):
+    """N linked shards searching at once on one device (host threads, one CTA
+    per SM each): exact counts and a partition of the frontier, whoever stole."""
+    import threading
+
+    from paper_2207_12116_b200 import Model
+    from paper_2207_12116_b200.distributed import combine_enum
+    m = Model.random_csp(1)
+    g = golden["csp1"]["enumerate_d22"]
+    engs = _linked(m, n_shards)
+    try:
+        for rep in range(2):
+            parts = [None] * n_shards
+            th = [threading.Thread(target=lambda k=k: parts.__setitem__(k, engs[k].enumerate(depth_cap=22)))
+                  for k in range(n_shards)]
+            for t in th:
+                t.start()
+            for t in th:
+                t.join()
+            fronts = [e.frontier() for e in engs]
+            tot = combine_enum(parts)
+            for key in ("nodes", "failures", "solutions", "open_leaves", "hash_sum"):
+                assert tot[key] == g[key], (n_shards, rep, key)
+            _check_partition(fronts)
+    finally:
+        for e in engs:
+            e.close()
 
 
 def test_unlinked_shards_keep_the_static_split(golden):
