@@ -171,6 +171,8 @@ typedef struct pccp_stats {
                               subproblem roots (solver.cpp:266-268); distinct tree nodes = nodes -
                               rematerialised */
   uint64_t stolen;      /* N linked shards: frontier subproblems this shard took from peers' shares */
+  uint64_t remote_in;   /* N linked shards: pending branches donated to this GPU by peers */
+  uint64_t remote_out;  /* ... and by this GPU to peers */
 } pccp_stats;
 
 typedef struct pccp_enum_result {

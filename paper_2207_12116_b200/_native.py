@@ -85,6 +85,8 @@ class PccpStats(C.Structure):
         ("donations", C.c_uint64),
         ("rematerialised", C.c_uint64),
         ("stolen", C.c_uint64),
+        ("remote_in", C.c_uint64),
+        ("remote_out", C.c_uint64),
     ]
 
 

@@ -124,7 +124,7 @@ struct pccp_gpu_ctx {
   int plan_occ = 0, plan_occ_dec = 0;
   std::uint32_t audit_taken = 0;  // node-audit samples of the last search
 
-  DBuf<int> fa, fb, ia, ib, stack, best, io, mailbox, waitq, dec, chunk, audit;
+  DBuf<int> fa, fb, ia, ib, stack, best, io, mailbox, dec, chunk, audit;  // (the wait ring lives behind Globals)
   DBuf<unsigned char> flags, st;
   DBuf<unsigned> rnd;
   dev::Globals* G = nullptr;
@@ -307,6 +307,8 @@ void plan(pccp_gpu_ctx* c) {
     c->plan_occ_dec = occ_dec;
   }
   if (occ_dec < 1) throw LimitError("decomposition kernel does not fit on an SM");
+  if ((long long)c->n_sm * std::max(occ, 1) * (c->warp ? c->gpc : 1) > dev::kMaxGroups)
+    throw LimitError("more search groups than the wait ring holds");
   if (occ < 1) throw LimitError("kernel does not fit on an SM (smem " + std::to_string(c->smem) + " B)");
   if (c->cfg.ctas_per_sm > 0) occ = std::min(occ, c->cfg.ctas_per_sm);
   c->ctas = c->n_sm * occ;
@@ -518,7 +520,6 @@ void run_search(pccp_gpu_ctx* c, int mode, const int32_t* root_words, int depth_
   if (rflag) {
     c->stack.ensure((size_t)c->groups() * (size_t)dmax * (size_t)entry);
     c->mailbox.ensure((size_t)c->groups() * (size_t)mb_stride);
-    c->waitq.ensure((size_t)c->groups());
   }
 
   // EPS decomposition: whole BFS levels until the frontier holds target nodes.
@@ -674,13 +675,13 @@ void run_search(pccp_gpu_ctx* c, int mode, const int32_t* root_words, int depth_
     P.n_groups = c->groups();
     P.mb_stride = mb_stride;
     CK(cudaMemsetAsync(c->mailbox.p, 0, (size_t)P.n_groups * P.mb_stride * 4, c->stream));
-    CK(cudaMemsetAsync(c->waitq.p, 0xff, (size_t)P.n_groups * 4, c->stream));
+    CK(cudaMemsetAsync(dev::waitq_of(c->G), 0xff, (size_t)P.n_groups * 4, c->stream));
     const int active = P.n_groups;
     CK(cudaMemcpyAsync(&c->G->active, &active, sizeof(int), cudaMemcpyHostToDevice, c->stream));
     P.mailbox = c->mailbox.p;
     P.value_order = c->cfg.value_order >= 0 ? std::min(c->cfg.value_order, 2) : 0;
     if (const char* vo = std::getenv("PCCP_VALUE_ORDER")) P.value_order = std::atoi(vo);
-    P.waitq = c->waitq.p;
+    P.waitq = dev::waitq_of(c->G);
     if (steal) {  // the whole shared frontier; positions come from the share cells
       P.shard_index = shard_index;
       P.shard_count = shard_count;
@@ -694,6 +695,14 @@ void run_search(pccp_gpu_ctx* c, int mode, const int32_t* root_words, int depth_
         c->qlog.ensure((size_t)count);
         P.qlog = c->qlog.p;
       }
+      // cross-GPU donation of pending branches (search.cuh hand_over_remote)
+      P.remote = !c->warp && nw + 3 <= dev::kSlotWords && !std::getenv("PCCP_NO_REMOTE_DONATE") ? 1 : 0;  // CTA groups
+    }
+    {  // what peers read before they donate: the ring's modulus, whether this search takes donations, its epoch
+      const int pub[3] = {P.n_groups, P.remote, (int)P.epoch};
+      static_assert(offsetof(dev::Globals, remote) == offsetof(dev::Globals, n_groups_pub) + sizeof(int), "layout");
+      static_assert(offsetof(dev::Globals, epoch_pub) == offsetof(dev::Globals, remote) + sizeof(int), "layout");
+      CK(cudaMemcpyAsync(&c->G->n_groups_pub, pub, sizeof(pub), cudaMemcpyHostToDevice, c->stream));
     }
     C.count = 1;
     if (C.audit_n > 0) dev::k_search<Gp, TS, F, true><<<c->ctas, c->block, c->smem, c->stream>>>(M, C, P);
@@ -745,6 +754,9 @@ void run_search(pccp_gpu_ctx* c, int mode, const int32_t* root_words, int depth_
             (unsigned)nw, L.packed ? " (bit-plane 0/1 cells)" : "", out.root_ms, out.decompose_ms - out.root_ms, count,
             (unsigned long long)level, out.kernel_ms, out.g.nodes, out.g.rounds, out.g.donations,
             out.g.incomplete ? ", incomplete" : "");
+  if (c->cfg.verbose && out.g.incomplete)
+    fprintf(stderr, "pccp_gpu[dev %d shard %d/%d]: incomplete causes %d, stop %d, remote in %llu out %llu\n", c->device,
+            shard_index, shard_count, out.g.why, out.g.stop, out.g.remote_in, out.g.remote_out);
   if (out.g.stop == 2) {
     if (out.g.error_code == 1) throw std::runtime_error("branch: a candidate variable is unbounded");
     throw LimitError("DFS stack capacity exceeded");
@@ -774,6 +786,8 @@ void fill_stats(const pccp_gpu_ctx* c, const RunOut& r, pccp_stats& s) {
   s.donations = r.g.donations;
   s.rematerialised = r.g.rematerialised;
   s.stolen = r.g.stolen;
+  s.remote_in = r.g.remote_in;
+  s.remote_out = r.g.remote_out;
 }
 
 // Counters of consecutive searches of one call (primal segments, exact
@@ -792,6 +806,8 @@ void merge_run(RunOut& acc, const RunOut& r, bool first) {
   g.donations += acc.g.donations;
   g.rematerialised += acc.g.rematerialised;
   g.stolen += acc.g.stolen;
+  g.remote_in += acc.g.remote_in;
+  g.remote_out += acc.g.remote_out;
   acc.g = g;
   acc.bfs_rounds += r.bfs_rounds;
   acc.decompose_ms += r.decompose_ms;
@@ -861,8 +877,9 @@ int pccp_gpu_open(const pccp_gpu_cfg* cfg, pccp_gpu_ctx** out) {
       c->smem_optin = prop.sharedMemPerBlockOptin;
       CK(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
       for (auto& e : c->ev) CK(cudaEventCreate(&e));
-      CK(cudaMalloc(&c->G, sizeof(dev::Globals)));
-      CK(cudaMemset(c->G, 0, sizeof(dev::Globals)));
+      // Globals, the wait ring and the inbox slots in one allocation (one IPC handle maps all)
+      CK(cudaMalloc(&c->G, dev::kGlobalsBytes));
+      CK(cudaMemset(c->G, 0, dev::kGlobalsBytes));
       reset_shared(c);
     } catch (...) {
       pccp_gpu_close(c);
@@ -885,7 +902,6 @@ void pccp_gpu_close(pccp_gpu_ctx* c) {
   c->ib.release();
   c->stack.release();
   c->mailbox.release();
-  c->waitq.release();
   c->dec.release();
   c->chunk.release();
   c->audit.release();
@@ -959,11 +975,9 @@ int pccp_gpu_load(pccp_gpu_ctx* c, const pccp_model* m) {
         try {
           c->stack.ensure(bytes / 4);
           c->mailbox.ensure((size_t)c->groups() * entry);
-          c->waitq.ensure((size_t)c->groups());
-        } catch (const LimitError&) {
+              } catch (const LimitError&) {
           c->stack.release();
           c->mailbox.release();
-          c->waitq.release();
         }
       }
     }

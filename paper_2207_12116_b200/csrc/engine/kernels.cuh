@@ -86,7 +86,31 @@ struct Globals {
   unsigned long long rematerialised;  // frontier nodes materialised again by the search (mode 1)
   unsigned long long qlog_n;          // record_frontier: frontier positions this shard processed
   unsigned long long stolen;          // frontier positions taken from peers' shares
+  // Cross-GPU donation (search.cuh hand_over_remote): a peer's busy group
+  // hands a pending branch to one of this GPU's idle groups through an inbox
+  // slot of this allocation (the wait ring and the slots follow Globals in
+  // the same cudaMalloc, so the IPC handle of Globals maps them too).
+  int running;                        // groups of this GPU's search kernel inside k_search
+  int n_groups_pub;                   // groups of the running search (the wait ring's modulus)
+  int remote;                         // this search receives cross-GPU donations
+  int epoch_pub;                      // its sharded-search epoch: donations only within one epoch
+  int inbox_state[4];                 // 0 free, 1 being written, 2 ready for inbox_rcv, 9 closed
+  int inbox_rcv[4];                   // the receiving group (popped from this GPU's wait ring)
+  int inbox_depth[4];
+  unsigned long long remote_in, remote_out;  // donations received from / sent to peers
+  int why;                            // incomplete: 1 decomposition, 2 abandoned, 4 stopped idle, 8 inbox, 16 pop stop
 };
+
+// The allocation behind a context's Globals: Globals, then the wait ring of
+// idle groups (kMaxGroups ints), then kInbox inbox slots of kSlotWords each.
+constexpr int kMaxGroups = 16384, kInbox = 4, kSlotWords = 16384;
+constexpr size_t kWaitqOffset = (sizeof(Globals) + 255) & ~size_t(255);
+constexpr size_t kInboxOffset = kWaitqOffset + sizeof(int) * kMaxGroups;
+constexpr size_t kGlobalsBytes = kInboxOffset + sizeof(int) * (size_t)kInbox * kSlotWords;
+__host__ __device__ __forceinline__ int* waitq_of(Globals* G) { return (int*)((char*)G + kWaitqOffset); }
+__host__ __device__ __forceinline__ int* inbox_of(Globals* G, int s) {
+  return (int*)((char*)G + kInboxOffset) + (size_t)s * kSlotWords;
+}
 
 __device__ __forceinline__ unsigned long long globaltimer() {
   unsigned long long t;

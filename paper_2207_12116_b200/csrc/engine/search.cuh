@@ -67,7 +67,7 @@ struct alignas(16) Pf {
   int hung[4];  // hungry, padding
   int own;      // best value this group recorded (INT_MAX: none)
   int inc;      // the incumbent of the last completed prefetch (ctl[3] may be in flight again)
-  int pad[2];   // pad[0]: the next node's control word (CTA groups)
+  int pad[2];   // pad[0]: the next node's control word (CTA groups); pad[1]: node tick (remote donation)
 };
 
 __device__ __forceinline__ void prefetch_ctl(Pf* pf, const Globals* G) {
@@ -295,7 +295,10 @@ __device__ __forceinline__ Frame frame(const Model& M) {
     reinterpret_cast<unsigned long long*>(f.cnt)[i] = 0ull;
   off += M.cnt_slots * (int)(sizeof(Cnt) / 4);
   f.pf = reinterpret_cast<Pf*>(smem + off);
-  for (int i = threadIdx.x; i < M.cnt_slots; i += blockDim.x) f.pf[i].own = f.pf[i].inc = INT_MAX;
+  for (int i = threadIdx.x; i < M.cnt_slots; i += blockDim.x) {
+    f.pf[i].own = f.pf[i].inc = INT_MAX;
+    f.pf[i].pad[1] = 0;
+  }
   off += M.cnt_slots * (int)(sizeof(Pf) / 4);
   f.dm = smem + off;  // filtered kPacked rounds: zero between propagations (propagate_packed)
   for (int i = threadIdx.x; i < M.cnt_slots * M.dm_words; i += blockDim.x) f.dm[i] = 0;
@@ -480,7 +483,7 @@ __device__ void expand_level(const G& g, volatile int* S, unsigned sb, const Tab
   for (int p = gid; p < n_par; p += ng) {
     if (time_stop(g, C, 2)) {  // abandoned parent: its subtree is unexplored
       if (g.rank() == 0) {
-        C.G->incomplete = 1;
+        C.G->incomplete = 1; atomicOr(&C.G->why, 1);
         flags[2 * p] = flags[2 * p + 1] = 0;
       }
       g.sync();
@@ -704,6 +707,7 @@ struct SearchParams {
   const int* peer_shard;   // each peer's shard index
   int n_peers;
   int* qlog;               // record_frontier: the positions this shard processed (or null)
+  int remote;              // cross-GPU donation to / from the peers (hand_over_remote)
 };
 
 // Pop from an epoch-tagged share cell (Globals::qcell): k < n_share of this
@@ -814,6 +818,134 @@ __device__ __forceinline__ void hand_over(const G& g, const SearchParams& P, Glo
   else ++bot;
 }
 
+// Cross-GPU donation.  When no group of its own GPU is hungry, a busy group
+// with pending branches looks (every 32nd node) for a peer GPU of the same
+// epoch whose kernel is running with idle groups, and hands one of them its
+// shallowest pending branch, as hand_over does inside a GPU: it claims a free
+// inbox slot (CAS 0 -> 1) and one unit of the peer's hunger, takes the
+// receiver from the peer's wait ring, marks it active, writes the node into
+// the slot through NVLink (peer stores), fences at system scope and flags the
+// slot ready for that receiver.  One hunger unit, one ring entry, one
+// receiver: the same accounting as a local donation.  Idle groups wait for
+// donations while a fully resident peer is busy (peers_busy); a group leaving
+// the kernel closes the inbox first (close_inbox), so no donation lands after
+// the kernel ends.
+// Rank 0: returns (peer << 8 | slot << 16 | 4) or 0.
+__device__ __forceinline__ int claim_remote_rank0(const SearchParams& P, Globals* Gl) {
+  // Donate only while every group of this kernel is resident: then the
+  // receiver's GPU counts this one busy (peers_busy) and keeps its idle
+  // groups — the receiver among them — until the node has landed.  (Its
+  // groups leave only at quiescence, so residency holds while this group is
+  // active.)  On one device a kernel can be partly resident behind another.
+  if (*(volatile int*)&Gl->running < P.n_groups) return 0;
+  for (int j = 0; j < P.n_peers; ++j) {
+    Globals* B = P.peers[j];
+    if (*(volatile int*)&B->running <= 0 || !*(volatile int*)&B->remote || *(volatile int*)&B->stop ||
+        *(volatile int*)&B->epoch_pub != (int)P.epoch)
+      continue;
+    if (*(volatile int*)&B->hungry <= 0) continue;
+    // the slot first: while this group holds it (state 1) the peer cannot
+    // close its inbox, so it cannot exit (nor its host reset the hunger)
+    // under the claim below
+    int slot = -1;
+    for (int k = 0; k < kInbox && slot < 0; ++k)
+      if (atomicCAS_system(&B->inbox_state[k], 0, 1) == 0) slot = k;
+    if (slot < 0) continue;
+    if (atomicAdd_system(&B->hungry, -1) <= 0) {
+      atomicAdd_system(&B->hungry, 1);
+      __threadfence_system();
+      atomicExch_system(&B->inbox_state[slot], 0);
+      continue;
+    }
+    return 4 | (j << 8) | (slot << 16);
+  }
+  return 0;
+}
+
+// Whether a peer of this epoch that may donate runs its whole kernel (every
+// group resident) with an active group: idle groups keep waiting for it.  A
+// peer not fully resident is not waited for — on one device its remaining
+// CTAs may need this kernel's SMs.
+__device__ __forceinline__ bool peers_busy(const SearchParams& P) {
+  for (int j = 0; j < P.n_peers; ++j) {
+    Globals* B = P.peers[j];
+    if (*(volatile int*)&B->remote && *(volatile int*)&B->epoch_pub == (int)P.epoch &&
+        *(volatile int*)&B->running >= *(volatile int*)&B->n_groups_pub && *(volatile int*)&B->active > 0)
+      return true;
+  }
+  return false;
+}
+
+// At quiescence (no active group here, no busy peer) an idle group closes
+// the inbox before it leaves: free slots 0 -> 9, so no donor can claim one
+// afterwards — donors claim a slot before the hunger and the ring entry, so
+// the hunger and ring entries the idle groups leave behind draw no donation.
+// A slot being written or ready (1, 2) means a donation is landing (its donor
+// marks a receiver active first): the group keeps waiting.  Returns whether
+// every slot is closed.
+__device__ __forceinline__ bool close_inbox_quiet(Globals* Gl) {
+  bool all = true;
+  for (int k = 0; k < kInbox; ++k) {
+    const int st = atomicCAS(&Gl->inbox_state[k], 0, 9);
+    if (st != 0 && st != 9) all = false;
+  }
+  return all;
+}
+
+// A group leaving the kernel closes this GPU's inbox (slots 0 -> 9): no donor
+// can claim a slot afterwards, so none writes into cells its host will reset.
+// A slot being written (1) is waited for; a ready one (2) no group will take
+// any more: its node is abandoned (the search is incomplete) and the donor's
+// activation of the receiver is undone, so this GPU can still become quiet.
+__device__ __forceinline__ void close_inbox(Globals* Gl) {
+  for (int k = 0; k < kInbox; ++k) {
+    for (;;) {
+      const int st = *(volatile int*)&Gl->inbox_state[k];
+      if (st == 9) break;
+      if (st == 1) {
+        __nanosleep(100);
+        continue;
+      }
+      if (atomicCAS(&Gl->inbox_state[k], st, 9) != st) continue;
+      if (st == 2) {
+        Gl->incomplete = 1; atomicOr(&Gl->why, 8);
+        atomicAdd(&Gl->active, -1);
+      }
+      break;
+    }
+  }
+}
+
+template <class G>
+__device__ __forceinline__ void hand_over_remote(const G& g, const SearchParams& P, Globals* Gl, int* stk, int nw,
+                                                 int& bot, int ctl) {
+  const int j = (ctl >> 8) & 0xff, slot = (ctl >> 16) & 0xff;
+  Globals* B = P.peers[j];
+  if (g.rank() == 0) {
+    const unsigned n = (unsigned)*(volatile int*)&B->n_groups_pub;
+    const unsigned h = atomicAdd_system(&B->wait_head, 1u) % n;
+    volatile int* wq = waitq_of(B);
+    int recv;
+    while ((recv = wq[h]) < 0) {
+    }
+    wq[h] = -1;
+    atomicAdd_system(&B->active, 1);
+    *(volatile int*)&B->inbox_rcv[slot] = recv;
+    atomicAdd(&Gl->remote_out, 1ull);
+  }
+  const int* ent = stk + (size_t)bot * P.entry_stride;
+  int* dst = inbox_of(B, slot);
+  for (int i = g.rank(); i < nw; i += g.size()) dst[i] = ent[i];
+  g.sync();
+  if (g.rank() == 0) {
+    apply_pending(dst, ent[nw], ent[nw + 1]);
+    *(volatile int*)&B->inbox_depth[slot] = ent[nw + 2] + 1;
+    __threadfence_system();
+    *(volatile int*)&B->inbox_state[slot] = 2;
+  }
+  ++bot;
+}
+
 // Rank 0's control for the next node of a CTA group: claim (bit 1), stop
 // (bit 0), from the prefetched control words, then the next prefetch.
 __device__ __forceinline__ int node_ctl_rank0(const SearchCtl& C, const SearchParams& P, Globals* Gl, Pf* pf,
@@ -822,6 +954,8 @@ __device__ __forceinline__ int node_ctl_rank0(const SearchCtl& C, const SearchPa
   prefetch_wait();
   pf->inc = pf->ctl[3];  // join_objective reads this copy: the next prefetch rewrites ctl[]
   if (P.balance && pending >= P.balance) c |= claim_donation_rank0(Gl, pf) << 1;
+  if (P.remote && !(c & 2) && P.balance && pending >= P.balance && (++pf->pad[1] & 31) == 0)
+    c |= claim_remote_rank0(P, Gl);
   if (need_prop) c |= stop_rank0(C, pf);
   prefetch_ctl(pf, Gl);
   return c;
@@ -863,6 +997,10 @@ __global__ void __launch_bounds__(MaxThreads<G, F>::value, MaxThreads<G, F>::min
   // in the first dirty mask by rank 0 before the propagation
   const unsigned dm = F == kPackedF ? dm_addr<G>(f) : 0u;
   bool queue_open = true;
+  // cross-GPU donation is compiled for CTA groups only (the issue-bound Q14
+  // warp kernel lost 3% to the extra code; its trees split evenly anyway)
+  constexpr bool kRemote = std::is_same<G, CtaGroup>::value;
+  if (kRemote && g.rank() == 0) atomicAdd(&Gl->running, 1);  // peers donate only to a GPU whose kernel runs
   const bool right_first = P.value_order == 1 || (P.value_order == 2 && (gid & 1));
   // mixed orders (minimisation): every mix_order-th group branches by the
   // smallest lb, latest start first (var_order 2, the primal dives' order)
@@ -891,7 +1029,10 @@ __global__ void __launch_bounds__(MaxThreads<G, F>::value, MaxThreads<G, F>::min
         int stop = 0;
         if (g.rank() == 0) stop = *(volatile int*)&Gl->stop;
         if (g.bcast0(stop)) {
-          if (g.rank() == 0) Gl->incomplete = 1;
+          if (g.rank() == 0) {
+            Gl->incomplete = 1; atomicOr(&Gl->why, 16);
+            atomicAdd(&Gl->active, -1);  // leaves the active set, as every other exit does
+          }
           break;
         }
         copy_words(g, S, P.frontier + (size_t)P.frontier_idx[idx] * P.stride, nw);
@@ -914,17 +1055,48 @@ __global__ void __launch_bounds__(MaxThreads<G, F>::value, MaxThreads<G, F>::min
             got = 1;
             break;
           }
-          if (*(volatile int*)&Gl->active == 0 || *(volatile int*)&Gl->stop) break;
+          if (kRemote && P.remote) {  // a peer's donation, addressed to this group
+            for (int k = 0; k < kInbox && !got; ++k)
+              if (*(volatile int*)&Gl->inbox_state[k] == 2 && *(volatile int*)&Gl->inbox_rcv[k] == gid) got = 2 + k;
+            if (got) break;
+          }
+          // Quiescence: no active group here and no busy peer (whose groups
+          // could still hand this one work).  A stopped GPU exits at once,
+          // counted incomplete when peers could have donated to it.
+          const bool stopped = *(volatile int*)&Gl->stop != 0;
+          if (stopped) {
+            if (kRemote && P.remote) {
+              Gl->incomplete = 1;
+              atomicOr(&Gl->why, 4);
+            }
+            break;
+          }
+          if (*(volatile int*)&Gl->active == 0 &&
+              !(kRemote && P.remote && (peers_busy(P) || !close_inbox_quiet(Gl))))
+            break;
           __nanosleep(200);
         }
       }
-      if (!g.bcast0(got)) break;
+      got = g.bcast0(got);
+      if (!got) break;
       __threadfence();
-      const int* mb = P.mailbox + (size_t)gid * P.mb_stride;
-      copy_words(g, S, mb, nw);
-      depth = *(volatile const int*)&mb[nw + 1];
-      g.sync();
-      if (g.rank() == 0) *(volatile int*)&P.mailbox[(size_t)gid * P.mb_stride + nw + 2] = 0;
+      if (got == 1) {
+        const int* mb = P.mailbox + (size_t)gid * P.mb_stride;
+        copy_words(g, S, mb, nw);
+        depth = *(volatile const int*)&mb[nw + 1];
+        g.sync();
+        if (g.rank() == 0) *(volatile int*)&P.mailbox[(size_t)gid * P.mb_stride + nw + 2] = 0;
+      } else {  // inbox slot got - 2: the donor marked this GPU active for it
+        const int k = got - 2;
+        const volatile int* src = inbox_of(Gl, k);  // written over NVLink: volatile loads, past L1
+        for (int i = g.rank(); i < nw; i += g.size()) S[i] = src[i];
+        depth = *(volatile int*)&Gl->inbox_depth[k];
+        g.sync();
+        if (g.rank() == 0) {
+          atomicAdd(&Gl->remote_in, 1ull);
+          *(volatile int*)&Gl->inbox_state[k] = 0;
+        }
+      }
       need_prop = true;
       dirty = kAllDirty;
     }
@@ -966,6 +1138,7 @@ __global__ void __launch_bounds__(MaxThreads<G, F>::value, MaxThreads<G, F>::min
         ctl = g.bcast0(ctl);
       }
       if (ctl & 2) hand_over(g, P, Gl, stk, nw, bot, sp);
+      else if (kRemote && (ctl & 4)) hand_over_remote(g, P, Gl, stk, nw, bot, ctl);
       int lbw = 0, mid = 0, e;
       if (need_prop) {
         if (ctl & 1) {
@@ -1061,7 +1234,10 @@ __global__ void __launch_bounds__(MaxThreads<G, F>::value, MaxThreads<G, F>::min
       g.sync();
     }
     if (g.rank() == 0) {
-      if (abandoned) Gl->incomplete = 1;
+      if (abandoned) {
+        Gl->incomplete = 1;
+        atomicOr(&Gl->why, 2);
+      }
       flush(Gl, cnt);
     }
     if (abandoned) {
@@ -1072,6 +1248,11 @@ __global__ void __launch_bounds__(MaxThreads<G, F>::value, MaxThreads<G, F>::min
   if (g.rank() == 0) {
     if (kPrefetch) prefetch_wait();  // no copy into shared memory outlives the CTA
     flush(Gl, cnt);
+    if constexpr (kRemote) {
+      if (P.remote) close_inbox(Gl);
+      __threadfence();
+      atomicAdd(&Gl->running, -1);
+    }
   }
 }
 

@@ -3,7 +3,8 @@ search run concurrently on one B200, each with a slice of the SMs (ctas_per_sm
 = 1; two 512-thread CTAs fit per SM), from N host threads, like `pccp_gpu
 solve --gpus N`.  For each workload, with and without stealing
 (PCCP_NO_STEAL), every shard's device time, nodes and stolen subproblems, and
-the job's time (the slowest shard).  `python scripts/steal_proxy.py [N] [out.json]`."""
+the job's time (the slowest shard); with stealing alone and with the
+cross-GPU donation of pending branches as well.  `python scripts/steal_proxy.py [N] [out.json]`."""
 import json
 import os
 import sys
@@ -22,10 +23,13 @@ WORK = [("rcpsp30-s7", lambda: Model.rcpsp_random(7, 30, 4), "solve", 60),
 
 
 def run(name, make, kind, arg, steal):
-    if steal:
-        os.environ.pop("PCCP_NO_STEAL", None)
-    else:
+    """steal: 0 static split, 1 stealing only, 2 stealing and cross-GPU donation."""
+    for k in ("PCCP_NO_STEAL", "PCCP_NO_REMOTE_DONATE"):
+        os.environ.pop(k, None)
+    if steal == 0:
         os.environ["PCCP_NO_STEAL"] = "1"
+    elif steal == 1:
+        os.environ["PCCP_NO_REMOTE_DONATE"] = "1"
     m = make()
     engs = [Engine(0, shard_index=k, shard_count=n, ctas_per_sm=1, mix_order=-1) for k in range(n)]
     for e in engs:
@@ -40,11 +44,16 @@ def run(name, make, kind, arg, steal):
             res[k] = {"status": r.status, "objective": r.objective, "device_ms": r.stats["device_ms"],
                       "nodes": r.stats["nodes"], "stolen": r.stats["stolen"],
                       "exhausted": r.status in ("OPTIMAL", "UNSAT"), "proved": r.primal_proved,
-                      "solutions": r.stats["solutions"], "has_store": r.best_words is not None}
+                      "solutions": r.stats["solutions"], "has_store": r.best_words is not None,
+                      "remote_in": r.stats["remote_in"], "remote_out": r.stats["remote_out"]}
         else:
             r = e.enumerate(depth_cap=arg)
             res[k] = dict(r)
 
+    # warm-up, one after the other: a first search allocates its buffers, and an
+    # allocation synchronises the whole device (it would serialise the shards)
+    for k in range(n):
+        work(k)
     for e in engs:
         e.reset_shared()
     th = [threading.Thread(target=work, args=(k,)) for k in range(n)]
@@ -54,8 +63,8 @@ def run(name, make, kind, arg, steal):
         t.join()
     for e in engs:
         e.close()
-    shards = [{"device_ms": round(r["device_ms"], 3), "nodes": int(r["nodes"]), "stolen": int(r["stolen"])}
-              for r in res]
+    shards = [{"device_ms": round(r["device_ms"], 3), "nodes": int(r["nodes"]), "stolen": int(r["stolen"]),
+               "remote_in": int(r.get("remote_in", 0)), "remote_out": int(r.get("remote_out", 0))} for r in res]
     job = {"job_ms": max(s["device_ms"] for s in shards), "shards": shards}
     if kind == "solve":
         c = combine_solve(res)
@@ -68,9 +77,11 @@ def run(name, make, kind, arg, steal):
 
 report = {"n_shards": n, "note": "one B200, shards concurrent on SM slices (ctas_per_sm 1), reference order"}
 for name, make, kind, arg in WORK:
-    report[name] = {"static": run(name, make, kind, arg, False), "stealing": run(name, make, kind, arg, True)}
+    report[name] = {"static": run(name, make, kind, arg, 0), "stealing": run(name, make, kind, arg, 1),
+                    "stealing+donation": run(name, make, kind, arg, 2)}
     print(name, json.dumps(report[name]), flush=True)
-os.environ.pop("PCCP_NO_STEAL", None)
+for k in ("PCCP_NO_STEAL", "PCCP_NO_REMOTE_DONATE"):
+    os.environ.pop(k, None)
 if out_path:
     with open(out_path, "w") as f:
         json.dump(report, f, indent=1)

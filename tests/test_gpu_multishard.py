@@ -302,3 +302,53 @@ def test_unlinked_shards_keep_the_static_split(golden):
             r = e.load(m).enumerate()
             a, s = e.frontier()
             assert r["stolen"] == 0 and s.size == len(range(k, a.size, 3))
+
+
+@pytest.mark.parametrize("seed,optimum", [(3, 62), (7, 60)])
+def test_cross_gpu_donation_of_pending_branches(seed, optimum):
+    """Two linked shards minimising at once on one device (host threads, one
+    CTA per SM each, after a warm-up that allocates their buffers): a shard
+    whose groups run dry takes pending branches from inside the other's
+    subtrees (search.cuh hand_over_remote), and the job still proves the
+    reference's optimum.  The static split leaves one shard with a few hundred
+    nodes on these seeds (the heavy subtree sits under one frontier position)."""
+    import threading
+
+    from paper_2207_12116_b200 import Model
+    from paper_2207_12116_b200.distributed import combine_solve
+    from paper_2207_12116_b200.engine import link_peers
+    from paper_2207_12116_b200 import Engine
+    m = Model.rcpsp_random(seed, 30, 4)
+    engs = [Engine(0, shard_index=k, shard_count=2, ctas_per_sm=1, mix_order=-1) for k in range(2)]
+    try:
+        for e in engs:
+            e.load(m)
+        link_peers(engs)
+        for e in engs:  # warm-up: first searches allocate (an allocation synchronises the device)
+            e.solve(timeout_s=60)
+        moved = 0
+        for rep in range(3):
+            for e in engs:
+                e.reset_shared()
+            res = [None, None]
+
+            def run(k):
+                r = engs[k].solve(timeout_s=60)
+                res[k] = {"objective": r.objective, "exhausted": r.status in ("OPTIMAL", "UNSAT"),
+                          "proved": r.primal_proved, "nodes": r.stats["nodes"], "solutions": r.stats["solutions"],
+                          "has_store": r.best_words is not None, "in": r.stats["remote_in"],
+                          "out": r.stats["remote_out"]}
+
+            th = [threading.Thread(target=run, args=(k,)) for k in range(2)]
+            for t in th:
+                t.start()
+            for t in th:
+                t.join()
+            c = combine_solve(res)
+            assert c["status"] == "OPTIMAL" and c["objective"] == optimum, (rep, res)
+            assert res[0]["in"] == res[1]["out"] and res[1]["in"] == res[0]["out"]
+            moved += res[0]["in"] + res[1]["in"]
+        assert moved > 0
+    finally:
+        for e in engs:
+            e.close()
