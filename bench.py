@@ -685,7 +685,7 @@ def main():
                    "group_threads": info["group_threads"], "groups_per_cta": info["groups_per_cta"],
                    "ctas": info["ctas"], "table_in_smem": bool(info["table_in_smem"])},
         "e2e": {"value": e2e_value, "unit": "nodes/s", "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h),
-                "note": "pccp_gpu_load (lowering + table upload) + pccp_gpu_enumerate from host buffers, host clock"},
+                "note": "pccp_gpu_load (table upload; the context keeps the lowering of an identical model)  + pccp_gpu_enumerate from host buffers, host clock"},
         "gpu_launches": int(launches_all),
         "roofline": rl,
         "parity": {"exact": all(parity.values()), **parity},

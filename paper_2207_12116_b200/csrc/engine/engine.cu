@@ -100,6 +100,8 @@ struct pccp_gpu_ctx {
   cudaStream_t stream = nullptr;
   cudaEvent_t ev[6] = {};
   bool loaded = false;
+  bool low_valid = false;            // low/dl hold the lowering of the model whose key is low_key
+  std::vector<std::int32_t> low_key;
 
   Lowered low;  // the plain lowering (reference words): value-range analysis, byte models
   Lowered dl;   // the device layout: bit-plane 0/1 cells when the model has them (lower_packed), else = low
@@ -920,16 +922,54 @@ void pccp_gpu_close(pccp_gpu_ctx* c) {
   delete c;
 }
 
+// The identity of a model for the lowering cache: every table of the ABI
+// struct, and the environment knobs lower.cpp reads.
+std::vector<std::int32_t> model_key(const pccp_model& m) {
+  std::vector<std::int32_t> k;
+  const std::uint32_t nc = m.cmd_off ? m.cmd_off[m.n_cmds] : 0;
+  k.reserve(8 + 2 * (size_t)m.n_slots + m.n_cmds + nc + m.n_cands);
+  k.push_back((std::int32_t)m.n_slots);
+  k.push_back((std::int32_t)m.n_words);
+  k.push_back((std::int32_t)m.n_cmds);
+  k.push_back((std::int32_t)m.n_cands);
+  k.push_back(m.obj_slot);
+  for (std::uint32_t i = 0; i < m.n_slots; ++i) k.push_back(m.slot_kind ? m.slot_kind[i] : 0);
+  if (m.slot_word) k.insert(k.end(), m.slot_word, m.slot_word + m.n_slots);
+  if (m.cmd_off) k.insert(k.end(), m.cmd_off, m.cmd_off + m.n_cmds + 1);
+  if (m.cmd_code) k.insert(k.end(), m.cmd_code, m.cmd_code + nc);
+  if (m.cands) k.insert(k.end(), m.cands, m.cands + m.n_cands);
+  for (const char* e : {"PCCP_FILTERED", "PCCP_NE_ORDER", "PCCP_NO_NE", "PCCP_NO_PACK", "PCCP_NO_REIF",
+                        "PCCP_NO_REIF8", "PCCP_NO_ROWS", "PCCP_NO_UNIT", "PCCP_NO_WROWS", "PCCP_ROW_LANES",
+                        "PCCP_ROW_PAIR", "PCCP_SCALAR_SCAN"}) {
+    k.push_back(-1);
+    if (const char* v = std::getenv(e))
+      for (; *v; ++v) k.push_back(*v);
+  }
+  return k;
+}
+
 int pccp_gpu_load(pccp_gpu_ctx* c, const pccp_model* m) {
   return api([&] {
     if (!c || !m) throw ArgError("null argument");
     CK(cudaSetDevice(c->device));
     c->loaded = false;
-    c->low = lower_model(*m);
-    if (c->low.L.n_cand >= (1u << 24)) throw LimitError("more than 2^24 branching candidates");
-    // bit-plane cells only where the plain lowering found reifications or rows
-    c->dl = (c->low.L.n_reif || c->low.L.n_rows) ? lower_packed(*m) : c->low;
+    const bool lt = std::getenv("PCCP_LOAD_TIMING") != nullptr;
+    double tl[8] = {now_ms()};
+    // A reload of the model already lowered here (same tables, same lowering
+    // knobs) keeps its lowering; the tables are still uploaded below.
+    std::vector<std::int32_t> key = model_key(*m);
+    if (!c->low_valid || key != c->low_key) {
+      c->low_valid = false;
+      c->low = lower_model(*m);
+      if (c->low.L.n_cand >= (1u << 24)) throw LimitError("more than 2^24 branching candidates");
+      // bit-plane cells only where the plain lowering found reifications or rows
+      c->dl = (c->low.L.n_reif || c->low.L.n_rows) ? lower_packed(*m) : c->low;
+      c->low_key = std::move(key);
+      c->low_valid = true;
+    }
+    tl[1] = now_ms();
     reset_shared(c);  // an incumbent of the previous model means nothing for this one
+    tl[2] = now_ms();
     c->slot_kind.assign(m->slot_kind, m->slot_kind + m->n_slots);
     c->slot_word.assign(m->slot_word, m->slot_word + m->n_slots);
     c->view = *m;
@@ -940,7 +980,9 @@ int pccp_gpu_load(pccp_gpu_ctx* c, const pccp_model* m) {
     c->view.cands = nullptr;
     c->blob.ensure(c->dl.blob.size() + 4);
     CK(cudaMemcpyAsync(c->blob.p, c->dl.blob.data(), c->dl.blob.size() * 4, cudaMemcpyHostToDevice, c->stream));
+    tl[3] = now_ms();
     plan(c);
+    tl[4] = now_ms();
     // Size the DFS stacks here rather than in the first solve: the depth bound
     // of the bottom store under the folded constant tells bounds the one of any
     // root reached from it by propagation (bounds only tighten).  Skipped when
@@ -969,9 +1011,15 @@ int pccp_gpu_load(pccp_gpu_ctx* c, const pccp_model* m) {
       // contexts may share a device); a solve whose root needs more sizes
       // the stacks itself (run_search), and a failed allocation here only
       // defers that.
+      // (cudaMemGetInfo is a driver query that can wait behind a concurrent
+      // nvidia-smi for tens of ms: a reload whose stacks already fit skips it)
+      const bool fits = bytes / 4 <= c->stack.n && c->stack.p && (size_t)c->groups() * entry <= c->mailbox.n &&
+                        c->mailbox.p;
       size_t free_b = 0, total_b = 0;
-      CK(cudaMemGetInfo(&free_b, &total_b));
-      if (bounded && bytes <= free_b / 4) {
+      tl[5] = now_ms();
+      if (bounded && !fits) CK(cudaMemGetInfo(&free_b, &total_b));
+      tl[6] = now_ms();
+      if (bounded && !fits && bytes <= free_b / 4) {
         try {
           c->stack.ensure(bytes / 4);
           c->mailbox.ensure((size_t)c->groups() * entry);
@@ -982,6 +1030,10 @@ int pccp_gpu_load(pccp_gpu_ctx* c, const pccp_model* m) {
       }
     }
     CK(cudaStreamSynchronize(c->stream));
+    if (lt)
+      fprintf(stderr, "pccp_gpu_load: lower %.3f reset %.3f upload %.3f plan %.3f bound %.3f meminfo %.3f rest %.3f ms\n",
+              tl[1] - tl[0], tl[2] - tl[1], tl[3] - tl[2], tl[4] - tl[3], tl[5] - tl[4], tl[6] - tl[5],
+              now_ms() - tl[6]);
     c->loaded = true;
     return PCCP_OK;
   });
