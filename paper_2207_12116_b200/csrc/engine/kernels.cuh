@@ -745,8 +745,16 @@ __device__ bool eval_rows_fast(const G& g, unsigned sb, const Tab<TS>& tab, cons
         v[t] = t < n_my ? sld(sb + ((unsigned)tword(x[t]) << 2)) : 0;
       }
     }
+    // m: the largest coef - coef * lb of this lane's terms, so that no term's
+    // zeroing guard coef + s - coef * lb > c holds unless m + s > c: lanes
+    // (and, at run time, whole warps) skip the guard loop on quiet rows.
+    int m = 0;
 #pragma unroll
-    for (int t = 0; t < kRowTerms; ++t) s += tcoef(x[t]) * v[t];
+    for (int t = 0; t < kRowTerms; ++t) {
+      s += tcoef(x[t]) * v[t];
+      const int a = tcoef(x[t]) - tcoef(x[t]) * v[t];
+      m = t == 0 || a > m ? a : m;
+    }
     for (int o = R >> 1; o > 0; o >>= 1) s += __shfl_xor_sync(kFull, s, o, R);
     if (act) {
       const bool over = s > c;
@@ -756,7 +764,7 @@ __device__ bool eval_rows_fast(const G& g, unsigned sb, const Tab<TS>& tab, cons
         ch = 1u;
       }
       if (sub == 0 && (over || lsum_now == INT_MAX)) fl = true;  // the cell is (or becomes) top: failed
-      if (c != INT_MAX) {
+      if (c != INT_MAX && (over || (n_my > 0 && m + s > c))) {
 #pragma unroll
         for (int t = 0; t < kRowTerms; ++t) {
           const int coef = tcoef(x[t]);
@@ -1199,31 +1207,42 @@ __device__ __forceinline__ bool packed_round(const G& g, unsigned sb, const Tab<
     if (segs) {
       const int nwarps = g.warps(), wid = g.warp(), lane = g.rank() & 31;
       int turn = 0;  // the warp that takes the next chunk (the same sequence in every warp)
+      // Chunk j of a segment goes to warp (turn + j) mod nwarps: a warp visits
+      // only its own chunks, then every warp advances turn by the chunk count.
       auto seg = [&](int b, int e, bool indirect) {
-        for (int c0 = b; c0 < e; c0 += 32) {
-          const bool mine = turn == wid;
-          if (++turn == nwarps) turn = 0;
-          if (!mine) continue;
-          const int i = c0 + lane;
+        if (e <= b) return;
+        const int nc = (e - b + 31) >> 5;
+        int j = wid - turn;
+        if (j < 0) j += nwarps;
+        for (; j < nc; j += nwarps) {
+          const int i = b + 32 * j + lane;
           if (i < e) reif(indirect ? tab.ld1(L.r_xrec, i) : i);
         }
+        turn += nc;
+        if (turn >= nwarps) turn %= nwarps;
       };
-      for (unsigned w = 0; w < L.dm_s; ++w) {
-        for (unsigned bits = sldu(cs + 4u * w); bits; bits &= bits - 1u) {
-          const unsigned k = 32u * w + (unsigned)(__ffs((int)bits) - 1);
-          if (k >= L.r_ns) continue;
-          const int2 yr = tab.ld2(L.r_y, (int)k);
-          seg(yr.x, yr.y, false);
-          seg(tab.ld1(L.r_xoff, (int)k), tab.ld1(L.r_xoff, (int)k + 1), true);
+      // The marked bits of a mask of n words, in order: the lanes read 32 words
+      // at once and the warp walks the nonzero ones (a ballot), not every word.
+      auto walk = [&](unsigned m, unsigned n, auto&& fn) {
+        for (unsigned w0 = 0; w0 < n; w0 += 32) {
+          const unsigned val = w0 + (unsigned)lane < n ? sldu(m + 4u * (w0 + (unsigned)lane)) : 0u;
+          for (unsigned nz = __ballot_sync(kFull, val != 0u); nz; nz &= nz - 1u) {
+            const int k = __ffs((int)nz) - 1;
+            for (unsigned bits = __shfl_sync(kFull, val, k); bits; bits &= bits - 1u)
+              fn(32u * (w0 + (unsigned)k) + (unsigned)(__ffs((int)bits) - 1));
+          }
         }
-      }
-      for (unsigned w = 0; w < L.dm_p; ++w) {
-        for (unsigned bits = sldu(cp + 4u * w); bits; bits &= bits - 1u) {
-          const unsigned p = 32u * w + (unsigned)(__ffs((int)bits) - 1);
-          if (p >= L.n_pairs) continue;
-          seg(tab.ld1(L.r_p, (int)p), tab.ld1(L.r_p, (int)p + 1), false);
-        }
-      }
+      };
+      walk(cs, L.dm_s, [&](unsigned k) {
+        if (k >= L.r_ns) return;
+        const int2 yr = tab.ld2(L.r_y, (int)k);
+        seg(yr.x, yr.y, false);
+        seg(tab.ld1(L.r_xoff, (int)k), tab.ld1(L.r_xoff, (int)k + 1), true);
+      });
+      walk(cp, L.dm_p, [&](unsigned p) {
+        if (p >= L.n_pairs) return;
+        seg(tab.ld1(L.r_p, (int)p), tab.ld1(L.r_p, (int)p + 1), false);
+      });
     }
   }
   if (!segs) {
