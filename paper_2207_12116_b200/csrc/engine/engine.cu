@@ -538,14 +538,17 @@ void run_search(pccp_gpu_ctx* c, int mode, const int32_t* root_words, int depth_
   // tree node is still materialised exactly once across the GPUs.
   int count = rflag ? 1 : 0;
   int level = 0;
+  // two flag buffers of 2 cap bytes (k_decompose), 16-byte aligned for the
+  // small levels' word loads
+  const int fstride = (int)((2 * (size_t)cap + 15) / 16 * 16);
   if (count > 0) {
     c->fb.ensure(2 * (size_t)cap * stride);
     c->ib.ensure(2 * (size_t)cap);
     c->ia.ensure(2 * (size_t)cap);  // may reallocate: index 0 of the root frontier is rewritten
     CK(cudaMemcpyAsync(c->ia.p, &zero, 4, cudaMemcpyHostToDevice, c->stream));
-    c->flags.ensure(2 * (size_t)cap);
+    c->flags.ensure(2 * (size_t)fstride);
     c->dec.ensure(2);
-    c->chunk.ensure((size_t)c->dec_ctas + 2);
+    c->chunk.ensure((size_t)c->dec_ctas + 3);
   }
   CK(cudaEventRecord(c->ev[4], c->stream));
   dev::DecState* d_st = reinterpret_cast<dev::DecState*>(c->dec.p);
@@ -555,10 +558,10 @@ void run_search(pccp_gpu_ctx* c, int mode, const int32_t* root_words, int depth_
   auto expand_until = [&](int target) -> bool {
     if (count <= 0 || count >= target) return true;
     const int grid = c->dec_ctas;
-    c->chunk.ensure((size_t)grid + 2);
+    c->chunk.ensure((size_t)grid + 3);
     const dev::DecState st0{count, level};
     CK(cudaMemcpyAsync(c->dec.p, &st0, sizeof(st0), cudaMemcpyHostToDevice, c->stream));
-    CK(cudaMemsetAsync(c->chunk.p + grid, 0, 2 * sizeof(int), c->stream));  // grid barrier words
+    CK(cudaMemsetAsync(c->chunk.p + grid, 0, 3 * sizeof(int), c->stream));  // grid barrier words, stop snapshot
     int* fb0 = c->fa.p;
     int* fb1 = c->fb.p;
     int* ib0 = c->ia.p;
@@ -566,7 +569,7 @@ void run_search(pccp_gpu_ctx* c, int mode, const int32_t* root_words, int depth_
     unsigned char* flags = c->flags.p;
     int* chunk_count = c->chunk.p;
     unsigned* bar = reinterpret_cast<unsigned*>(c->chunk.p + grid);
-    int tgt = target, strd = stride;
+    int tgt = target, strd = stride, fstr = fstride;
     const bool dbg = std::getenv("PCCP_DEBUG_DEC") != nullptr;
     DBuf<unsigned long long> profbuf;
     unsigned long long* prof = nullptr;
@@ -580,7 +583,8 @@ void run_search(pccp_gpu_ctx* c, int mode, const int32_t* root_words, int depth_
       CK(cudaMemcpyToSymbolAsync(dev::g_dbg_round, &tr, sizeof(tr), 0, cudaMemcpyHostToDevice, c->stream));
     }
     void* args[] = {(void*)&M, (void*)&C, (void*)&fb0, (void*)&fb1, (void*)&ib0, (void*)&ib1, (void*)&d_st,
-                    (void*)&tgt, (void*)&strd, (void*)&flags, (void*)&chunk_count, (void*)&bar, (void*)&prof};
+                    (void*)&tgt, (void*)&strd, (void*)&flags, (void*)&fstr, (void*)&chunk_count, (void*)&bar,
+                    (void*)&prof};
     const int level0 = level;
     CK(cudaLaunchCooperativeKernel((const void*)dev::k_decompose<Gp, TS, F>, dim3(grid), dim3(c->block), args,
                                    c->smem, c->stream));

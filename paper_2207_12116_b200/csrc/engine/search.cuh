@@ -465,6 +465,88 @@ __device__ __forceinline__ void grid_sync(unsigned* bar) {
   __syncthreads();
 }
 
+// grid_sync that also snapshots *stop: the last CTA to arrive copies it into
+// bar[2] before releasing the others, so every CTA reads the same value (a
+// stop raised by the next level's expansion cannot reach a CTA that is still
+// deciding whether to run it).  bar[2] is rewritten only at the next barrier,
+// which no CTA reaches before every CTA has read it.
+__device__ __forceinline__ int grid_sync_snap(unsigned* bar, const int* stop) {
+  __shared__ int snap;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    const unsigned gen = *(volatile unsigned*)&bar[1];
+    __threadfence();
+    if (atomicAdd(&bar[0], 1u) == gridDim.x - 1) {
+      __threadfence();
+      *(volatile int*)&bar[2] = *(volatile const int*)stop;
+      *(volatile unsigned*)&bar[0] = 0;
+      __threadfence();
+      atomicAdd(&bar[1], 1u);
+    } else {
+      while (*(volatile unsigned*)&bar[1] == gen) __nanosleep(32);
+    }
+    __threadfence();
+    snap = *(volatile int*)&bar[2];
+  }
+  __syncthreads();
+  return snap;
+}
+
+// Compaction of a small level (n <= 32 x blockDim flags) without a grid
+// barrier: every CTA scans all n flags itself (thread t: flags [32t, 32t+32),
+// two 16-byte loads past L1) and writes the index entries its own groups
+// will read next, positions p with (p / per_cta) mod gridDim.x == blockIdx.x,
+// so the CTAs together write all of them.  Returns the total on every thread.
+__device__ __forceinline__ int small_compact(const unsigned char* flags, int n, int* idx, int per_cta) {
+  __shared__ int wtot[33];
+  const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5, nw = (int)(blockDim.x >> 5);
+  const int lo = 32 * tid;
+  unsigned bits = 0;
+  if (lo < n) {
+    // two independent 16-byte loads through L2 (ld.global.cg: past this SM's
+    // L1, which may hold a previous level's flags), issued together
+    const uint4* w = reinterpret_cast<const uint4*>(flags + lo);
+    const uint4 a = __ldcg(w), b = lo + 16 < n ? __ldcg(w + 1) : make_uint4(0u, 0u, 0u, 0u);
+    const unsigned v[8] = {a.x, a.y, a.z, a.w, b.x, b.y, b.z, b.w};
+#pragma unroll
+    for (int k = 0; k < 8; ++k)  // bytes are 0 or 1
+      bits |= ((v[k] & 1u) | ((v[k] >> 7) & 2u) | ((v[k] >> 14) & 4u) | ((v[k] >> 21) & 8u)) << (4 * k);
+    if (n - lo < 32) bits &= (1u << (n - lo)) - 1u;  // bytes past n are a previous level's
+  }
+  const int c = __popc(bits);
+  int incl = c;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const int u = __shfl_up_sync(kFull, incl, o);
+    if (lane >= o) incl += u;
+  }
+  if (lane == 31) wtot[wid] = incl;
+  __syncthreads();
+  int before = 0, total = 0;
+  for (int k = 0; k < nw; ++k) {
+    const int t = wtot[k];
+    before += k < wid ? t : 0;
+    total += t;
+  }
+  // this thread's positions p0, p0 + 1, ... in set-bit order: only the owned
+  // ones (q = p / per_cta = blockIdx.x + m gridDim.x, windows of per_cta
+  // positions per_cta gridDim.x apart) are written
+  if (c) {
+    const int p0 = before + incl - c, G = (int)gridDim.x;
+    int q = p0 / per_cta;
+    int r = ((int)blockIdx.x - q) % G;
+    q += r < 0 ? r + G : r;
+    int ws = q * per_cta;  // the next owned window [ws, ws + per_cta)
+    int p = p0;
+    for (unsigned b = bits; b; b &= b - 1u, ++p) {
+      if (p >= ws + per_cta) ws += G * per_cta;
+      if (p >= ws) idx[p] = lo + __ffs((int)b) - 1;
+    }
+  }
+  __syncthreads();  // the groups of this CTA read idx next; wtot is reused by the next call
+  return total;
+}
+
 // Both children of every parent of one level (one group per parent).
 __device__ unsigned long long* g_dbg_tl = nullptr;  // PCCP_DEBUG_TIMELINE: CTA 0's last parent
 __device__ __forceinline__ void dbg_mark(int k) {
@@ -620,34 +702,43 @@ __device__ int grid_compact(const unsigned char* flags, int n, int* idx, int* ch
 template <class G, bool TS, int F>
 __global__ void __launch_bounds__(MaxThreads<G, F>::value, MaxThreads<G, F>::min_blocks)
     k_decompose(Model M, SearchCtl C, int* fb0, int* fb1, int* ib0, int* ib1, DecState* st, int target, int stride,
-                unsigned char* flags, int* chunk_count, unsigned* bar, unsigned long long* prof) {
+                unsigned char* flags, int fstride, int* chunk_count, unsigned* bar, unsigned long long* prof) {
   const Frame f = frame(M);
   const G g = GroupOf<G>::make(f);
   const Tab<TS> tab = make_tab<TS>(f);
   volatile int* S = f.stores + GroupOf<G>::in_cta() * M.store_stride;
   const unsigned sb = init_store(g, S, M.L);
   Cnt& cnt = f.cnt[GroupOf<G>::in_cta()];
-  int* FB[2] = {fb0, fb1};
-  int* IB[2] = {ib0, ib1};
   int count = *(volatile int*)&st->count;
   int levels = *(volatile int*)&st->levels;
+  // no kernel writes stop before the first level: the same value everywhere
+  bool err = *(volatile int*)&C.G->stop == 2;
   for (int k = 0;; ++k) {
-    if (count <= 0 || count >= target || *(volatile int*)&C.G->stop == 2) break;  // uniform across the grid
-    const int src = k & 1, dst = src ^ 1;
+    if (count <= 0 || count >= target || err) break;  // uniform across the grid
+    // ping-pong by selects, not a two-element array (a dynamic index puts it on the stack)
+    int* const fsrc = (k & 1) ? fb1 : fb0;
+    int* const fdst = (k & 1) ? fb0 : fb1;
+    int* const isrc = (k & 1) ? ib1 : ib0;
+    int* const idst = (k & 1) ? ib0 : ib1;
+    // flags alternate between two buffers: a CTA may expand level k+1 while
+    // another still scans level k's flags (small levels have no second barrier)
+    unsigned char* fl = flags + (size_t)(k & 1) * (size_t)fstride;
     const bool rec = prof && blockIdx.x == 0 && threadIdx.x == 0 && k < 60;  // PCCP_DEBUG_DEC timeline
     if (rec) prof[4 * k] = globaltimer();
-    expand_level<G, TS, F>(g, S, sb, tab, f, M.L, C, cnt, FB[src], IB[src], count, stride, levels + 1, FB[dst],
-                           flags);
-    grid_sync(bar);
+    expand_level<G, TS, F>(g, S, sb, tab, f, M.L, C, cnt, fsrc, isrc, count, stride, levels + 1, fdst,
+                           fl);
+    err = grid_sync_snap(bar, &C.G->stop) == 2;
     if (rec) prof[4 * k + 1] = globaltimer();
-    count = grid_compact(flags, 2 * count, IB[dst], chunk_count, bar);
+    const bool small = 2 * count <= 32 * (int)blockDim.x;
+    count = small ? small_compact(fl, 2 * count, idst, GroupOf<G>::per_cta())
+                  : grid_compact(fl, 2 * count, idst, chunk_count, bar);
     if (rec) prof[4 * k + 2] = globaltimer();
     ++levels;
     if (blockIdx.x == 0 && threadIdx.x == 0) {
       st->count = count;
       st->levels = levels;
     }
-    grid_sync(bar);  // every CTA has read the chunk counts and agrees on `count`
+    if (!small) grid_sync(bar);  // every CTA has read the chunk counts and agrees on `count`
     if (rec) prof[4 * k + 3] = globaltimer();
   }
   if (g.rank() == 0) flush(C.G, cnt);
