@@ -495,8 +495,8 @@ __device__ __forceinline__ int grid_sync_snap(unsigned* bar, const int* stop) {
 // Compaction of a small level (n <= 32 x blockDim flags) without a grid
 // barrier: every CTA scans all n flags itself (thread t: flags [32t, 32t+32),
 // two 16-byte loads past L1) and writes the index entries its own groups
-// will read next, positions p with (p / per_cta) mod gridDim.x == blockIdx.x,
-// so the CTAs together write all of them.  Returns the total on every thread.
+// will read next (see expand_level's assignment below), so the CTAs together
+// write all of them.  Returns the total on every thread.
 __device__ __forceinline__ int small_compact(const unsigned char* flags, int n, int* idx, int per_cta) {
   __shared__ int wtot[33];
   const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5, nw = (int)(blockDim.x >> 5);
@@ -528,19 +528,26 @@ __device__ __forceinline__ int small_compact(const unsigned char* flags, int n, 
     before += k < wid ? t : 0;
     total += t;
   }
-  // this thread's positions p0, p0 + 1, ... in set-bit order: only the owned
-  // ones (q = p / per_cta = blockIdx.x + m gridDim.x, windows of per_cta
-  // positions per_cta gridDim.x apart) are written
+  // this thread's positions p0, p0 + 1, ... in set-bit order: only the ones
+  // this CTA's groups read next are written.  expand_level hands parent p to
+  // group p mod ng, or, when the next level splits (2 total <= ng), its two
+  // children to groups 2p and 2p + 1.
   if (c) {
-    const int p0 = before + incl - c, G = (int)gridDim.x;
-    int q = p0 / per_cta;
-    int r = ((int)blockIdx.x - q) % G;
-    q += r < 0 ? r + G : r;
-    int ws = q * per_cta;  // the next owned window [ws, ws + per_cta)
+    const int p0 = before + incl - c, G = (int)gridDim.x, B = (int)blockIdx.x;
     int p = p0;
-    for (unsigned b = bits; b; b &= b - 1u, ++p) {
-      if (p >= ws + per_cta) ws += G * per_cta;
-      if (p >= ws) idx[p] = lo + __ffs((int)b) - 1;
+    if (2 * total <= G * per_cta) {  // items [B per_cta, (B+1) per_cta) hold 2p or 2p+1 for p in [plo, phi]
+      const int plo = (B * per_cta) >> 1, phi = ((B + 1) * per_cta - 1) >> 1;
+      for (unsigned b = bits; b; b &= b - 1u, ++p)
+        if (p >= plo && p <= phi) idx[p] = lo + __ffs((int)b) - 1;
+    } else {
+      int q = p0 / per_cta;
+      int r = (B - q) % G;
+      q += r < 0 ? r + G : r;
+      int ws = q * per_cta;  // the next owned window [ws, ws + per_cta): q = blockIdx.x + m gridDim.x
+      for (unsigned b = bits; b; b &= b - 1u, ++p) {
+        if (p >= ws + per_cta) ws += G * per_cta;
+        if (p >= ws) idx[p] = lo + __ffs((int)b) - 1;
+      }
     }
   }
   __syncthreads();  // the groups of this CTA read idx next; wtot is reused by the next call
@@ -562,11 +569,18 @@ __device__ void expand_level(const G& g, volatile int* S, unsigned sb, const Tab
                              unsigned char* flags) {
   const int gid = blockIdx.x * GroupOf<G>::per_cta() + GroupOf<G>::in_cta();
   const int ng = gridDim.x * GroupOf<G>::per_cta();
-  for (int p = gid; p < n_par; p += ng) {
-    if (time_stop(g, C, 2)) {  // abandoned parent: its subtree is unexplored
+  // A level with fewer parents than half the groups gives each child its own
+  // group (both read the parent and take the same decision), so the two
+  // children of a parent propagate side by side instead of one after the other.
+  const bool split = 2 * n_par <= ng;
+  const int n_items = split ? 2 * n_par : n_par;
+  for (int j = gid; j < n_items; j += ng) {
+    const int p = split ? j >> 1 : j;
+    const int side0 = split ? (j & 1) : 0, side1 = split ? (j & 1) : 1;
+    if (time_stop(g, C, (unsigned)(side1 - side0 + 1))) {  // abandoned: the subtree is unexplored
       if (g.rank() == 0) {
         C.G->incomplete = 1; atomicOr(&C.G->why, 1);
-        flags[2 * p] = flags[2 * p + 1] = 0;
+        for (int side = side0; side <= side1; ++side) flags[2 * p + side] = 0;
       }
       g.sync();
       continue;
@@ -580,10 +594,10 @@ __device__ void expand_level(const G& g, volatile int* S, unsigned sb, const Tab
     const int b = branch(g, S, f.T, L, lbw, mid);
     g.sync();  // every thread has read S before rank 0 joins the decision
     dbg_mark(2);
-    for (int side = 0; side < 2; ++side) {
+    for (int side = side0; side <= side1; ++side) {
       unsigned char keep = 0;
       if (b == 1) {
-        if (side == 1) {
+        if (side != side0) {
           copy_words(g, S, par, (int)L.n_words);
           g.sync();
         }
