@@ -714,7 +714,7 @@ __device__ __forceinline__ bool eval_small(volatile int* S, const int* __restric
 // tighten, so a snapshot already at 0 stays there), and a due join proves a
 // change this round, issued return-free like eval_ne_fast's.
 constexpr int kRowTerms = 8;
-template <class G, bool TS, bool Pair>
+template <class G, bool TS, bool Pair, int T = kRowTerms>
 __device__ bool eval_rows_fast(const G& g, unsigned sb, const Tab<TS>& tab, const DeviceLayout& L, bool& fl) {
   const int R = (int)L.row_lanes, lg = (int)L.row_lg;  // R = 2^lg: shifts, not divisions (CSP: 10% of instructions)
   const int sub = g.rank() & (R - 1);
@@ -727,16 +727,16 @@ __device__ bool eval_rows_fast(const G& g, unsigned sb, const Tab<TS>& tab, cons
     const int row = base + my;
     const bool act = row < n_rows;
     int s = 0;
-    int x[kRowTerms], v[kRowTerms], u[kRowTerms];
+    int x[T], v[T], u[T];
     const int4 meta = act ? tab.ld4(off_meta, row) : make_int4(0, 0, INT_MAX, 0);  // {beg, end, c, lsum}
     const int j0 = meta.x + sub, end = meta.y, c = meta.z;
     const unsigned alsum = sb + ((unsigned)meta.w << 2);
-    const int n_my = end > j0 ? (end - j0 + R - 1) >> lg : 0;  // this lane's terms (<= kRowTerms)
+    const int n_my = end > j0 ? (end - j0 + R - 1) >> lg : 0;  // this lane's terms (<= T)
 #pragma unroll
-    for (int t = 0; t < kRowTerms; ++t) x[t] = t < n_my ? tab.ld1(off_terms, j0 + t * R) : 0;
+    for (int t = 0; t < T; ++t) x[t] = t < n_my ? tab.ld1(off_terms, j0 + t * R) : 0;
     const int lsum_now = act && sub == 0 ? sld(alsum) : INT_MAX;  // snapshot for the lsum join
 #pragma unroll
-    for (int t = 0; t < kRowTerms; ++t) {
+    for (int t = 0; t < T; ++t) {
       if constexpr (Pair) {
         const int2 p = t < n_my ? sld2(sb + ((unsigned)tword(x[t]) << 2)) : make_int2(0, 0);
         v[t] = p.x;
@@ -750,7 +750,7 @@ __device__ bool eval_rows_fast(const G& g, unsigned sb, const Tab<TS>& tab, cons
     // (and, at run time, whole warps) skip the guard loop on quiet rows.
     int m = 0;
 #pragma unroll
-    for (int t = 0; t < kRowTerms; ++t) {
+    for (int t = 0; t < T; ++t) {
       s += tcoef(x[t]) * v[t];
       const int a = tcoef(x[t]) - tcoef(x[t]) * v[t];
       m = t == 0 || a > m ? a : m;
@@ -766,7 +766,7 @@ __device__ bool eval_rows_fast(const G& g, unsigned sb, const Tab<TS>& tab, cons
       if (sub == 0 && (over || lsum_now == INT_MAX)) fl = true;  // the cell is (or becomes) top: failed
       if (c != INT_MAX && (over || (n_my > 0 && m + s > c))) {
 #pragma unroll
-        for (int t = 0; t < kRowTerms; ++t) {
+        for (int t = 0; t < T; ++t) {
           const int coef = tcoef(x[t]);
           if (t < n_my && (over || coef + s - coef * v[t] > c)) {
             const unsigned a = sb + ((unsigned)tword(x[t]) << 2);
@@ -795,8 +795,12 @@ __device__ bool eval_rows_fast(const G& g, unsigned sb, const Tab<TS>& tab, cons
 // failure the scalar scan would find (skipped when every scalar is a row's cell).
 template <class G, bool TS>
 __device__ bool eval_rows(const G& g, unsigned sb, const Tab<TS>& tab, const DeviceLayout& L, bool& fl) {
-  if (L.rows_fast)
-    return L.row_even ? eval_rows_fast<G, TS, true>(g, sb, tab, L, fl) : eval_rows_fast<G, TS, false>(g, sb, tab, L, fl);
+  if (L.rows_fast) {
+    if (L.row_even) return eval_rows_fast<G, TS, true>(g, sb, tab, L, fl);
+    // short rows (random CSP: <= 5 terms per lane): 5 unrolled term slots, not 8
+    if (L.row_tl <= 5) return eval_rows_fast<G, TS, false, 5>(g, sb, tab, L, fl);
+    return eval_rows_fast<G, TS, false>(g, sb, tab, L, fl);
+  }
   const int R = (int)L.row_lanes, lg = (int)L.row_lg;
   const int sub = g.rank() & (R - 1);
   const int per_pass = g.size() >> lg;

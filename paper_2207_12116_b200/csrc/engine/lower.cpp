@@ -1074,6 +1074,7 @@ Lowered lower_impl(const pccp_model& m, bool want_bits) {
   }
   L.row_lg = 0;
   while ((1u << L.row_lg) < L.row_lanes) ++L.row_lg;
+  L.row_tl = (max_terms + L.row_lanes - 1) / L.row_lanes;
   L.row_off = reserve_arr(L.n_rows + 1);
   L.row_lsum = reserve_arr(L.n_rows);
   L.row_c = reserve_arr(L.n_rows);

@@ -57,6 +57,7 @@ struct DeviceLayout {
   std::uint32_t row_meta;  // int4 per row: {first term, end, c, lsum word}
   std::uint32_t n_rows, n_row_terms, row_lanes;  // lanes per row (power of two <= 32)
   std::uint32_t row_lg;                           // log2 row_lanes
+  std::uint32_t row_tl;                           // the most terms one lane reads (ceil(max terms / row_lanes))
   std::uint32_t row_even;                         // every row term's lb word is even: (lb, ub) is one 8-byte load
   std::uint32_t gen_off;                          // offsets into gen_code
   std::uint32_t gen_code;
