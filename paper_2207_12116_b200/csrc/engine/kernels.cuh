@@ -1222,8 +1222,8 @@ __device__ __forceinline__ bool packed_round(const G& g, unsigned sb, const Tab<
           const int i = b + 32 * j + lane;
           if (i < e) reif(indirect ? tab.ld1(L.r_xrec, i) : i);
         }
-        turn += nc;
-        if (turn >= nwarps) turn %= nwarps;
+        turn += nc;  // a few chunks per segment: subtract rather than divide
+        while (turn >= nwarps) turn -= nwarps;
       };
       // The marked bits of a mask of n words, in order: the lanes read 32 words
       // at once and the warp walks the nonzero ones (a ballot), not every word.
