@@ -200,7 +200,8 @@ TTO_OPTIMA = {1: 84, 2: 77, 5: 73, 7: 60, 9: 61, 11: 99}
 
 def time_to_optimum(local, rank, world, dist):
     """Config 4 (RCPSP 30x4): optimum, time to the first optimal incumbent and
-    time to the proof on the GPU(s).  With N > 1 the incumbent is shared
+    time to the proof on the GPU(s) (at N = 1 the median of three solves, all
+    three listed).  With N > 1 the incumbent is shared
     through CUDA IPC + system-scope atomicMin (paper_2207_12116_b200/distributed.py)."""
     from paper_2207_12116_b200 import Engine, Model
     from paper_2207_12116_b200.distributed import attach_incumbents, run_solve
@@ -220,9 +221,14 @@ def time_to_optimum(local, rank, world, dist):
             status, obj, ok = res["status"], res["objective"], res.get("checked")
             local_r = res["local"]
         else:
-            r = eng.solve(timeout_s=120)
+            # three solves: the search order (and so the node count) depends on
+            # incumbent timing; the median run by time to proof is reported
+            runs = [eng.solve(timeout_s=120) for _ in range(3)]
+            assert len({(x.status, x.objective) for x in runs}) == 1, [(x.status, x.objective) for x in runs]
+            runs.sort(key=lambda x: x.stats["device_ms"])
+            r = runs[1]
             status, obj = r.status, r.objective
-            ok = r.best_words is not None and m.check_solution(r.best_words)
+            ok = all(x.best_words is not None and m.check_solution(x.best_words) for x in runs)
             local_r = r
         t_first = min((ms for v, ms in local_r.improvements if v == obj), default=float("inf"))
         t_proof = local_r.stats["device_ms"]
@@ -237,6 +243,8 @@ def time_to_optimum(local, rank, world, dist):
                           "nodes": local_r.stats["nodes"],
                           "tree_nodes": local_r.stats["nodes"] - local_r.stats["rematerialised"],
                           "roofline": roofline(st, eng.lowering_info(), sm_mhz)}
+        if world == 1:
+            out[str(seed)]["t_proof_ms_runs"] = [x.stats["device_ms"] for x in runs]
         if ref is not None:
             rr = ref.load(m).solve(timeout_s=120)
             out[str(seed)]["reference_order"] = {
