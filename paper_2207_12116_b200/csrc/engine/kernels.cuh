@@ -1127,19 +1127,22 @@ __device__ __forceinline__ bool eval_other_families(const G& g, volatile int* S,
       for (int i = g.rank(); i < (int)L.n_reif; i += g.size()) ch |= eval_reif<false>(sb, tab.ld4(L.reif, i));
     }
     dbg_r(0);
+    // unit records from the last warp down: the rows' last, partial pass
+    // falls on the first warps, so the two remainders land on different warps
+    const int ru = (g.size() - 32 * (g.rank() >> 5) - 32) + (g.rank() & 31);
     if (L.unit_fast) {
       unsigned uch = 0;
       const int2 none = make_int2(0, INT_MAX);  // S[0] - S[0] <= INT_MAX: no second guard
-      for (int i = g.rank(); i < (int)L.n_unit1; i += g.size()) eval_unit_fast(sb, tab.ld4(L.unit1, i), none, uch);
-      for (int i = g.rank(); i < (int)L.n_unit2; i += g.size())
+      for (int i = ru; i < (int)L.n_unit1; i += g.size()) eval_unit_fast(sb, tab.ld4(L.unit1, i), none, uch);
+      for (int i = ru; i < (int)L.n_unit2; i += g.size())
         eval_unit_fast(sb, tab.ld4(L.unit2, i), tab.ld2(L.unit2g, i), uch);
       ch |= uch != 0;
     } else {
-      for (int i = g.rank(); i < (int)L.n_unit1; i += g.size()) {
+      for (int i = ru; i < (int)L.n_unit1; i += g.size()) {
         const int4 q = tab.ld4(L.unit1, i);
         if (unit_guard(sb, q.x, q.y)) ch |= unit_tell(sb, q.z, q.w);
       }
-      for (int i = g.rank(); i < (int)L.n_unit2; i += g.size()) {
+      for (int i = ru; i < (int)L.n_unit2; i += g.size()) {
         const int4 q = tab.ld4(L.unit2, i);
         if (unit_guard(sb, q.x, q.y)) {
           const int2 q2 = tab.ld2(L.unit2g, i);
