@@ -554,7 +554,8 @@ __device__ __forceinline__ int small_compact(const unsigned char* flags, int n, 
   return total;
 }
 
-// Both children of every parent of one level (one group per parent).
+// Both children of every parent of one level (one group per parent, or one
+// per child on small levels).
 __device__ unsigned long long* g_dbg_tl = nullptr;  // PCCP_DEBUG_TIMELINE: CTA 0's last parent
 __device__ __forceinline__ void dbg_mark(int k) {
 #ifdef PCCP_DEBUG_TIMELINE
