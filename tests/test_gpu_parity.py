@@ -437,3 +437,27 @@ def test_interleaved_scalar_cells(seed, hengine):
     res = hengine.load(m).enumerate(depth_cap=24)
     for k in ("nodes", "failures", "solutions", "open_leaves", "hash_sum"):
         assert res[k] == g[k], k
+
+
+@pytest.mark.parametrize("group_threads,groups_per_cta,ctas_per_sm,eps_factor", [
+    (32, 3, 0, 0),    # warp groups, 3 per CTA: ownership windows of a non-power-of-two width
+    (32, 8, 1, 64),   # one CTA per SM, a deep frontier: small levels, then chunked ones
+    (128, 0, 0, 4),   # CTA groups with a decomposition (one group per CTA)
+    (256, 0, 1, 1),   # CTA groups, a frontier of one node per group
+])
+def test_decomposition_shapes_enumerate_exactly(group_threads, groups_per_cta, ctas_per_sm, eps_factor, golden):
+    """The EPS decomposition's barrier-free small levels (every CTA compacting
+    the flags itself, children on their own groups) and its chunked large
+    levels, under grid shapes the defaults do not use: Q10 and the CSP at
+    depth 12 must give the golden counts and hash-sums."""
+    from paper_2207_12116_b200 import Engine
+    with Engine(0, hash=True, group_threads=group_threads, groups_per_cta=groups_per_cta, ctas_per_sm=ctas_per_sm,
+                eps_factor=eps_factor) as e:
+        g = golden["nqueens10"]["enumerate"]
+        res = e.load(build("nqueens10")).enumerate()
+        for k in ("nodes", "failures", "solutions", "hash_sum"):
+            assert res[k] == g[k], (k, res[k], g[k])
+        g = golden["csp1"]["enumerate_d12"]
+        res = e.load(build("csp1")).enumerate(depth_cap=12)
+        for k in ("nodes", "failures", "solutions", "open_leaves", "hash_sum"):
+            assert res[k] == g[k], (k, res[k], g[k])
